@@ -1,0 +1,202 @@
+/*
+ * cve_b200.h -- C ABI of the B200 (sm_100a) chaotic video cipher engine.
+ *
+ * Drop-in boundary.  The first block of entry points has exactly the names,
+ * argument meaning, status codes and error behaviour of the reference's
+ * hot-path C ABI (reference: /root/reference/proj/include/cve.h); each
+ * declaration cites the line it replaces.  A program written against the
+ * reference's cipher-handle API compiles and links against libcve_b200.so
+ * unchanged.  The second block is additive: batched,
+ * pipelined and device-resident variants the synchronous per-frame call
+ * cannot express.
+ *
+ * Only PLCM keys (tag 0x00, 66 hex chars) drive the GPU engine.  LASM keys
+ * validate (cve_key_validate) but cve_cipher_create rejects them with
+ * CVE_ERROR_INVALID_ARGUMENT: the LASM map needs a glibc-exact device sin
+ * and is out of this round's scope.
+ *
+ * Threading matches the reference (cve.h:5-6): one handle is driven by one
+ * thread at a time; distinct handles are independent.  All calls are
+ * synchronous unless the name ends in _async.
+ */
+#ifndef CVE_B200_H
+#define CVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define CVE_B200_API __attribute__((visibility("default")))
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status values are numerically identical to the reference (cve.h:24-32). */
+typedef enum cve_status {
+  CVE_OK = 0,
+  CVE_ERROR_INVALID_ARGUMENT = 1,
+  CVE_ERROR_BAD_KEY = 2,
+  CVE_ERROR_IO = 3,
+  CVE_ERROR_BAD_FORMAT = 4,
+  CVE_ERROR_MISMATCH = 5,
+  CVE_ERROR_INTERNAL = 6 /* also: CUDA failure, no usable sm_100 device */
+} cve_status;
+
+typedef enum cve_map_kind { CVE_MAP_PLCM = 0, CVE_MAP_LASM = 1 } cve_map_kind;
+
+typedef struct cve_cipher cve_cipher;
+
+/* ---- reference hot-path subset ------------------------------------------ */
+
+/* replaces cve.h:39.  Returns the engine version string. */
+CVE_B200_API const char* cve_version(void);
+
+/* replaces cve.h:42.  Never NULL, for any value. */
+CVE_B200_API const char* cve_status_message(cve_status status);
+
+/* replaces cve.h:45.  Thread-local detail of the last failure ("" if none). */
+CVE_B200_API const char* cve_last_error(void);
+
+/* replaces cve.h:47.  Frees strings this library returned; NULL is a no-op. */
+CVE_B200_API void cve_string_free(char* s);
+
+/* replaces cve.h:53-54.  Fresh key from OS entropy; PLCM needs cap >= 67,
+ * LASM >= 51. */
+CVE_B200_API cve_status cve_key_generate(cve_map_kind kind, char* hex_out,
+                                         size_t hex_cap);
+
+/* replaces cve.h:57-58.  kind_out may be NULL. */
+CVE_B200_API cve_status cve_key_validate(const char* key_hex,
+                                         cve_map_kind* kind_out);
+
+/* replaces cve.h:67-69.  workers = subframe (row band) count n, a cipher
+ * parameter; rounds in 1..255.  `parallel` is accepted for ABI compatibility
+ * and ignored: output is bit-identical to the reference either way. */
+CVE_B200_API cve_status cve_cipher_create(const char* key_hex,
+                                          uint32_t workers, uint32_t rounds,
+                                          int parallel, cve_cipher** out);
+
+/* replaces cve.h:70.  NULL is a no-op. */
+CVE_B200_API void cve_cipher_destroy(cve_cipher* cipher);
+
+/* replaces cve.h:75-76 / 77-78.  In place on a side*side*3 interleaved RGB24
+ * host buffer.  The k-th encrypt OR decrypt call on a handle binds to frame
+ * index k.  NULL/0 arguments -> INVALID_ARGUMENT with no seed drawn; a side
+ * not divisible by workers -> MISMATCH after the frame's seed was drawn
+ * (reference engine.cpp:293-296, 189-196). */
+CVE_B200_API cve_status cve_cipher_encrypt_frame(cve_cipher* cipher,
+                                                 uint8_t* pixels,
+                                                 uint32_t side);
+CVE_B200_API cve_status cve_cipher_decrypt_frame(cve_cipher* cipher,
+                                                 uint8_t* pixels,
+                                                 uint32_t side);
+
+/* replaces cve.h:81-82. */
+CVE_B200_API cve_status cve_cipher_seeds_drawn(const cve_cipher* cipher,
+                                               uint64_t* out);
+
+/* ---- additive: batched / device-resident / introspection ---------------- */
+
+/* `count` consecutive square frames, contiguous in host memory
+ * (count*side*side*3 bytes), processed in place as frames k..k+count-1 of
+ * the handle.  H2D copy, keystream generation, cipher rounds and D2H copy
+ * overlap across frames.  Pinned (cudaHostAlloc'd / registered) buffers are
+ * copied by DMA asynchronously; pageable buffers work too but each copy then
+ * goes through the driver's staging and blocks the host.  Same validation as the per-frame call; on MISMATCH one seed is
+ * drawn (as the first of `count` per-frame calls would) and no data is
+ * touched.  count == 0 is INVALID_ARGUMENT. */
+CVE_B200_API cve_status cve_cipher_encrypt_frames(cve_cipher* cipher,
+                                                  uint8_t* pixels,
+                                                  uint32_t side,
+                                                  uint32_t count);
+CVE_B200_API cve_status cve_cipher_decrypt_frames(cve_cipher* cipher,
+                                                  uint8_t* pixels,
+                                                  uint32_t side,
+                                                  uint32_t count);
+
+/* Same, on frames already resident in device memory of the handle's GPU.
+ * Work is ordered after everything previously enqueued on `stream`
+ * (a cudaStream_t, or NULL for the legacy default stream), and `stream` is
+ * made to wait for its completion before the call returns -- the call itself
+ * does not block the host.  `d_pixels` must stay valid until `stream`
+ * reaches that point. */
+CVE_B200_API cve_status cve_cipher_encrypt_frames_async(cve_cipher* cipher,
+                                                        uint8_t* d_pixels,
+                                                        uint32_t side,
+                                                        uint32_t count,
+                                                        void* stream);
+CVE_B200_API cve_status cve_cipher_decrypt_frames_async(cve_cipher* cipher,
+                                                        uint8_t* d_pixels,
+                                                        uint32_t side,
+                                                        uint32_t count,
+                                                        void* stream);
+
+/* Blocks until every operation of the handle has finished. */
+CVE_B200_API cve_status cve_cipher_synchronize(cve_cipher* cipher);
+
+/* Selects the CUDA device used by handles created afterwards on this thread
+ * (default: the current device). */
+CVE_B200_API cve_status cve_set_device(int device);
+
+/* Copies the next `len` keystream bytes of subframe generator `worker` to
+ * host memory WITHOUT consuming them from the cipher's stream (diagnostics /
+ * parity; the reference's per-worker Prbg output, chaos.cpp:143-153). */
+CVE_B200_API cve_status cve_cipher_peek_keystream(cve_cipher* cipher,
+                                                  uint32_t worker,
+                                                  uint8_t* out, size_t len);
+
+/* Runs the keystream generator ahead so that the next `bytes` bytes per
+ * worker (beyond the current stream position) are produced before the
+ * frames that will consume them arrive.  Does not consume them.
+ * Asynchronous on the handle's streams. */
+CVE_B200_API cve_status cve_cipher_prefetch_keystream(cve_cipher* cipher,
+                                                      uint64_t bytes);
+
+/* Profiling counters of the handle (cumulative since create). */
+typedef struct cve_cipher_stats {
+  uint64_t frames;           /* frames completed (encrypt + decrypt) */
+  uint64_t keystream_iters;  /* PLCM iterations generated per lane */
+  uint64_t kernel_launches;  /* CUDA kernels launched by this handle */
+  uint64_t prbg_launches;    /* of which keystream-generator launches */
+  uint64_t guard_replays;    /* 8-iteration blocks replayed exactly */
+  double prbg_ms;            /* device time of generator launches */
+  double cipher_ms;          /* device time of cipher-round launches */
+} cve_cipher_stats;
+
+/* Fills *out.  Device times are read back from CUDA events and therefore
+ * synchronize the handle. */
+CVE_B200_API cve_status cve_cipher_get_stats(cve_cipher* cipher,
+                                             cve_cipher_stats* out);
+
+/* Keystream of one generator with explicit lanes {x0_a, p_a, x0_b, p_b},
+ * computed by the GPU generator kernel: the reference's
+ * Prbg(PlcmParams, PlcmParams).take(len) (chaos.cpp:79-91, 143-153).  Raw
+ * generator bytes for external statistical suites (reference nist-export,
+ * capi.cpp:385-415) and for parity tests.  Out-of-domain lanes -> BAD_KEY. */
+CVE_B200_API cve_status cve_keystream_generate(const double lanes[4],
+                                               uint8_t* out, size_t len);
+
+/* Host-only keying (no GPU needed): the lane table the key's coordinator
+ * derives for `workers` subframes -- lanes_out[4*i .. 4*i+3] = x0_a, p_a,
+ * x0_b, p_b of subframe i (reference keying.cpp:180-207) -- followed by the
+ * first `nseeds` per-frame confusion seeds (keying.cpp:209-218).  PLCM keys
+ * only.  For key management and diagnostics; the cipher handle does the same
+ * derivation internally. */
+CVE_B200_API cve_status cve_derive_worker_lanes(const char* key_hex,
+                                                uint32_t workers,
+                                                double* lanes_out,
+                                                uint32_t* seeds_out,
+                                                size_t nseeds);
+
+/* Device times (ms) of the keystream-generator launches since the previous
+ * call, oldest first; *count receives the number available, at most `cap`
+ * are copied to `out` (which may be NULL to query).  Synchronizes. */
+CVE_B200_API cve_status cve_cipher_take_prbg_times(cve_cipher* cipher,
+                                                   float* out, size_t cap,
+                                                   size_t* count);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* CVE_B200_H */

@@ -1,0 +1,280 @@
+"""B200-native chaotic video cipher (arXiv 2302.07411) -- Python host mirror.
+
+The product is ``libcve_b200.so`` (C ABI declared in ``include/cve_b200.h``):
+host C++ keying + sm_100a CUDA kernels.  This module is a thin ctypes binding
+that mirrors the reference's cipher-handle interface
+(``/root/reference/proj/include/cve.h:60-82``) with the same names, argument
+meaning and error behaviour, so tests read like the reference's test_capi.cpp.
+
+There is no CPU fallback: if the shared library is missing, importing the
+binding raises; if no B200 is present, ``Cipher(...)`` raises ``CveError``
+with status ``CVE_ERROR_INTERNAL``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+__all__ = [
+    "CveError", "Cipher", "lib", "lib_path", "key_validate", "key_generate",
+    "derive_worker_lanes", "padded_side", "pad_to_square", "crop_to_original",
+    "CVE_OK", "CVE_ERROR_INVALID_ARGUMENT", "CVE_ERROR_BAD_KEY",
+    "CVE_ERROR_MISMATCH", "CVE_ERROR_INTERNAL", "CVE_MAP_PLCM", "CVE_MAP_LASM",
+]
+
+CVE_OK = 0
+CVE_ERROR_INVALID_ARGUMENT = 1
+CVE_ERROR_BAD_KEY = 2
+CVE_ERROR_IO = 3
+CVE_ERROR_BAD_FORMAT = 4
+CVE_ERROR_MISMATCH = 5
+CVE_ERROR_INTERNAL = 6
+CVE_MAP_PLCM = 0
+CVE_MAP_LASM = 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libcve_b200.so")
+
+
+class CveError(RuntimeError):
+    """A non-OK cve_status, with the library's thread-local detail string."""
+
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.detail = detail
+        super().__init__(f"cve status {status}: {detail}")
+
+
+class Stats(C.Structure):
+    _fields_ = [("frames", C.c_uint64), ("keystream_iters", C.c_uint64),
+                ("kernel_launches", C.c_uint64), ("prbg_launches", C.c_uint64),
+                ("guard_replays", C.c_uint64), ("prbg_ms", C.c_double),
+                ("cipher_ms", C.c_double)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(lib_path):
+        raise ImportError(
+            f"{lib_path} is not built; run `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (there is no CPU fallback)")
+    L = C.CDLL(lib_path)
+    u8p, vp = C.POINTER(C.c_uint8), C.c_void_p
+    sig = {
+        "cve_version": (C.c_char_p, []),
+        "cve_status_message": (C.c_char_p, [C.c_int]),
+        "cve_last_error": (C.c_char_p, []),
+        "cve_string_free": (None, [vp]),
+        "cve_key_generate": (C.c_int, [C.c_int, C.c_char_p, C.c_size_t]),
+        "cve_key_validate": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
+        "cve_cipher_create": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_int,
+                                        C.POINTER(vp)]),
+        "cve_cipher_destroy": (None, [vp]),
+        "cve_cipher_encrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
+        "cve_cipher_decrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
+        "cve_cipher_seeds_drawn": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "cve_cipher_encrypt_frames": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32]),
+        "cve_cipher_decrypt_frames": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32]),
+        "cve_cipher_encrypt_frames_async": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, vp]),
+        "cve_cipher_decrypt_frames_async": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, vp]),
+        "cve_cipher_synchronize": (C.c_int, [vp]),
+        "cve_set_device": (C.c_int, [C.c_int]),
+        "cve_cipher_peek_keystream": (C.c_int, [vp, C.c_uint32, vp, C.c_size_t]),
+        "cve_cipher_prefetch_keystream": (C.c_int, [vp, C.c_uint64]),
+        "cve_cipher_get_stats": (C.c_int, [vp, C.POINTER(Stats)]),
+        "cve_cipher_take_prbg_times": (C.c_int, [vp, C.POINTER(C.c_float), C.c_size_t,
+                                                 C.POINTER(C.c_size_t)]),
+        "cve_keystream_generate": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
+        "cve_derive_worker_lanes": (C.c_int, [C.c_char_p, C.c_uint32,
+                                              C.POINTER(C.c_double),
+                                              C.POINTER(C.c_uint32), C.c_size_t]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    del u8p
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int) -> None:
+    if status != CVE_OK:
+        raise CveError(status, lib.cve_last_error().decode(errors="replace"))
+
+
+def _as_key(key) -> bytes:
+    return key.encode() if isinstance(key, str) else bytes(key)
+
+
+def key_validate(key_hex) -> int:
+    """Returns the map kind (CVE_MAP_PLCM / CVE_MAP_LASM); raises on a bad key."""
+    kind = C.c_int(-1)
+    _check(lib.cve_key_validate(_as_key(key_hex), C.byref(kind)))
+    return kind.value
+
+
+def key_generate(kind: int = CVE_MAP_PLCM) -> str:
+    buf = C.create_string_buffer(80)
+    _check(lib.cve_key_generate(kind, buf, len(buf)))
+    return buf.value.decode()
+
+
+def derive_worker_lanes(key_hex, workers: int, seeds: int = 0
+                        ) -> Tuple[np.ndarray, np.ndarray]:
+    """Host keying only (no GPU): the (workers, 4) lane table
+    (x0_a, p_a, x0_b, p_b) the coordinator derives, then `seeds` confusion
+    seeds (reference keying.cpp:164-218)."""
+    lanes = np.zeros((workers, 4), dtype=np.float64)
+    out = np.zeros(max(seeds, 1), dtype=np.uint32)
+    _check(lib.cve_derive_worker_lanes(
+        _as_key(key_hex), workers, lanes.ctypes.data_as(C.POINTER(C.c_double)),
+        out.ctypes.data_as(C.POINTER(C.c_uint32)), seeds))
+    return lanes, out[:seeds]
+
+
+def keystream_generate(lanes, length: int) -> np.ndarray:
+    """GPU keystream of one generator with explicit lanes (x0_a, p_a, x0_b, p_b)."""
+    lan = (C.c_double * 4)(*[float(v) for v in lanes])
+    out = np.zeros(length, dtype=np.uint8)
+    _check(lib.cve_keystream_generate(lan, out.ctypes.data, length))
+    return out
+
+
+# ---- frame model (reference frame.cpp:19-51) --------------------------------
+
+def padded_side(width: int, height: int, workers: int) -> int:
+    if width == 0 or height == 0 or workers == 0:
+        raise CveError(CVE_ERROR_INVALID_ARGUMENT, "dimensions and workers must be >= 1")
+    m = max(width, height)
+    return (m + workers - 1) // workers * workers
+
+
+def pad_to_square(rgb: np.ndarray, workers: int) -> np.ndarray:
+    """(h, w, 3) uint8 -> (side, side, 3), zero rows bottom / columns right."""
+    h, w = rgb.shape[:2]
+    side = padded_side(w, h, workers)
+    out = np.zeros((side, side, 3), dtype=np.uint8)
+    out[:h, :w] = rgb
+    return out
+
+
+def crop_to_original(frame: np.ndarray, width: int, height: int) -> np.ndarray:
+    if width > frame.shape[1] or height > frame.shape[0]:
+        raise CveError(CVE_ERROR_INVALID_ARGUMENT, "original dimensions exceed the frame side")
+    return np.ascontiguousarray(frame[:height, :width])
+
+
+# ---- the cipher handle --------------------------------------------------------
+
+class Cipher:
+    """One streaming cipher handle (reference cve_cipher, cve.h:62-82).
+
+    The k-th encrypt or decrypt call binds to frame index k of the clip.
+    """
+
+    def __init__(self, key_hex, workers: int, rounds: int = 5, parallel: bool = True):
+        h = C.c_void_p()
+        _check(lib.cve_cipher_create(_as_key(key_hex), workers, rounds,
+                                     1 if parallel else 0, C.byref(h)))
+        self._h = h
+        self.workers = workers
+        self.rounds = rounds
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "cipher is closed")
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            lib.cve_cipher_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @staticmethod
+    def _frames(buf: np.ndarray) -> Tuple[int, int]:
+        if buf.dtype != np.uint8 or not buf.flags.c_contiguous:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "need a C-contiguous uint8 array")
+        if buf.ndim == 3:
+            count, side = 1, buf.shape[0]
+        elif buf.ndim == 4:
+            count, side = buf.shape[0], buf.shape[1]
+        else:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "need (side,side,3) or (n,side,side,3)")
+        if buf.shape[-3:] != (side, side, 3):
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "frames must be square RGB24")
+        return count, side
+
+    def encrypt_frame(self, frame: np.ndarray) -> None:
+        """In place, like cve_cipher_encrypt_frame."""
+        _, side = self._frames(frame)
+        _check(lib.cve_cipher_encrypt_frame(self.handle, frame.ctypes.data, side))
+
+    def decrypt_frame(self, frame: np.ndarray) -> None:
+        _, side = self._frames(frame)
+        _check(lib.cve_cipher_decrypt_frame(self.handle, frame.ctypes.data, side))
+
+    def encrypt_frames(self, frames: np.ndarray) -> None:
+        count, side = self._frames(frames)
+        _check(lib.cve_cipher_encrypt_frames(self.handle, frames.ctypes.data, side, count))
+
+    def decrypt_frames(self, frames: np.ndarray) -> None:
+        count, side = self._frames(frames)
+        _check(lib.cve_cipher_decrypt_frames(self.handle, frames.ctypes.data, side, count))
+
+    def encrypt_frames_device(self, ptr: int, side: int, count: int, stream: int = 0) -> None:
+        """Frames resident in device memory (e.g. torch.Tensor.data_ptr())."""
+        _check(lib.cve_cipher_encrypt_frames_async(self.handle, C.c_void_p(ptr), side,
+                                                   count, C.c_void_p(stream)))
+
+    def decrypt_frames_device(self, ptr: int, side: int, count: int, stream: int = 0) -> None:
+        _check(lib.cve_cipher_decrypt_frames_async(self.handle, C.c_void_p(ptr), side,
+                                                   count, C.c_void_p(stream)))
+
+    def synchronize(self) -> None:
+        _check(lib.cve_cipher_synchronize(self.handle))
+
+    @property
+    def seeds_drawn(self) -> int:
+        v = C.c_uint64()
+        _check(lib.cve_cipher_seeds_drawn(self.handle, C.byref(v)))
+        return v.value
+
+    def peek_keystream(self, worker: int, length: int) -> np.ndarray:
+        out = np.zeros(length, dtype=np.uint8)
+        _check(lib.cve_cipher_peek_keystream(self.handle, worker, out.ctypes.data, length))
+        return out
+
+    def prefetch_keystream(self, nbytes: int) -> None:
+        _check(lib.cve_cipher_prefetch_keystream(self.handle, nbytes))
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib.cve_cipher_get_stats(self.handle, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def take_prbg_times(self, cap: int = 1 << 20) -> np.ndarray:
+        """Device times (ms) of keystream-generator launches since last call."""
+        out = np.zeros(cap, dtype=np.float32)
+        n = C.c_size_t()
+        _check(lib.cve_cipher_take_prbg_times(
+            self.handle, out.ctypes.data_as(C.POINTER(C.c_float)), cap, C.byref(n)))
+        return out[:min(n.value, cap)].copy()
+
+
+def set_device(device: int) -> None:
+    _check(lib.cve_set_device(device))
+

@@ -1,0 +1,290 @@
+// C ABI of libcve_b200.so (include/cve_b200.h).
+//
+// Status mapping and argument-check order follow the reference C ABI
+// (capi.cpp:36-67 `guarded`, 166-181 `run_frame`, 187-260 exports): argument
+// errors are reported before any seed is drawn; exceptions map to
+// cve_status; the detail string is thread-local and only set on failure.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/cve_b200.h"
+#include "engine.hpp"
+#include "keying.hpp"
+
+struct cve_cipher {
+  std::unique_ptr<cveb::Engine> engine;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_device = -1;
+
+template <typename Fn>
+cve_status guarded(Fn&& fn) {
+  try {
+    fn();
+    return CVE_OK;
+  } catch (const cveb::Error& e) {
+    g_last_error = e.what();
+    return static_cast<cve_status>(e.code);
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return CVE_ERROR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CVE_ERROR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown failure";
+    return CVE_ERROR_INTERNAL;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) cveb::raise(cveb::Errc::invalid_argument, what);
+}
+
+// Runs the handle's work on its own device, restoring the caller's.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess)
+      cveb::raise(cveb::Errc::internal, "cannot select the handle's CUDA device");
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+cve_status run_frames(cve_cipher* c, uint8_t* px, uint32_t side,
+                      uint32_t count, bool decrypt) {
+  return guarded([&] {
+    require(c != nullptr, "cipher is null");
+    require(px != nullptr, "pixels is null");
+    require(side != 0, "side must be >= 1");
+    require(count != 0, "count must be >= 1");
+    DeviceScope scope(c->engine->device());
+    c->engine->run_host(px, side, count, decrypt);
+  });
+}
+
+cve_status run_frames_async(cve_cipher* c, uint8_t* d_px, uint32_t side,
+                            uint32_t count, void* stream, bool decrypt) {
+  return guarded([&] {
+    require(c != nullptr, "cipher is null");
+    require(d_px != nullptr, "pixels is null");
+    require(side != 0, "side must be >= 1");
+    require(count != 0, "count must be >= 1");
+    DeviceScope scope(c->engine->device());
+    c->engine->run_device(d_px, side, count, decrypt,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cve_version(void) { return "1.0.0-b200"; }
+
+const char* cve_status_message(cve_status status) {
+  switch (status) {
+    case CVE_OK:
+      return "ok";
+    case CVE_ERROR_INVALID_ARGUMENT:
+      return "invalid argument";
+    case CVE_ERROR_BAD_KEY:
+      return "malformed or out-of-domain key";
+    case CVE_ERROR_IO:
+      return "file i/o failure";
+    case CVE_ERROR_BAD_FORMAT:
+      return "unrecognized or corrupt input format";
+    case CVE_ERROR_MISMATCH:
+      return "parameters do not match the input";
+    case CVE_ERROR_INTERNAL:
+      return "internal failure";
+  }
+  return "unknown status";
+}
+
+const char* cve_last_error(void) { return g_last_error.c_str(); }
+
+void cve_string_free(char* s) { std::free(s); }
+
+cve_status cve_key_generate(cve_map_kind kind, char* hex_out, size_t hex_cap) {
+  return guarded([&] {
+    require(hex_out != nullptr, "hex_out is null");
+    require(kind == CVE_MAP_PLCM || kind == CVE_MAP_LASM, "unknown map kind");
+    const std::string hex =
+        cveb::key_hex(cveb::fresh_key(static_cast<cveb::MapKind>(kind)));
+    require(hex_cap >= hex.size() + 1, "key buffer too small");
+    std::memcpy(hex_out, hex.c_str(), hex.size() + 1);
+  });
+}
+
+cve_status cve_key_validate(const char* key_hex, cve_map_kind* kind_out) {
+  return guarded([&] {
+    require(key_hex != nullptr, "key_hex is null");
+    const cveb::Key k = cveb::parse_key(key_hex);
+    if (kind_out) *kind_out = static_cast<cve_map_kind>(k.kind);
+  });
+}
+
+cve_status cve_cipher_create(const char* key_hex, uint32_t workers,
+                             uint32_t rounds, int parallel, cve_cipher** out) {
+  (void)parallel;  // scheduling-only in the reference (cve.h:64-66)
+  return guarded([&] {
+    require(out != nullptr, "out is null");
+    require(key_hex != nullptr, "key_hex is null");
+    const cveb::Key key = cveb::parse_key(key_hex);
+    int dev = g_device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    auto c = std::make_unique<cve_cipher>();
+    c->engine = std::make_unique<cveb::Engine>(key, workers, rounds, dev);
+    *out = c.release();
+  });
+}
+
+void cve_cipher_destroy(cve_cipher* cipher) { delete cipher; }
+
+cve_status cve_cipher_encrypt_frame(cve_cipher* cipher, uint8_t* pixels,
+                                    uint32_t side) {
+  return run_frames(cipher, pixels, side, 1, false);
+}
+
+cve_status cve_cipher_decrypt_frame(cve_cipher* cipher, uint8_t* pixels,
+                                    uint32_t side) {
+  return run_frames(cipher, pixels, side, 1, true);
+}
+
+cve_status cve_cipher_seeds_drawn(const cve_cipher* cipher, uint64_t* out) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(out != nullptr, "out is null");
+    *out = cipher->engine->seeds_drawn();
+  });
+}
+
+cve_status cve_cipher_encrypt_frames(cve_cipher* cipher, uint8_t* pixels,
+                                     uint32_t side, uint32_t count) {
+  return run_frames(cipher, pixels, side, count, false);
+}
+
+cve_status cve_cipher_decrypt_frames(cve_cipher* cipher, uint8_t* pixels,
+                                     uint32_t side, uint32_t count) {
+  return run_frames(cipher, pixels, side, count, true);
+}
+
+cve_status cve_cipher_encrypt_frames_async(cve_cipher* cipher,
+                                           uint8_t* d_pixels, uint32_t side,
+                                           uint32_t count, void* stream) {
+  return run_frames_async(cipher, d_pixels, side, count, stream, false);
+}
+
+cve_status cve_cipher_decrypt_frames_async(cve_cipher* cipher,
+                                           uint8_t* d_pixels, uint32_t side,
+                                           uint32_t count, void* stream) {
+  return run_frames_async(cipher, d_pixels, side, count, stream, true);
+}
+
+cve_status cve_cipher_synchronize(cve_cipher* cipher) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    DeviceScope scope(cipher->engine->device());
+    cipher->engine->synchronize();
+  });
+}
+
+cve_status cve_set_device(int device) {
+  return guarded([&] {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      cveb::raise(cveb::Errc::internal, "no CUDA device");
+    require(device >= 0 && device < count, "device index out of range");
+    g_device = device;
+  });
+}
+
+cve_status cve_cipher_peek_keystream(cve_cipher* cipher, uint32_t worker,
+                                     uint8_t* out, size_t len) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(out != nullptr || len == 0, "out is null");
+    DeviceScope scope(cipher->engine->device());
+    cipher->engine->peek(worker, out, len);
+  });
+}
+
+cve_status cve_cipher_prefetch_keystream(cve_cipher* cipher, uint64_t bytes) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    DeviceScope scope(cipher->engine->device());
+    cipher->engine->prefetch(bytes);
+  });
+}
+
+cve_status cve_cipher_get_stats(cve_cipher* cipher, cve_cipher_stats* out) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(out != nullptr, "out is null");
+    DeviceScope scope(cipher->engine->device());
+    const cveb::EngineStats s = cipher->engine->stats();
+    out->frames = s.frames;
+    out->keystream_iters = s.keystream_iters;
+    out->kernel_launches = s.kernel_launches;
+    out->prbg_launches = s.prbg_launches;
+    out->guard_replays = s.guard_replays;
+    out->prbg_ms = s.prbg_ms;
+    out->cipher_ms = s.cipher_ms;
+  });
+}
+
+cve_status cve_keystream_generate(const double lanes[4], uint8_t* out,
+                                  size_t len) {
+  return guarded([&] {
+    require(lanes != nullptr, "lanes is null");
+    require(out != nullptr || len == 0, "out is null");
+    cveb::standalone_stream(cveb::Lane{lanes[0], lanes[1]},
+                            cveb::Lane{lanes[2], lanes[3]}, out, len);
+  });
+}
+
+cve_status cve_derive_worker_lanes(const char* key_hex, uint32_t workers,
+                                   double* lanes_out, uint32_t* seeds_out,
+                                   size_t nseeds) {
+  return guarded([&] {
+    require(key_hex != nullptr, "key_hex is null");
+    require(workers != 0, "workers must be >= 1");
+    require(lanes_out != nullptr, "lanes_out is null");
+    require(seeds_out != nullptr || nseeds == 0, "seeds_out is null");
+    cveb::Coordinator coord(cveb::parse_key(key_hex));
+    const std::vector<cveb::WorkerLanes> w = coord.derive_workers(workers);
+    for (uint32_t i = 0; i < workers; ++i) {
+      lanes_out[4 * i + 0] = w[i].a.x0;
+      lanes_out[4 * i + 1] = w[i].a.p;
+      lanes_out[4 * i + 2] = w[i].b.x0;
+      lanes_out[4 * i + 3] = w[i].b.p;
+    }
+    for (size_t k = 0; k < nseeds; ++k) seeds_out[k] = coord.next_seed();
+  });
+}
+
+cve_status cve_cipher_take_prbg_times(cve_cipher* cipher, float* out,
+                                      size_t cap, size_t* count) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(count != nullptr, "count is null");
+    DeviceScope scope(cipher->engine->device());
+    const std::vector<float> t = cipher->engine->take_prbg_times();
+    *count = t.size();
+    if (out) std::memcpy(out, t.data(), sizeof(float) * std::min(cap, t.size()));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,571 @@
+// K2/K3/K4: confusion + diffusion round kernels for sm_100a.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   confusion   confuse_rows            src/engine.cpp:32-47   (scatter form)
+//               inverse_confuse_rows    src/engine.cpp:49-64
+//   diffusion   diffuse_region          src/engine.cpp:66-73, engine.hpp:32-34
+//               seed byte s_d           src/engine.cpp:237
+//   inverse     inverse_diffuse_region  src/engine.cpp:75-83, engine.hpp:36-38
+//               head fix-up             src/engine.cpp:271-276
+//   shift table build_shift_table       src/engine.cpp:14-30
+//
+// Restated for the GPU (probe P1):
+//   confusion as a GATHER: y[al][be] = x[(al-o) mod w][o], o = (be-shift[al]) mod w.
+//     Destination rows [al0, al0+R) read, from EVERY source row a, the
+//     contiguous run o in [al0-a, al0-a+R) -- a diagonal stripe.
+//   diffusion as an XOR PREFIX SCAN: with t_j = b_j ^ ((y_j + b_j) mod 256),
+//     c_j = s_d ^ t_0 ^ ... ^ t_j   over the bytes of one row band.
+//   inverse diffusion is elementwise: d_j = ((b_j ^ c_j ^ c_{j-1}) - b_j),
+//     the band head using the next band's recovered last byte.
+//
+// Data layout in HBM: frames are the reference's square row-major
+// interleaved RGB24 buffers; band i = bytes [i*region, (i+1)*region).
+// Keystream: one ring per worker, stream byte s at ring[i*R + s % R]; the
+// bytes of round k of a frame start at the frame's stream position + k*region
+// (engine.cpp:198-205, 227-230).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "kernels.hpp"
+#include "keying.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace cveb {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr uint32_t kEncThreads = 512;
+constexpr uint32_t kDecThreads = 512;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+// floor(n / d) for 32-bit n, d via one 64x64 high multiply.
+struct FastDiv {
+  uint32_t d;
+  uint64_t m;  // floor((2^64-1)/d) + 1, or 0 when d == 1
+};
+
+FastDiv make_div(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.m = d == 1 ? 0 : (~uint64_t(0)) / d + 1;
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.d == 1 ? n : uint32_t(__umul64hi(uint64_t(n), f.m));
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Byte lanes of a word: (y + b) mod 256 without cross-byte carries.
+__device__ __forceinline__ uint32_t add_bytes(uint32_t y, uint32_t b) {
+  return ((y & 0x7F7F7F7Fu) + (b & 0x7F7F7F7Fu)) ^ ((y ^ b) & 0x80808080u);
+}
+
+// t = b ^ (y + b) on 8 bytes, then inclusive XOR prefix across the bytes
+// (byte k of the result = t_0 ^ ... ^ t_k, little-endian byte order).
+__device__ __forceinline__ uint64_t t_prefix8(uint32_t y0, uint32_t y1,
+                                              uint32_t b0, uint32_t b1) {
+  const uint64_t t = uint64_t(b0 ^ add_bytes(y0, b0)) |
+                     (uint64_t(b1 ^ add_bytes(y1, b1)) << 32);
+  uint64_t s = t ^ (t << 8);
+  s ^= s << 16;
+  s ^= s << 32;
+  return s;
+}
+
+constexpr uint64_t kBcast = 0x0101010101010101ull;
+
+// Exclusive XOR scan of one byte per thread across the CTA.  `wsum` holds
+// 2 x 32 words (double-buffered by `phase` so one barrier per call suffices).
+__device__ __forceinline__ uint32_t block_xor_scan(uint32_t v, uint32_t* wsum,
+                                                   uint32_t phase,
+                                                   uint32_t& total) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nwarps = blockDim.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(kFull, inc, d);
+    if (lane >= uint32_t(d)) inc ^= u;
+  }
+  uint32_t* ws = wsum + 32 * (phase & 1);
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  uint32_t wprefix = 0, tot = 0;
+  // every warp scans the (<=32) warp totals redundantly: no second barrier
+  const uint32_t w = lane < nwarps ? ws[lane] : 0u;
+  uint32_t winc = w;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(kFull, winc, d);
+    if (lane >= uint32_t(d)) winc ^= u;
+  }
+  wprefix = __shfl_sync(kFull, winc ^ w, warp);  // exclusive for this warp
+  tot = __shfl_sync(kFull, winc, 31);
+  total = tot;
+  return wprefix ^ inc ^ v;
+}
+
+// ---------------------------------------------------------------------------
+// K4: per-frame shift table.
+__global__ void k_shift(const double* __restrict__ sine, uint32_t seed,
+                        int32_t* __restrict__ shift, uint32_t side) {
+  const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= side) return;
+  const double v = __dmul_rn(double(seed), sine[a]);
+  const long long s = (long long)floor(v);
+  long long r = s % (long long)side;
+  if (r < 0) r += side;
+  shift[a] = int32_t(r);
+}
+
+// ---------------------------------------------------------------------------
+// K2: fused forward round.  One CTA per (band, chunk of chunk_rows rows);
+// the h chunks of a band form one thread-block cluster and exchange their
+// XOR aggregates through distributed shared memory.
+struct EncArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  const uint8_t* ring;
+  uint64_t ring_bytes;
+  uint64_t pos;
+  const int32_t* shift;
+  uint32_t side, n, rows, chunk_rows, h;
+  uint64_t region;
+  FastDiv div_cr;
+};
+
+__device__ __forceinline__ uint8_t seed_byte(const EncArgs& a, uint32_t band) {
+  // s_d = post-confusion byte ((band+1) mod n + 1)*region - 1: pixel
+  // (last row of the next band, column side-1), channel 2.
+  const uint32_t nb = band + 1 == a.n ? 0 : band + 1;
+  const uint32_t al = nb * a.rows + a.rows - 1;
+  int o = int(a.side - 1) - a.shift[al];
+  if (o < 0) o += a.side;
+  int sr = int(al) - o;
+  if (sr < 0) sr += a.side;
+  return a.src[(uint64_t(sr) * a.side + uint32_t(o)) * 3 + 2];
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kEncThreads)
+    k_encrypt_round(const EncArgs a) {
+  extern __shared__ uint4 smem[];
+  __shared__ uint32_t wsum[64];
+  __shared__ uint32_t agg_share;
+  __shared__ uint32_t prefix_share;
+
+  uint8_t* ys = reinterpret_cast<uint8_t*>(smem);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t band = blockIdx.x / a.h;
+  const uint32_t chunk = blockIdx.x - band * a.h;
+  const uint32_t cr = a.chunk_rows, side = a.side;
+  const uint32_t al0 = band * a.rows + chunk * cr;
+  const uint32_t cb = cr * side * 3;               // chunk bytes
+  const uint32_t cb16 = (cb + 15) & ~15u;
+  int32_t* shs = reinterpret_cast<int32_t*>(ys + cb16);
+
+  for (uint32_t t = tid; t < cr; t += blockDim.x) shs[t] = a.shift[al0 + t];
+  if (!VEC)
+    for (uint32_t i = cb + tid; i < cb16; i += blockDim.x) ys[i] = 0;
+  __syncthreads();
+
+  // Stage + permute: source pixel (sr, o) with sr + o == al (mod side) lands
+  // at chunk row al - al0, column (o + shift[al]) mod side.
+  const uint32_t items = side * cr;
+  for (uint32_t idx = tid; idx < items; idx += blockDim.x) {
+    const uint32_t sr = fdiv(idx, a.div_cr);
+    const uint32_t t = idx - sr * cr;
+    int o = int(al0 + t) - int(sr);
+    if (o < 0) o += side;
+    uint32_t be = uint32_t(o) + uint32_t(shs[t]);
+    if (be >= side) be -= side;
+    const uint8_t* sp = a.src + (uint64_t(sr) * side + uint32_t(o)) * 3;
+    uint8_t* dp = ys + (t * side + be) * 3;
+    dp[0] = sp[0];
+    dp[1] = sp[1];
+    dp[2] = sp[2];
+  }
+  if (tid == 0) prefix_share = seed_byte(a, band);
+  __syncthreads();
+
+  // Chunk-local inclusive XOR prefix of t, written back over y.
+  const uint8_t* ks = a.ring + uint64_t(band) * a.ring_bytes;
+  uint64_t kbase = a.pos + uint64_t(chunk) * cb;  // < 2R
+  if (kbase >= a.ring_bytes) kbase -= a.ring_bytes;
+  const uint32_t G = cb16 / 16;
+  uint32_t carry = 0, phase = 0;
+  for (uint32_t g0 = 0; g0 < G; g0 += blockDim.x, ++phase) {
+    const uint32_t g = g0 + tid;
+    uint64_t lo = 0, hi = 0;
+    uint32_t agg = 0;
+    if (g < G) {
+      const uint4 y = smem[g];
+      uint4 k;
+      if (VEC) {
+        uint64_t kp = kbase + 16ull * g;
+        if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+        k = ld_stream(ks + kp);
+      } else {
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (uint32_t i = 0; i < 16; ++i) {
+          const uint32_t j = 16 * g + i;
+          if (j < cb) {
+            uint64_t kp = kbase + j;
+            if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+            w[i >> 2] |= uint32_t(ks[kp]) << (8 * (i & 3));
+          }
+        }
+        k = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      lo = t_prefix8(y.x, y.y, k.x, k.y);
+      hi = t_prefix8(y.z, y.w, k.z, k.w);
+      hi ^= (lo >> 56) * kBcast;
+      agg = uint32_t(hi >> 56);
+    }
+    uint32_t total;
+    const uint32_t excl = block_xor_scan(agg, wsum, phase, total) ^ carry;
+    if (g < G) {
+      const uint64_t m = uint64_t(excl) * kBcast;
+      lo ^= m;
+      hi ^= m;
+      smem[g] = make_uint4(uint32_t(lo), uint32_t(lo >> 32), uint32_t(hi),
+                           uint32_t(hi >> 32));
+    }
+    carry ^= total;
+  }
+
+  // Band prefix: s_d ^ aggregates of the chunks before this one.
+  if (a.h > 1) {
+    cg::cluster_group cluster = cg::this_cluster();
+    if (tid == 0) agg_share = carry;
+    cluster.sync();
+    if (tid == 0) {
+      uint32_t p = prefix_share;
+      const uint32_t me = cluster.block_rank();
+      for (uint32_t j = 0; j < me; ++j) p ^= *cluster.map_shared_rank(&agg_share, j);
+      prefix_share = p;
+    }
+    cluster.sync();
+  } else {
+    __syncthreads();
+  }
+  const uint64_t m = uint64_t(prefix_share) * kBcast;
+  const uint32_t mlo = uint32_t(m);
+  uint8_t* out = a.dst + uint64_t(band) * a.region + uint64_t(chunk) * cb;
+  if (VEC) {
+    uint4* out4 = reinterpret_cast<uint4*>(out);
+    for (uint32_t g = tid; g < G; g += blockDim.x) {
+      uint4 v = smem[g];
+      v.x ^= mlo;
+      v.y ^= mlo;
+      v.z ^= mlo;
+      v.w ^= mlo;
+      out4[g] = v;
+    }
+  } else {
+    for (uint32_t j = tid; j < cb; j += blockDim.x) out[j] = ys[j] ^ uint8_t(mlo);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused inverse round.  One CTA per tile of T output rows; for every
+// cipher row al it gathers the contiguous run of T pixels that lands in the
+// tile, inverse-diffuses them elementwise, and writes the tile back with
+// coalesced stores.
+struct DecArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  const uint8_t* ring;
+  uint64_t ring_bytes;
+  uint64_t pos;
+  const int32_t* shift;
+  uint32_t side, n, rows, T;
+  uint64_t region;
+  FastDiv div_T, div_rows;
+};
+
+__device__ __forceinline__ uint8_t ks_byte(const DecArgs& a, uint32_t band,
+                                           uint64_t j) {
+  uint64_t kp = a.pos + j;
+  if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+  return a.ring[uint64_t(band) * a.ring_bytes + kp];
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kDecThreads)
+    k_decrypt_round(const DecArgs a) {
+  extern __shared__ uint4 smem[];
+  uint8_t* tile = reinterpret_cast<uint8_t*>(smem);
+  const uint32_t side = a.side, T = a.T;
+  const uint32_t a0 = blockIdx.x * T;
+  const uint32_t tv = min(T, side - a0);
+  const uint32_t items = side * T;
+  for (uint32_t idx = threadIdx.x; idx < items; idx += blockDim.x) {
+    const uint32_t al = fdiv(idx, a.div_T);
+    const uint32_t t = idx - al * T;
+    if (t >= tv) continue;
+    int o = int(al) - int(a0 + t);
+    if (o < 0) o += side;
+    uint32_t be = uint32_t(o) + uint32_t(__ldg(a.shift + al));
+    if (be >= side) be -= side;
+    const uint64_t P = (uint64_t(al) * side + be) * 3;
+    const uint32_t band = fdiv(al, a.div_rows);
+    const uint64_t j0 = P - uint64_t(band) * a.region;
+    const uint8_t c0 = a.src[P], c1 = a.src[P + 1], c2 = a.src[P + 2];
+    uint8_t cp;
+    if (j0 == 0) {  // band head: next band's recovered last byte
+      const uint32_t nb = band + 1 == a.n ? 0 : band + 1;
+      const uint64_t L = (uint64_t(nb) + 1) * a.region - 1;
+      const uint8_t kl = ks_byte(a, nb, a.region - 1);
+      cp = uint8_t((kl ^ a.src[L] ^ a.src[L - 1]) - kl);
+    } else {
+      cp = a.src[P - 1];
+    }
+    const uint8_t k0 = ks_byte(a, band, j0), k1 = ks_byte(a, band, j0 + 1),
+                  k2 = ks_byte(a, band, j0 + 2);
+    uint8_t* d = tile + (t * side + uint32_t(o)) * 3;
+    d[0] = uint8_t((k0 ^ c0 ^ cp) - k0);
+    d[1] = uint8_t((k1 ^ c1 ^ c0) - k1);
+    d[2] = uint8_t((k2 ^ c2 ^ c1) - k2);
+  }
+  __syncthreads();
+  const uint32_t bytes = tv * side * 3;
+  uint8_t* out = a.dst + uint64_t(a0) * side * 3;
+  if (VEC) {
+    uint4* out4 = reinterpret_cast<uint4*>(out);
+    for (uint32_t g = threadIdx.x; g < bytes / 16; g += blockDim.x) out4[g] = smem[g];
+  } else {
+    for (uint32_t j = threadIdx.x; j < bytes; j += blockDim.x) out[j] = tile[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic forward round for geometries whose band chunks do not fit one
+// cluster's shared memory: gather -> chunk aggregates -> band prefixes ->
+// chunk scans, through global scratch.
+constexpr uint32_t kGenChunk = 4096;  // bytes per chunk (256 threads x 16 B)
+
+__global__ void k_gather(const uint8_t* __restrict__ src, uint8_t* __restrict__ y,
+                         const int32_t* __restrict__ shift, uint32_t side) {
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= uint64_t(side) * side) return;
+  const uint32_t al = uint32_t(q / side), be = uint32_t(q - uint64_t(al) * side);
+  int o = int(be) - shift[al];
+  if (o < 0) o += side;
+  int sr = int(al) - o;
+  if (sr < 0) sr += side;
+  const uint8_t* sp = src + (uint64_t(sr) * side + uint32_t(o)) * 3;
+  y[q * 3] = sp[0];
+  y[q * 3 + 1] = sp[1];
+  y[q * 3 + 2] = sp[2];
+}
+
+struct GenArgs {
+  const uint8_t* y;
+  uint8_t* dst;
+  const uint8_t* ring;
+  uint64_t ring_bytes, pos, region;
+  uint32_t n, nch;
+  uint32_t* agg;  // n * nch
+};
+
+__device__ __forceinline__ void gen_chunk_values(const GenArgs& a, uint32_t band,
+                                                 uint32_t ch, uint64_t& lo,
+                                                 uint64_t& hi, uint32_t& agg) {
+  uint32_t yw[4] = {0, 0, 0, 0}, kw[4] = {0, 0, 0, 0};
+  const uint64_t j = uint64_t(ch) * kGenChunk + 16ull * threadIdx.x;
+  for (uint32_t i = 0; i < 16; ++i) {
+    if (j + i < a.region) {
+      yw[i >> 2] |= uint32_t(a.y[uint64_t(band) * a.region + j + i]) << (8 * (i & 3));
+      uint64_t kp = (a.pos + j + i) % a.ring_bytes;
+      kw[i >> 2] |= uint32_t(a.ring[uint64_t(band) * a.ring_bytes + kp]) << (8 * (i & 3));
+    }
+  }
+  lo = t_prefix8(yw[0], yw[1], kw[0], kw[1]);
+  hi = t_prefix8(yw[2], yw[3], kw[2], kw[3]);
+  hi ^= (lo >> 56) * kBcast;
+  agg = uint32_t(hi >> 56);
+}
+
+__global__ void __launch_bounds__(256) k_gen_aggregate(const GenArgs a) {
+  __shared__ uint32_t wsum[64];
+  const uint32_t band = blockIdx.y, ch = blockIdx.x;
+  uint64_t lo, hi;
+  uint32_t agg, total;
+  gen_chunk_values(a, band, ch, lo, hi, agg);
+  block_xor_scan(agg, wsum, 0, total);
+  if (threadIdx.x == 0) a.agg[band * a.nch + ch] = total;
+}
+
+__global__ void k_gen_prefix(const GenArgs a) {
+  const uint32_t band = blockIdx.x * blockDim.x + threadIdx.x;
+  if (band >= a.n) return;
+  const uint32_t nb = band + 1 == a.n ? 0 : band + 1;
+  uint32_t p = a.y[(uint64_t(nb) + 1) * a.region - 1];
+  for (uint32_t c = 0; c < a.nch; ++c) {
+    const uint32_t v = a.agg[band * a.nch + c];
+    a.agg[band * a.nch + c] = p;  // exclusive prefix incl. s_d
+    p ^= v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gen_scan(const GenArgs a) {
+  __shared__ uint32_t wsum[64];
+  const uint32_t band = blockIdx.y, ch = blockIdx.x;
+  uint64_t lo, hi;
+  uint32_t agg, total;
+  gen_chunk_values(a, band, ch, lo, hi, agg);
+  const uint32_t excl = block_xor_scan(agg, wsum, 0, total) ^ a.agg[band * a.nch + ch];
+  const uint64_t m = uint64_t(excl) * kBcast;
+  lo ^= m;
+  hi ^= m;
+  const uint64_t j = uint64_t(ch) * kGenChunk + 16ull * threadIdx.x;
+  uint8_t* out = a.dst + uint64_t(band) * a.region;
+  for (uint32_t i = 0; i < 16; ++i)
+    if (j + i < a.region) out[j + i] = uint8_t((i < 8 ? lo >> (8 * i) : hi >> (8 * (i - 8))));
+}
+
+__global__ void k_ring_move(const uint8_t* __restrict__ src, uint64_t sb,
+                            uint8_t* __restrict__ dst, uint64_t db, uint64_t lo,
+                            uint64_t hi, uint32_t workers) {
+  const uint64_t span = hi - lo;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < span * workers; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t w = i / span, s = lo + (i - w * span);
+    dst[w * db + s % db] = src[w * sb + s % sb];
+  }
+}
+
+inline void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    char msg[256];
+    std::snprintf(msg, sizeof msg, "%s launch failed: %s", what,
+                  cudaGetErrorString(e));
+    throw Error(Errc::internal, msg);
+  }
+}
+
+}  // namespace
+
+void launch_shift_table(const double* sine, uint32_t seed, int32_t* shift,
+                        uint32_t side, cudaStream_t s) {
+  k_shift<<<(side + 255) / 256, 256, 0, s>>>(sine, seed, shift, side);
+  check_launch("shift_table");
+}
+
+EncPlan plan_encrypt(const Geom& g) {
+  // Chunks of a band: h | rows, h <= 8 (one portable cluster).  Take the
+  // smallest h that gives a full wave (n*h >= 148 CTAs) with <= 100 KB of
+  // shared memory (2 CTAs/SM); otherwise the largest h that fits (most CTAs).
+  // No feasible h -> generic multi-kernel path.
+  const uint64_t row_bytes = uint64_t(g.side) * 3;
+  EncPlan best{false, 0, 0, 0};
+  for (uint32_t h = 1; h <= 8; ++h) {
+    if (g.rows % h) continue;
+    const uint64_t cb = uint64_t(g.rows / h) * row_bytes;
+    const size_t smem = size_t(((cb + 15) & ~uint64_t(15)) + 4 * (g.rows / h));
+    if (smem > kSmemBudget) continue;
+    best = EncPlan{true, g.rows / h, h, smem};
+    if (smem <= 100 * 1024 && uint64_t(g.n) * h >= 148) break;
+  }
+  return best;
+}
+
+void launch_encrypt_round(const EncPlan& plan, const Geom& g,
+                          const uint8_t* src, uint8_t* dst, KsWindow ks,
+                          const int32_t* shift, uint8_t* scratch,
+                          cudaStream_t s, uint64_t* launches) {
+  if (plan.fused) {
+    EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
+              g.rows, plan.chunk_rows, plan.h, g.region, make_div(plan.chunk_rows)};
+    const bool vec = (g.side % 16 == 0) && (ks.pos % 16 == 0) &&
+                     (ks.ring_bytes % 16 == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.n * plan.h);
+    cfg.blockDim = dim3(kEncThreads);
+    cfg.dynamicSmemBytes = plan.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = plan.h;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (vec) {
+      cudaFuncSetAttribute(k_encrypt_round<true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
+      cudaLaunchKernelEx(&cfg, k_encrypt_round<true>, a);
+    } else {
+      cudaFuncSetAttribute(k_encrypt_round<false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
+      cudaLaunchKernelEx(&cfg, k_encrypt_round<false>, a);
+    }
+    check_launch("encrypt_round");
+    ++*launches;
+    return;
+  }
+  // generic path: scratch holds y (frame_bytes) followed by chunk aggregates
+  const uint64_t pix = uint64_t(g.side) * g.side;
+  k_gather<<<uint32_t((pix + 255) / 256), 256, 0, s>>>(src, scratch, shift, g.side);
+  check_launch("gather");
+  const uint32_t nch = uint32_t((g.region + kGenChunk - 1) / kGenChunk);
+  uint32_t* agg = reinterpret_cast<uint32_t*>(scratch + ((g.frame_bytes + 255) & ~uint64_t(255)));
+  GenArgs a{scratch, dst, ks.ring, ks.ring_bytes, ks.pos, g.region, g.n, nch, agg};
+  k_gen_aggregate<<<dim3(nch, g.n), 256, 0, s>>>(a);
+  check_launch("gen_aggregate");
+  k_gen_prefix<<<(g.n + 127) / 128, 128, 0, s>>>(a);
+  check_launch("gen_prefix");
+  k_gen_scan<<<dim3(nch, g.n), 256, 0, s>>>(a);
+  check_launch("gen_scan");
+  *launches += 4;
+}
+
+void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
+                          KsWindow ks, const int32_t* shift, cudaStream_t s,
+                          uint64_t* launches) {
+  const uint64_t row_bytes = uint64_t(g.side) * 3;
+  uint32_t T = uint32_t(std::max<uint64_t>(1, (96 * 1024) / row_bytes));
+  const uint32_t want = std::max<uint32_t>(8, (g.side + 147) / 148);
+  T = std::min(T, want);
+  T = std::min(T, g.side);
+  const size_t smem = ((uint64_t(T) * row_bytes + 15) & ~uint64_t(15));
+  if (smem > kSmemBudget) throw Error(Errc::invalid_argument, "frame side too large");
+  DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
+            T, g.region, make_div(T), make_div(g.rows)};
+  const uint32_t grid = (g.side + T - 1) / T;
+  if (g.side % 16 == 0) {
+    cudaFuncSetAttribute(k_decrypt_round<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
+    k_decrypt_round<true><<<grid, kDecThreads, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_decrypt_round<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
+    k_decrypt_round<false><<<grid, kDecThreads, smem, s>>>(a);
+  }
+  check_launch("decrypt_round");
+  ++*launches;
+}
+
+void launch_ring_move(const uint8_t* src, uint64_t src_bytes, uint8_t* dst,
+                      uint64_t dst_bytes, uint64_t lo, uint64_t hi,
+                      uint32_t workers, cudaStream_t s) {
+  if (hi <= lo) return;
+  k_ring_move<<<1024, 256, 0, s>>>(src, src_bytes, dst, dst_bytes, lo, hi, workers);
+  check_launch("ring_move");
+}
+
+}  // namespace cveb

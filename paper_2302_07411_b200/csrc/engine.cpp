@@ -1,0 +1,479 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+namespace cveb {
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+    throw Error(Errc::internal, msg);
+  }
+}
+
+uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
+
+}  // namespace
+
+Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
+    : key_(key), n_(workers), r_(rounds), dev_(device), coord_(key) {
+  // engine.cpp:168-179: coordinator first, then workers/rounds checks.
+  if (workers == 0) raise(Errc::invalid_argument, "workers must be >= 1");
+  if (rounds == 0 || rounds > 255)
+    raise(Errc::invalid_argument, "rounds must be in 1..255");
+  const std::vector<WorkerLanes> lanes = coord_.derive_workers(n_);
+
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    raise(Errc::internal, "no CUDA device: the B200 engine has no CPU path");
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, dev_), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    raise(Errc::internal, std::string("engine is built for sm_100a; device is ") +
+                              prop.name);
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+
+  ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&s_work_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+
+  const uint32_t nl = 2 * n_;
+  std::vector<LaneConst> lc(nl);
+  std::vector<double> x0(nl);
+  for (uint32_t i = 0; i < n_; ++i) {
+    lc[2 * i] = make_lane_const(lanes[i].a.p);
+    lc[2 * i + 1] = make_lane_const(lanes[i].b.p);
+    x0[2 * i] = lanes[i].a.x0;
+    x0[2 * i + 1] = lanes[i].b.x0;
+  }
+  double* d_x0 = nullptr;
+  ck(cudaMalloc(&d_state_, nl * sizeof(double)), "cudaMalloc state");
+  ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
+  ck(cudaMalloc(&d_x0, nl * sizeof(double)), "cudaMalloc x0");
+  ck(cudaMalloc(&d_replays_, sizeof(unsigned long long)), "cudaMalloc");
+  ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice),
+     "upload lanes");
+  ck(cudaMemcpy(d_x0, x0.data(), nl * sizeof(double), cudaMemcpyHostToDevice),
+     "upload x0");
+  ck(cudaMemset(d_replays_, 0, sizeof(unsigned long long)), "memset");
+  launch_prbg_init(d_state_, d_lc_, d_x0, nl, s_gen_);
+  ck(cudaGetLastError(), "prbg_init launch");
+  ++st_.kernel_launches;
+  ck(cudaStreamSynchronize(s_gen_), "prbg_init");
+  cudaFree(d_x0);
+
+  if (const char* e = std::getenv("CVE_B200_RESERVE_SMEM"))
+    reserve_smem_ = uint32_t(std::strtoul(e, nullptr, 10));
+}
+
+Engine::~Engine() {
+  cudaSetDevice(dev_);
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+    if (s) cudaStreamSynchronize(s);
+  for (auto& c : consumers_) ev_put(c.done);
+  for (auto& g : gens_) ev_put(g.ev);
+  for (auto& t : timed_) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  if (open_.a) cudaEventDestroy(open_.a);
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
+  for (uint8_t* p : slots_) cudaFree(p);
+  for (auto& kv : sines_) cudaFree(kv.second);
+  for (uint8_t* p : scratch_) cudaFree(p);
+  cudaFree(d_shift_);
+  cudaFree(ring_);
+  cudaFree(d_state_);
+  cudaFree(d_lc_);
+  cudaFree(d_replays_);
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+    if (s) cudaStreamDestroy(s);
+}
+
+Geom Engine::geometry(uint32_t side) const {
+  Geom g;
+  g.side = side;
+  g.n = n_;
+  g.rows = side / n_;
+  g.region = uint64_t(g.rows) * side * 3;
+  g.frame_bytes = uint64_t(side) * side * 3;
+  return g;
+}
+
+// Seed drawn before the side check, like Engine::encrypt (engine.cpp:293-296)
+// followed by check_frame (engine.cpp:189-196).  Returns nothing useful; the
+// seeds are drawn again per frame by the caller after this check passes.
+uint32_t Engine::draw_and_check(uint32_t side, uint32_t count) {
+  (void)count;
+  if (side % n_ != 0) {
+    coord_.next_seed();
+    raise(Errc::mismatch, "frame side is not divisible by the worker count");
+  }
+  if (side > 65536) {
+    coord_.next_seed();
+    raise(Errc::invalid_argument, "frame side above 65536 is not supported");
+  }
+  return 0;
+}
+
+cudaEvent_t Engine::ev_get() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  return e;
+}
+
+void Engine::ev_put(cudaEvent_t e) { ev_pool_.push_back(e); }
+
+void Engine::timed_begin(cudaStream_t s, bool prbg) {
+  Timed t{};
+  ck(cudaEventCreate(&t.a), "cudaEventCreate");
+  ck(cudaEventCreate(&t.b), "cudaEventCreate");
+  t.prbg = prbg;
+  ck(cudaEventRecord(t.a, s), "cudaEventRecord");
+  open_ = t;
+}
+
+void Engine::timed_end(cudaStream_t s) {
+  ck(cudaEventRecord(open_.b, s), "cudaEventRecord");
+  timed_.push_back(open_);
+  open_ = Timed{};
+  if (timed_.size() > 4096) fold_timings(false);
+}
+
+void Engine::fold_timings(bool wait) {
+  std::vector<Timed> keep;
+  for (auto& t : timed_) {
+    if (!wait && cudaEventQuery(t.b) != cudaSuccess) {
+      keep.push_back(t);
+      continue;
+    }
+    float ms = 0;
+    ck(cudaEventSynchronize(t.b), "timing event");
+    ck(cudaEventElapsedTime(&ms, t.a, t.b), "cudaEventElapsedTime");
+    if (t.prbg) {
+      st_.prbg_ms += ms;
+      if (prbg_times_.size() < (1u << 20)) prbg_times_.push_back(ms);
+    } else {
+      st_.cipher_ms += ms;
+    }
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  timed_.swap(keep);
+}
+
+// Ring of >= 4 frames of keystream per worker, so the generator can run one
+// frame ahead while up to two frames are still being ciphered.
+void Engine::ensure_ring(uint64_t need) {
+  if (ring_bytes_ >= 4 * need) return;
+  const uint64_t want = round_up(4 * need + 48 * 1024, 48 * 1024);
+  synchronize();
+  uint8_t* fresh = nullptr;
+  ck(cudaMalloc(&fresh, want * n_), "cudaMalloc keystream ring");
+  const uint64_t gen_bytes = gen_iters_ * 6;
+  if (ring_ && gen_bytes > cons_) {
+    launch_ring_move(ring_, ring_bytes_, fresh, want, cons_, gen_bytes, n_, s_gen_);
+    ++st_.kernel_launches;
+    ck(cudaStreamSynchronize(s_gen_), "ring move");
+  }
+  cudaFree(ring_);
+  ring_ = fresh;
+  ring_bytes_ = want;
+  for (auto& c : consumers_) ev_put(c.done);
+  consumers_.clear();
+  for (auto& g : gens_) ev_put(g.ev);
+  gens_.clear();
+}
+
+void Engine::ensure_buffers(const Geom& g, uint32_t slots) {
+  const uint64_t fb = g.frame_bytes;
+  const uint64_t scratch_need =
+      round_up(fb, 256) + 4 * uint64_t(g.n) * ((g.region + 4095) / 4096) + 256;
+  const bool generic = !plan_encrypt(g).fused;
+  if (scratch_bytes_ < scratch_need || (generic && !scratch_[2])) {
+    synchronize();
+    for (auto& p : scratch_) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    ck(cudaMalloc(&scratch_[0], scratch_need), "cudaMalloc scratch");
+    ck(cudaMalloc(&scratch_[1], scratch_need), "cudaMalloc scratch");
+    if (generic) ck(cudaMalloc(&scratch_[2], scratch_need), "cudaMalloc scratch");
+    scratch_bytes_ = scratch_need;
+  }
+  if (shift_cap_ < g.side) {
+    synchronize();
+    cudaFree(d_shift_);
+    ck(cudaMalloc(&d_shift_, sizeof(int32_t) * g.side), "cudaMalloc shift");
+    shift_cap_ = g.side;
+  }
+  if (slots && (slots_.size() < slots || slot_bytes_ < fb)) {
+    synchronize();
+    for (uint8_t* p : slots_) cudaFree(p);
+    slots_.assign(slots, nullptr);
+    for (auto& p : slots_) ck(cudaMalloc(&p, fb), "cudaMalloc frame slot");
+    slot_bytes_ = fb;
+    while (slot_free_.size() < slots) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(e, s_d2h_), "cudaEventRecord");
+      slot_free_.push_back(e);
+    }
+  }
+}
+
+const double* Engine::sine_for(uint32_t side) {
+  auto it = sines_.find(side);
+  if (it != sines_.end()) return it->second;
+  const std::vector<double> s = sine_table(side);
+  double* d = nullptr;
+  ck(cudaMalloc(&d, sizeof(double) * side), "cudaMalloc sine");
+  ck(cudaMemcpy(d, s.data(), sizeof(double) * side, cudaMemcpyHostToDevice),
+     "upload sine");
+  sines_[side] = d;
+  return d;
+}
+
+// Enqueue generator launches on s_gen until stream byte `end_byte` (per
+// worker) is produced.  Launches cover whole 8-iteration (48-byte) blocks.
+void Engine::gen_until(uint64_t end_byte) {
+  uint64_t target = round_up((end_byte + 5) / 6, 8);
+  // never produce beyond what the ring can hold ahead of unassigned bytes
+  const uint64_t cap = (cons_ + ring_bytes_) / 6 / 8 * 8;
+  target = std::min(target, cap);
+  while (gen_iters_ < target) {
+    uint64_t chunk = target - gen_iters_;
+    const uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+    chunk = std::min(chunk, max_chunk);
+    const uint64_t write_end = (gen_iters_ + chunk) * 6;
+    // bytes below write_end - R get overwritten: their readers must be done
+    if (write_end > ring_bytes_) {
+      const uint64_t dead = write_end - ring_bytes_;
+      while (!consumers_.empty() && consumers_.front().lo < dead) {
+        ck(cudaStreamWaitEvent(s_gen_, consumers_.front().done, 0), "wait");
+        if (consumers_.front().hi <= dead) {
+          ev_put(consumers_.front().done);
+          consumers_.pop_front();
+        } else {
+          break;
+        }
+      }
+    }
+    timed_begin(s_gen_, true);
+    launch_prbg_generate(d_state_, d_lc_, ring_, ring_bytes_, gen_iters_,
+                         uint32_t(chunk / 8), 2 * n_, d_replays_, reserve_smem_,
+                         s_gen_);
+    ck(cudaGetLastError(), "prbg_generate launch");
+    timed_end(s_gen_);
+    ++st_.kernel_launches;
+    ++st_.prbg_launches;
+    gen_iters_ += chunk;
+    st_.keystream_iters += chunk;
+    GenMark m{gen_iters_ * 6, ev_get()};
+    ck(cudaEventRecord(m.ev, s_gen_), "cudaEventRecord");
+    gens_.push_back(m);
+  }
+}
+
+// Event of the first generator launch whose output reaches end_byte.  Marks
+// ending below end_byte are useless to this and every later frame.
+cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
+  while (!gens_.empty() && gens_.front().end_byte < end_byte) {
+    ev_put(gens_.front().ev);
+    gens_.pop_front();
+  }
+  return gens_.empty() ? nullptr : gens_.front().ev;  // null: already synced
+}
+
+void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
+                           bool decrypt) {
+  const uint64_t need = uint64_t(r_) * g.region;
+  const uint64_t lo = cons_;
+  cons_ += need;
+  gen_until(lo + need);
+  if (cudaEvent_t ge = gen_event_covering(lo + need))
+    ck(cudaStreamWaitEvent(s_work_, ge, 0), "wait keystream");
+
+  timed_begin(s_work_, false);
+  launch_shift_table(sine_for(g.side), seed, d_shift_, g.side, s_work_);
+  ++st_.kernel_launches;
+  KsWindow ks{ring_, ring_bytes_, 0};
+  const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
+  // Round 0 reads buf; middle rounds ping-pong the two scratch frames; the
+  // last round writes buf (r == 1 goes through scratch and a copy).  The
+  // generic encrypt path stages y in a third scratch frame.
+  const uint8_t* src = buf;
+  for (uint32_t step = 0; step < r_; ++step) {
+    const uint32_t k = decrypt ? r_ - 1 - step : step;
+    uint8_t* dst = (step + 1 == r_ && r_ > 1)
+                       ? buf
+                       : (src == scratch_[0] ? scratch_[1] : scratch_[0]);
+    ks.pos = (lo + uint64_t(k) * g.region) % ring_bytes_;
+    if (decrypt)
+      launch_decrypt_round(g, src, dst, ks, d_shift_, s_work_, &st_.kernel_launches);
+    else
+      launch_encrypt_round(plan, g, src, dst, ks, d_shift_, scratch_[2], s_work_,
+                           &st_.kernel_launches);
+    src = dst;
+  }
+  if (r_ == 1)
+    ck(cudaMemcpyAsync(buf, src, g.frame_bytes, cudaMemcpyDeviceToDevice, s_work_),
+       "d2d");
+  timed_end(s_work_);
+  Consumer c{lo, lo + need, ev_get()};
+  ck(cudaEventRecord(c.done, s_work_), "cudaEventRecord");
+  consumers_.push_back(c);
+  ++st_.frames;
+  // run-ahead: start the next frame's keystream behind this one's
+  gen_until(cons_ + need);
+}
+
+void Engine::run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt) {
+  draw_and_check(side, count);
+  const Geom g = geometry(side);
+  ensure_ring(uint64_t(r_) * g.region);
+  ensure_buffers(g, kSlots);
+
+  for (uint32_t f = 0; f < count; ++f) {
+    const uint32_t seed = coord_.next_seed();
+    const uint32_t slot = f % kSlots;
+    uint8_t* host = px + uint64_t(f) * g.frame_bytes;
+    uint8_t* dbuf = slots_[slot];
+    ck(cudaStreamWaitEvent(s_h2d_, slot_free_[slot], 0), "wait slot");
+    ck(cudaMemcpyAsync(dbuf, host, g.frame_bytes, cudaMemcpyHostToDevice, s_h2d_),
+       "H2D");
+    cudaEvent_t in = ev_get();
+    ck(cudaEventRecord(in, s_h2d_), "record");
+    ck(cudaStreamWaitEvent(s_work_, in, 0), "wait H2D");
+    ev_put(in);
+    enqueue_frame(dbuf, g, seed, decrypt);
+    ck(cudaStreamWaitEvent(s_d2h_, consumers_.back().done, 0), "wait work");
+    ck(cudaMemcpyAsync(host, dbuf, g.frame_bytes, cudaMemcpyDeviceToHost, s_d2h_),
+       "D2H");
+    ck(cudaEventRecord(slot_free_[slot], s_d2h_), "record");
+  }
+  ck(cudaStreamSynchronize(s_d2h_), "frame pipeline");
+}
+
+void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
+                        bool decrypt, cudaStream_t user) {
+  draw_and_check(side, count);
+  const Geom g = geometry(side);
+  ensure_ring(uint64_t(r_) * g.region);
+  ensure_buffers(g, 0);
+  cudaEvent_t in = ev_get();
+  ck(cudaEventRecord(in, user), "record user stream");
+  ck(cudaStreamWaitEvent(s_work_, in, 0), "wait user stream");
+  ev_put(in);
+  for (uint32_t f = 0; f < count; ++f) {
+    const uint32_t seed = coord_.next_seed();
+    enqueue_frame(d_px + uint64_t(f) * g.frame_bytes, g, seed, decrypt);
+  }
+  ck(cudaStreamWaitEvent(user, consumers_.back().done, 0), "join user stream");
+}
+
+void Engine::synchronize() {
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+void Engine::peek(uint32_t worker, uint8_t* out, size_t len) {
+  if (worker >= n_) raise(Errc::invalid_argument, "worker index out of range");
+  if (len == 0) return;
+  ensure_ring(std::max<uint64_t>(len, 48));
+  if (len > ring_bytes_ / 2) raise(Errc::invalid_argument, "peek too long");
+  gen_until(cons_ + len);
+  synchronize();
+  const uint64_t start = cons_ % ring_bytes_;
+  const uint8_t* base = ring_ + uint64_t(worker) * ring_bytes_;
+  const uint64_t first = std::min<uint64_t>(len, ring_bytes_ - start);
+  ck(cudaMemcpy(out, base + start, first, cudaMemcpyDeviceToHost), "peek");
+  if (first < len)
+    ck(cudaMemcpy(out + first, base, len - first, cudaMemcpyDeviceToHost), "peek");
+}
+
+void Engine::prefetch(uint64_t bytes) {
+  ensure_ring(std::max<uint64_t>(bytes, 48));
+  gen_until(cons_ + bytes);
+}
+
+EngineStats Engine::stats() {
+  synchronize();
+  fold_timings(true);
+  unsigned long long rep = 0;
+  ck(cudaMemcpy(&rep, d_replays_, sizeof rep, cudaMemcpyDeviceToHost), "stats");
+  st_.guard_replays = rep;
+  return st_;
+}
+
+std::vector<float> Engine::take_prbg_times() {
+  synchronize();
+  fold_timings(true);
+  std::vector<float> out;
+  out.swap(prbg_times_);
+  return out;
+}
+
+// The reference's Prbg{lane_a, lane_b}.take(len) (chaos.cpp:79-91, 143-153,
+// 174-180) on the GPU: explicit lanes, one worker, K1 kernels.
+void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
+  if (len == 0) return;
+  HostPrbg validate(a, b);  // domain checks (bad_key), cheap
+  (void)validate;
+  const uint64_t iters = round_up((len + 5) / 6, 8);
+  const uint64_t ring = iters * 6;  // multiple of 48
+  LaneConst lc[2] = {make_lane_const(a.p), make_lane_const(b.p)};
+  const double x0[2] = {a.x0, b.x0};
+  double* d_state = nullptr;
+  double* d_x0 = nullptr;
+  LaneConst* d_lc = nullptr;
+  unsigned long long* d_rep = nullptr;
+  uint8_t* d_out = nullptr;
+  cudaStream_t s = nullptr;
+  auto cleanup = [&] {
+    cudaFree(d_state);
+    cudaFree(d_x0);
+    cudaFree(d_lc);
+    cudaFree(d_rep);
+    cudaFree(d_out);
+    if (s) cudaStreamDestroy(s);
+  };
+  try {
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    ck(cudaMalloc(&d_state, sizeof x0), "cudaMalloc");
+    ck(cudaMalloc(&d_x0, sizeof x0), "cudaMalloc");
+    ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
+    ck(cudaMalloc(&d_rep, sizeof(unsigned long long)), "cudaMalloc");
+    ck(cudaMalloc(&d_out, ring), "cudaMalloc");
+    ck(cudaMemcpy(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemcpy(d_x0, x0, sizeof x0, cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemset(d_rep, 0, sizeof(unsigned long long)), "memset");
+    launch_prbg_init(d_state, d_lc, d_x0, 2, s);
+    ck(cudaGetLastError(), "prbg_init");
+    launch_prbg_generate(d_state, d_lc, d_out, ring, 0, uint32_t(iters / 8), 2,
+                         d_rep, 0, s);
+    ck(cudaGetLastError(), "prbg_generate");
+    ck(cudaStreamSynchronize(s), "keystream");
+    ck(cudaMemcpy(out, d_out, len, cudaMemcpyDeviceToHost), "download");
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace cveb

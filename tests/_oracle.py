@@ -1,0 +1,144 @@
+"""ctypes access to the CHECKERS (test infrastructure only).
+
+* ``Oracle``    -- oracle/liboracle.so, the plain-C restatement of the
+                   reference path (oracle/cve_oracle.c).
+* ``Reference`` -- oracle/_ref/libcve_ref.so, the reference's own sources
+                   compiled in place by oracle/Makefile (absent if the
+                   reference was not available at build time).
+
+Nothing in the product package imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "liboracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libcve_ref.so")
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+class Oracle:
+    lib = None
+
+    def __init__(self, key_hex: str, workers: int, rounds: int = 5):
+        L = Oracle.load()
+        h = C.c_void_p()
+        st = L.orc_cipher_create(key_hex.encode(), workers, rounds, C.byref(h))
+        if st:
+            raise ValueError(f"oracle create status {st}")
+        self.h, self.workers, self.rounds = h, workers, rounds
+
+    @classmethod
+    def load(cls):
+        if cls.lib is None:
+            L = C.CDLL(ORACLE_SO)
+            vp = C.c_void_p
+            L.orc_cipher_create.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.POINTER(vp)]
+            L.orc_cipher_destroy.argtypes = [vp]
+            L.orc_cipher_encrypt_frame.argtypes = [vp, vp, C.c_uint32]
+            L.orc_cipher_decrypt_frame.argtypes = [vp, vp, C.c_uint32]
+            L.orc_cipher_worker_stream.argtypes = [vp, C.c_uint32, vp, C.c_size_t]
+            L.orc_cipher_next_seed.argtypes = [vp]
+            L.orc_cipher_next_seed.restype = C.c_uint32
+            L.orc_cipher_seeds_drawn.argtypes = [vp]
+            L.orc_cipher_seeds_drawn.restype = C.c_uint64
+            L.orc_cipher_params.argtypes = [vp]
+            L.orc_cipher_params.restype = C.POINTER(C.c_double)
+            L.orc_plcm_stream.argtypes = [C.c_double] * 4 + [vp, C.c_size_t]
+            L.orc_plcm_iterate.argtypes = [C.c_double, C.c_double]
+            L.orc_plcm_iterate.restype = C.c_double
+            L.orc_confusion_shift.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
+            L.orc_confusion_shift.restype = C.c_int64
+            L.orc_diffuse_byte.argtypes = [C.c_uint8] * 3
+            L.orc_diffuse_byte.restype = C.c_uint8
+            L.orc_inverse_diffuse_byte.argtypes = [C.c_uint8] * 3
+            L.orc_inverse_diffuse_byte.restype = C.c_uint8
+            L.orc_padded_side.argtypes = [C.c_uint32] * 3
+            L.orc_padded_side.restype = C.c_uint32
+            cls.lib = L
+        return cls.lib
+
+    def close(self):
+        if self.h:
+            Oracle.lib.orc_cipher_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def encrypt(self, frame: np.ndarray) -> int:
+        return Oracle.lib.orc_cipher_encrypt_frame(self.h, _ptr(frame), frame.shape[0])
+
+    def decrypt(self, frame: np.ndarray) -> int:
+        return Oracle.lib.orc_cipher_decrypt_frame(self.h, _ptr(frame), frame.shape[0])
+
+    def worker_stream(self, worker: int, n: int) -> np.ndarray:
+        out = np.zeros(n, dtype=np.uint8)
+        Oracle.lib.orc_cipher_worker_stream(self.h, worker, _ptr(out), n)
+        return out
+
+    def params(self) -> np.ndarray:
+        p = Oracle.lib.orc_cipher_params(self.h)
+        return np.ctypeslib.as_array(p, shape=(self.workers * 4,)).reshape(self.workers, 4).copy()
+
+    @property
+    def seeds_drawn(self) -> int:
+        return Oracle.lib.orc_cipher_seeds_drawn(self.h)
+
+
+def plcm_stream(xa, pa, xb, pb, n) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint8)
+    st = Oracle.load().orc_plcm_stream(xa, pa, xb, pb, _ptr(out), n)
+    assert st == 0
+    return out
+
+
+class Reference:
+    """The reference's own C ABI (cve.h) from oracle/_ref/libcve_ref.so."""
+    lib = None
+
+    @classmethod
+    def available(cls) -> bool:
+        return os.path.exists(REF_SO)
+
+    @classmethod
+    def load(cls):
+        if cls.lib is None:
+            L = C.CDLL(REF_SO)
+            vp = C.c_void_p
+            L.cve_cipher_create.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_int,
+                                            C.POINTER(vp)]
+            L.cve_cipher_destroy.argtypes = [vp]
+            L.cve_cipher_encrypt_frame.argtypes = [vp, vp, C.c_uint32]
+            L.cve_cipher_decrypt_frame.argtypes = [vp, vp, C.c_uint32]
+            L.cve_cipher_seeds_drawn.argtypes = [vp, C.POINTER(C.c_uint64)]
+            L.cve_last_error.restype = C.c_char_p
+            cls.lib = L
+        return cls.lib
+
+    def __init__(self, key_hex: str, workers: int, rounds: int = 5, parallel: int = 1):
+        L = Reference.load()
+        h = C.c_void_p()
+        st = L.cve_cipher_create(key_hex.encode(), workers, rounds, parallel, C.byref(h))
+        if st:
+            raise ValueError(f"reference create status {st}: {L.cve_last_error()}")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            Reference.lib.cve_cipher_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def encrypt(self, frame: np.ndarray) -> int:
+        return Reference.lib.cve_cipher_encrypt_frame(self.h, _ptr(frame), frame.shape[0])
+
+    def decrypt(self, frame: np.ndarray) -> int:
+        return Reference.lib.cve_cipher_decrypt_frame(self.h, _ptr(frame), frame.shape[0])

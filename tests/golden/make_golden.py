@@ -1,0 +1,138 @@
+"""Generates tests/golden/*.json from the REFERENCE ITSELF.
+
+Runs the reference's own C ABI (oracle/_ref/libcve_ref.so, compiled from
+/root/reference/proj/src by oracle/Makefile) on the seeded synthetic frames of
+paper_2302_07411_b200.synth and records:
+
+* reference_unit.json -- literal golden constants from the reference's own
+  unit tests (cited file:line), re-checked here against the reference.
+* frames.json -- per config: key, side, workers, and the SHA-256 of the
+  reference ciphertext of the first frames of each clip (C5 includes the
+  all-zero and all-255 edge frames); C3 adds the one-bit key-flip variant.
+* small.json -- full plaintext/ciphertext hex for small shapes (fast exact
+  checks incl. decrypt), and full worker keystream prefixes.
+
+Usage:  python tests/golden/make_golden.py   (needs oracle/_ref built)
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+
+from paper_2302_07411_b200 import synth  # noqa: E402
+from _oracle import Oracle, Reference  # noqa: E402
+
+PLCM_HEX = "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f"
+
+# frames of each clip recorded (C4/C5 reference frames cost ~0.2-0.7 s each)
+FRAMES = {"C1": 1, "C2": 24, "C3": 6, "C4": 2, "C5": 3}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def ref_encrypt_clip(key: str, n: int, frames):
+    r = Reference(key, n, synth.ROUNDS, 1)
+    out = []
+    for f in frames:
+        c = f.copy()
+        assert r.encrypt(c) == 0
+        out.append(c)
+    return out
+
+
+def main() -> None:
+    assert Reference.available(), "build oracle/_ref first (make -C oracle ref)"
+    unit = {
+        "source": "literal constants from the reference's unit tests",
+        "plcm_golden_48": {
+            "cite": "proj/tests/test_chaos.cpp:96-109",
+            "lanes": [0.123456789, 0.3141592653, 0.987654321, 0.2718281828],
+            "bytes": "14589028bd4e990d239256d86f321ffd6fdc5938c6fdd039"
+                     "ddaa0a4ed6d13462b5e73feabe3b9a5bc6fcfdcaca4865f0",
+        },
+        "worker_params_n2": {
+            "cite": "proj/tests/test_keying.cpp:160-179",
+            "key": PLCM_HEX,
+            "lanes": [[0.3075738289263239, 0.42253548314947736,
+                       0.86108381282468782, 0.11292260212592216],
+                      [0.81967628250537605, 0.45751880730777278,
+                       0.98740170016730744, 0.46952273822307322]],
+            "seeds": [2776256323, 2929325465, 448867532],
+        },
+        "shift_side4_seed7": {"cite": "proj/tests/test_engine.cpp:61-70",
+                              "shift": [0, 7, 0, -7]},
+        "diffuse_example": {"cite": "proj/tests/test_engine.cpp:117-120",
+                            "v": 0xF0, "b": 0x10, "prev": 0x0F, "c": 0x1F},
+        "extract_third": {"cite": "proj/tests/test_chaos.cpp:83-94",
+                          "value": "1/3", "bytes": "555555555555"},
+    }
+    with open(os.path.join(HERE, "reference_unit.json"), "w") as fh:
+        json.dump(unit, fh, indent=1)
+
+    frames = {}
+    for name, count in FRAMES.items():
+        c = synth.CONFIGS[name]
+        key = synth.config_key(name)
+        side = synth.config_side(name)
+        plain = synth.frame_list(name, count)
+        ct = ref_encrypt_clip(key, c["workers"], plain)
+        rec = {"key": key, "side": side, "workers": c["workers"],
+               "rounds": synth.ROUNDS,
+               "plain_sha256": [sha(p) for p in plain],
+               "cipher_sha256": [sha(x) for x in ct]}
+        if name == "C3":
+            fk = synth.flip_key_lsb(key)
+            ct_flip = ref_encrypt_clip(fk, c["workers"], plain[:1])[0]
+            rec["flip_key"] = fk
+            rec["flip_cipher_sha256"] = sha(ct_flip)
+            rec["flip_differ_fraction"] = float((ct_flip != ct[0]).mean())
+        if name == "C5":
+            rec["zero_frame_cipher_all_zero"] = bool((ct[0] == 0).all())
+            rec["full_frame_fraction_255"] = float((ct[1] == 255).mean())
+        frames[name] = rec
+        print(name, "done", flush=True)
+    with open(os.path.join(HERE, "frames.json"), "w") as fh:
+        json.dump(frames, fh, indent=1)
+
+    small = {"cases": []}
+    rng = np.random.Generator(np.random.PCG64(2302))
+    for side, n, r, nframes in [(8, 2, 3, 3), (24, 4, 5, 2), (30, 3, 5, 2), (48, 1, 2, 2),
+                                (96, 8, 5, 2), (20, 5, 1, 2)]:
+        key = synth.det_key(1000 + side + n)
+        plain = [rng.integers(0, 256, (side, side, 3), dtype=np.uint8) for _ in range(nframes)]
+        rr = Reference(key, n, r, 1)
+        ct = []
+        for p in plain:
+            x = p.copy()
+            assert rr.encrypt(x) == 0
+            ct.append(x.tobytes().hex())
+        small["cases"].append({"key": key, "side": side, "workers": n, "rounds": r,
+                               "plain": [p.tobytes().hex() for p in plain],
+                               "cipher": ct})
+    # keystream prefixes of every worker (reference Prbg via the oracle's
+    # restatement, itself pinned against the reference in test_oracle.py)
+    ks = {}
+    for name in ("C1", "C4"):
+        c = synth.CONFIGS[name]
+        o = Oracle(synth.config_key(name), c["workers"])
+        ks[name] = [hashlib.sha256(o.worker_stream(i, 1 << 20).tobytes()).hexdigest()
+                    for i in range(c["workers"])]
+    small["worker_stream_sha256_1MiB"] = ks
+    with open(os.path.join(HERE, "small.json"), "w") as fh:
+        json.dump(small, fh)
+    print("wrote", HERE)
+
+
+if __name__ == "__main__":
+    main()

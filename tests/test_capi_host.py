@@ -1,0 +1,138 @@
+"""Host-side C ABI behaviour of libcve_b200.so that needs no GPU: the
+library loads, exports every symbol include/cve_b200.h declares, and matches
+the reference's key / status / argument-validation semantics
+(reference proj/tests/test_capi.cpp:70-112, 164-174; test_keying.cpp)."""
+import ctypes as C
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2302_07411_b200 as cve
+from conftest import gpu_present
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PLCM = "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f"
+LASM = "01333333333333d33f666666666666e63f6f8104c58f31ed3f"
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "cve_b200.h")).read()
+    return sorted(set(re.findall(r"CVE_B200_API\s+[\w\s\*]+?\b(cve_\w+)\s*\(", text)))
+
+
+def test_every_declared_symbol_is_exported():
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(cve.lib, s), s
+
+
+def test_no_torch_or_oracle_in_library():
+    # the product .so links neither the oracle nor python/torch
+    blob = open(cve.lib_path, "rb").read()
+    assert b"orc_cipher" not in blob and b"libtorch" not in blob
+
+
+def test_identity_and_status_strings():
+    assert cve.lib.cve_version()
+    assert cve.lib.cve_status_message(0) == b"ok"
+    assert cve.lib.cve_status_message(99)
+    cve.lib.cve_string_free(None)
+
+
+def test_key_generate_capacity():
+    buf = C.create_string_buffer(80)
+    assert cve.lib.cve_key_generate(0, buf, 66) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert cve.lib.cve_key_generate(0, buf, 67) == 0 and len(buf.value) == 66
+    assert cve.key_validate(buf.value) == cve.CVE_MAP_PLCM
+    assert cve.lib.cve_key_generate(1, buf, 50) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert cve.lib.cve_key_generate(1, buf, 80) == 0 and len(buf.value) == 50
+    assert cve.key_validate(buf.value) == cve.CVE_MAP_LASM
+    assert cve.lib.cve_key_generate(0, None, 67) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert cve.lib.cve_key_generate(7, buf, 80) == cve.CVE_ERROR_INVALID_ARGUMENT
+
+
+def test_key_validate():
+    assert cve.key_validate(PLCM) == cve.CVE_MAP_PLCM
+    assert cve.key_validate(PLCM + "\n") == cve.CVE_MAP_PLCM  # trailing ws trimmed
+    assert cve.key_validate(LASM) == cve.CVE_MAP_LASM
+    corrupt = PLCM[:5] + "x" + PLCM[6:]
+    kind = C.c_int()
+    assert cve.lib.cve_key_validate(corrupt.encode(), C.byref(kind)) == cve.CVE_ERROR_BAD_KEY
+    assert len(cve.lib.cve_last_error()) > 0
+    assert cve.lib.cve_key_validate(None, C.byref(kind)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    for bad in ["00ff", "02" + PLCM[2:], PLCM[:-2]]:
+        with pytest.raises(cve.CveError) as e:
+            cve.key_validate(bad)
+        assert e.value.status == cve.CVE_ERROR_BAD_KEY
+    # out-of-domain p (0.5) is a bad key
+    import struct
+    k = "00" + "".join(struct.pack("<d", v).hex() for v in (0.3, 0.5, 0.4, 0.2))
+    with pytest.raises(cve.CveError):
+        cve.key_validate(k)
+
+
+def test_create_validation_before_device():
+    h = C.c_void_p()
+    L = cve.lib
+    assert L.cve_cipher_create(None, 2, 3, 1, C.byref(h)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create(b"00ff", 2, 3, 1, C.byref(h)) == cve.CVE_ERROR_BAD_KEY
+    assert L.cve_cipher_create(PLCM.encode(), 0, 3, 1, C.byref(h)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create(PLCM.encode(), 2, 0, 1, C.byref(h)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create(PLCM.encode(), 2, 256, 1, C.byref(h)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create(PLCM.encode(), 2, 3, 1, None) == cve.CVE_ERROR_INVALID_ARGUMENT
+
+
+def test_null_handle_calls():
+    L = cve.lib
+    buf = np.zeros(8 * 8 * 3, dtype=np.uint8)
+    assert L.cve_cipher_encrypt_frame(None, buf.ctypes.data, 8) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_decrypt_frame(None, buf.ctypes.data, 8) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_encrypt_frames(None, buf.ctypes.data, 8, 1) == cve.CVE_ERROR_INVALID_ARGUMENT
+    v = C.c_uint64()
+    assert L.cve_cipher_seeds_drawn(None, C.byref(v)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    L.cve_cipher_destroy(None)
+
+
+@pytest.mark.skipif(gpu_present(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback_without_gpu():
+    with pytest.raises(cve.CveError) as e:
+        cve.Cipher(PLCM, 8, 5)
+    assert e.value.status == cve.CVE_ERROR_INTERNAL
+
+
+def test_host_keying_matches_reference_goldens():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_unit.json")))
+    w = g["worker_params_n2"]
+    lanes, seeds = cve.derive_worker_lanes(w["key"], 2, 3)
+    assert lanes.tolist() == w["lanes"]
+    assert seeds.tolist() == w["seeds"]
+
+
+@pytest.mark.parametrize("workers", [1, 8, 64, 128])
+def test_host_keying_matches_oracle(workers):
+    from _oracle import Oracle
+    from paper_2302_07411_b200 import synth
+    key = synth.det_key(workers + 77)
+    lanes, seeds = cve.derive_worker_lanes(key, workers, 5)
+    o = Oracle(key, workers)
+    assert np.array_equal(lanes, o.params())
+    assert seeds.tolist() == [Oracle.lib.orc_cipher_next_seed(o.h) for _ in range(5)]
+
+
+def test_lasm_key_rejected_by_engine():
+    with pytest.raises(cve.CveError) as e:
+        cve.derive_worker_lanes(LASM, 1, 0)
+    assert e.value.status == cve.CVE_ERROR_INVALID_ARGUMENT
+
+
+def test_frame_model():
+    assert cve.padded_side(1920, 1080, 64) == 1920
+    assert cve.padded_side(3840, 2160, 128) == 3840
+    img = np.arange(5 * 7 * 3, dtype=np.uint8).reshape(5, 7, 3)
+    sq = cve.pad_to_square(img, 4)
+    assert sq.shape == (8, 8, 3) and not sq[5:].any() and not sq[:, 7:].any()
+    assert np.array_equal(cve.crop_to_original(sq, 7, 5), img)

@@ -1,0 +1,239 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Checkers: the oracle (oracle/cve_oracle.c, itself pinned in test_oracle.py),
+the reference's compiled library when present, and the committed digests of
+the reference's ciphertext (tests/golden).  Bar: bit-exact bytes.
+Full-size configs are checked against golden digests for their first frames
+and through size-independent properties (round trip, all-zero fixed point,
+key sensitivity, batch == per-frame == device-resident).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2302_07411_b200 as cve
+from paper_2302_07411_b200 import synth
+from _oracle import Oracle, plcm_stream
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+PLCM = "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f"
+
+
+def load(name):
+    with open(os.path.join(GOLD, name)) as fh:
+        return json.load(fh)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rand_frames(side, count, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.integers(0, 256, (count, side, side, 3), dtype=np.uint8)
+
+
+# ---- K1: keystream generator ----------------------------------------------
+
+def test_keystream_golden_48():
+    g = load("reference_unit.json")["plcm_golden_48"]
+    assert cve.keystream_generate(g["lanes"], 48).tobytes().hex() == g["bytes"]
+
+
+def test_keystream_random_lanes_vs_oracle():
+    # test_chaos.cpp:125-137 shape, longer streams (exercise many blocks)
+    rng = np.random.Generator(np.random.PCG64(21))
+    for _ in range(6):
+        xa, xb = rng.uniform(0, 1, 2)
+        pa, pb = rng.uniform(0.01, 0.49, 2)
+        n = 300_007
+        assert np.array_equal(cve.keystream_generate([xa, pa, xb, pb], n),
+                              plcm_stream(xa, pa, xb, pb, n))
+
+
+def test_keystream_guard_cases():
+    # test_chaos.cpp:185-213: identical lanes cancel; endpoint seeds collapse
+    # onto one guarded orbit; guarded degenerate seeds vary.  p = 0.25 with
+    # x = 0.0625 hits the guard set inside the orbit (x/p == p).
+    assert not cve.keystream_generate([0.3, 0.2, 0.3, 0.2], 600).any()
+    a = cve.keystream_generate([0.0, 0.3, 0.25, 0.2], 256)
+    b = cve.keystream_generate([1.0, 0.3, 0.25, 0.2], 256)
+    c = cve.keystream_generate([0.123, 0.3, 0.25, 0.2], 256)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+    for lanes in ([0.0, 0.3, 0.41, 0.17], [0.5, 0.3, 0.41, 0.17], [1.0, 0.3, 0.41, 0.17],
+                  [0.3, 0.3, 0.41, 0.17], [0.0625, 0.25, 0.125, 0.25], [0.5, 0.25, 0.75, 0.125],
+                  [0.2, 0.4, 0.6, 0.1]):
+        got = cve.keystream_generate(lanes, 4800)
+        assert np.array_equal(got, plcm_stream(*lanes, 4800)), lanes
+
+
+def test_keystream_bad_lanes():
+    with pytest.raises(cve.CveError) as e:
+        cve.keystream_generate([0.3, 0.5, 0.2, 0.2], 16)
+    assert e.value.status == cve.CVE_ERROR_BAD_KEY
+
+
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_worker_streams_vs_golden(name):
+    digests = load("small.json")["worker_stream_sha256_1MiB"][name]
+    c = cve.Cipher(synth.config_key(name), synth.CONFIGS[name]["workers"], 5)
+    for i, d in enumerate(digests):
+        assert hashlib.sha256(c.peek_keystream(i, 1 << 20).tobytes()).hexdigest() == d, i
+    assert c.seeds_drawn == 0  # peeking consumes nothing
+
+
+# ---- K2/K3/K4: whole frames ------------------------------------------------
+
+@pytest.mark.parametrize("case", range(6))
+def test_small_cases_vs_reference(case):
+    c = load("small.json")["cases"][case]
+    side, n, r = c["side"], c["workers"], c["rounds"]
+    enc, dec = cve.Cipher(c["key"], n, r), cve.Cipher(c["key"], n, r, parallel=False)
+    for p_hex, c_hex in zip(c["plain"], c["cipher"]):
+        x = np.frombuffer(bytes.fromhex(p_hex), np.uint8).reshape(side, side, 3).copy()
+        enc.encrypt_frame(x)
+        assert x.tobytes().hex() == c_hex
+        dec.decrypt_frame(x)
+        assert x.tobytes().hex() == p_hex
+    assert enc.seeds_drawn == len(c["plain"])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_config_clip_vs_reference_digests(name):
+    g = load("frames.json")[name]
+    frames = np.stack(synth.frame_list(name, len(g["cipher_sha256"])))
+    c = cve.Cipher(g["key"], g["workers"], g["rounds"])
+    per = frames.copy()
+    for t in range(len(per)):
+        c.encrypt_frame(per[t])
+        assert sha(per[t]) == g["cipher_sha256"][t], t
+    batch = frames.copy()
+    cve.Cipher(g["key"], g["workers"], g["rounds"]).encrypt_frames(batch)
+    assert np.array_equal(batch, per)
+    d = cve.Cipher(g["key"], g["workers"], g["rounds"])
+    d.decrypt_frames(batch)
+    assert np.array_equal(batch, frames)
+
+
+def test_device_resident_api_matches_host_api():
+    torch = pytest.importorskip("torch")
+    g = load("frames.json")["C2"]
+    frames = np.stack(synth.frame_list("C2", 8))
+    dev = torch.from_numpy(frames.copy()).cuda()
+    c = cve.Cipher(g["key"], g["workers"], 5)
+    s = torch.cuda.current_stream()
+    c.encrypt_frames_device(dev.data_ptr(), frames.shape[1], 4, s.cuda_stream)
+    c.encrypt_frames_device(dev.data_ptr() + 4 * frames[0].nbytes, frames.shape[1], 4,
+                            s.cuda_stream)
+    out = dev.cpu().numpy()  # ordered after the cipher on the same stream
+    for t in range(8):
+        assert sha(out[t]) == g["cipher_sha256"][t]
+    d = cve.Cipher(g["key"], g["workers"], 5)
+    d.decrypt_frames_device(dev.data_ptr(), frames.shape[1], 8, s.cuda_stream)
+    assert np.array_equal(dev.cpu().numpy(), frames)
+
+
+@pytest.mark.parametrize("side,n,r", [
+    (8, 2, 3), (16, 4, 1), (24, 4, 5), (30, 3, 5), (7, 7, 5), (97, 1, 2),
+    (100, 4, 5), (192, 12, 5), (256, 128, 5), (64, 64, 5), (1000, 1, 2),
+    (600, 1, 5), (480, 8, 1), (484, 4, 4)])
+def test_random_shapes_vs_oracle(side, n, r):
+    key = synth.det_key(side * 131 + n * 7 + r)
+    frames = rand_frames(side, 3, side + n)
+    o = Oracle(key, n, r)
+    c = cve.Cipher(key, n, r)
+    for f in frames:
+        a, b = f.copy(), f.copy()
+        assert o.encrypt(a) == 0
+        c.encrypt_frame(b)
+        assert np.array_equal(a, b)
+    # cross decryption: oracle ciphertext -> GPU decrypt
+    o2, d = Oracle(key, n, r), cve.Cipher(key, n, r)
+    for f in frames:
+        a = f.copy()
+        assert o2.encrypt(a) == 0
+        d.decrypt_frame(a)
+        assert np.array_equal(a, f)
+
+
+def test_mixed_sides_on_one_handle():
+    # stream continuity across frames of different sizes (ring growth)
+    key = synth.det_key(4242)
+    o, c = Oracle(key, 4), cve.Cipher(key, 4)
+    rng = np.random.Generator(np.random.PCG64(5))
+    for side in (16, 480, 32, 960, 8, 200, 1024):
+        f = rng.integers(0, 256, (side, side, 3), dtype=np.uint8)
+        a, b = f.copy(), f.copy()
+        assert o.encrypt(a) == 0
+        c.encrypt_frame(b)
+        assert np.array_equal(a, b), side
+    assert c.seeds_drawn == o.seeds_drawn == 7
+
+
+def test_error_semantics_match_reference():
+    # test_capi.cpp:116-162
+    c = cve.Cipher(PLCM, 2, 3)
+    assert c.seeds_drawn == 0
+    odd = rand_frames(7, 1, 2)[0]
+    with pytest.raises(cve.CveError) as e:
+        c.encrypt_frame(odd)
+    assert e.value.status == cve.CVE_ERROR_MISMATCH
+    assert c.seeds_drawn == 1  # seed drawn before the side check
+    # the next frame binds to frame index 1 in both implementations
+    o = Oracle(PLCM, 2, 3)
+    assert o.encrypt(odd.copy()) == 5
+    f = rand_frames(8, 1, 3)[0]
+    a, b = f.copy(), f.copy()
+    o.encrypt(a)
+    c.encrypt_frame(b)
+    assert np.array_equal(a, b)
+    batch = rand_frames(9, 2, 4)
+    with pytest.raises(cve.CveError) as e:
+        c.encrypt_frames(batch)
+    assert e.value.status == cve.CVE_ERROR_MISMATCH
+    assert c.seeds_drawn == 3
+
+
+def test_key_flip_sensitivity_c3():
+    g = load("frames.json")["C3"]
+    f = synth.config_frame("C3", 0)
+    a, b = f.copy(), f.copy()
+    cve.Cipher(g["key"], 32).encrypt_frame(a)
+    cve.Cipher(g["flip_key"], 32).encrypt_frame(b)
+    assert sha(b) == g["flip_cipher_sha256"]
+    frac = float((a != b).mean())
+    assert abs(frac - g["flip_differ_fraction"]) < 1e-12 and frac > 0.99
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_configs(name):
+    g = load("frames.json")[name]
+    k = len(g["cipher_sha256"])
+    frames = np.stack(synth.frame_list(name, k + 1))
+    c = cve.Cipher(g["key"], g["workers"], 5)
+    ct = frames.copy()
+    c.encrypt_frames(ct)
+    for t in range(k):
+        assert sha(ct[t]) == g["cipher_sha256"][t], t
+    if name == "C5":
+        assert not ct[0].any(), "all-zero frame must encrypt to all zeros"
+        assert abs(float((ct[1] == 255).mean()) - g["full_frame_fraction_255"]) < 1e-12
+    d = cve.Cipher(g["key"], g["workers"], 5)
+    d.decrypt_frames(ct)
+    assert np.array_equal(ct, frames)
+
+
+def test_stats_and_launch_accounting():
+    c = cve.Cipher(synth.config_key("C1"), 8, 5)
+    f = synth.config_frame("C1", 0)
+    c.encrypt_frame(f)
+    s = c.stats()
+    assert s["frames"] == 1 and s["prbg_launches"] >= 1
+    assert s["keystream_iters"] * 6 >= 5 * 480 * 480 * 3 // 8
+    assert s["kernel_launches"] >= 1 + 5 + s["prbg_launches"]
+    assert s["prbg_ms"] > 0 and s["cipher_ms"] > 0
