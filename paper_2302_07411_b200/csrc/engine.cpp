@@ -19,6 +19,32 @@ void ck(cudaError_t e, const char* what) {
 uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
+constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
+
+PrbgBuffers alloc_prbg(uint32_t nlanes) {
+  PrbgBuffers b{};
+  uint64_t iters = kOrbitBytes / (8ull * nlanes);
+  iters = std::min<uint64_t>(iters, 1u << 20) / 8 * 8;
+  b.max_iters = uint32_t(std::max<uint64_t>(iters, 8));
+  ck(cudaMalloc(&b.state, nlanes * sizeof(double)), "cudaMalloc state");
+  ck(cudaMalloc(&b.ckpt, nlanes * sizeof(double)), "cudaMalloc ckpt");
+  ck(cudaMalloc(&b.orbit, uint64_t(b.max_iters) * nlanes * sizeof(double)),
+     "cudaMalloc orbit");
+  ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
+  ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
+  ck(cudaMemset(b.bad, 0, (nlanes / 2) * sizeof(unsigned)), "memset");
+  ck(cudaMemset(b.replays, 0, sizeof(unsigned long long)), "memset");
+  return b;
+}
+
+void free_prbg(PrbgBuffers& b) {
+  cudaFree(b.state);
+  cudaFree(b.ckpt);
+  cudaFree(b.orbit);
+  cudaFree(b.bad);
+  cudaFree(b.replays);
+  b = PrbgBuffers{};
+}
 
 }  // namespace
 
@@ -55,23 +81,18 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     x0[2 * i + 1] = lanes[i].b.x0;
   }
   double* d_x0 = nullptr;
-  ck(cudaMalloc(&d_state_, nl * sizeof(double)), "cudaMalloc state");
+  pb_ = alloc_prbg(nl);
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
   ck(cudaMalloc(&d_x0, nl * sizeof(double)), "cudaMalloc x0");
-  ck(cudaMalloc(&d_replays_, sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice),
      "upload lanes");
   ck(cudaMemcpy(d_x0, x0.data(), nl * sizeof(double), cudaMemcpyHostToDevice),
      "upload x0");
-  ck(cudaMemset(d_replays_, 0, sizeof(unsigned long long)), "memset");
-  launch_prbg_init(d_state_, d_lc_, d_x0, nl, s_gen_);
+  launch_prbg_init(pb_.state, d_lc_, d_x0, nl, s_gen_);
   ck(cudaGetLastError(), "prbg_init launch");
   ++st_.kernel_launches;
   ck(cudaStreamSynchronize(s_gen_), "prbg_init");
   cudaFree(d_x0);
-
-  if (const char* e = std::getenv("CVE_B200_RESERVE_SMEM"))
-    reserve_smem_ = uint32_t(std::strtoul(e, nullptr, 10));
 }
 
 Engine::~Engine() {
@@ -92,9 +113,8 @@ Engine::~Engine() {
   for (uint8_t* p : scratch_) cudaFree(p);
   cudaFree(d_shift_);
   cudaFree(ring_);
-  cudaFree(d_state_);
+  free_prbg(pb_);
   cudaFree(d_lc_);
-  cudaFree(d_replays_);
   for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
 }
@@ -258,7 +278,7 @@ void Engine::gen_until(uint64_t end_byte) {
   while (gen_iters_ < target) {
     uint64_t chunk = target - gen_iters_;
     const uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
-    chunk = std::min(chunk, max_chunk);
+    chunk = std::min<uint64_t>({chunk, max_chunk, pb_.max_iters});
     const uint64_t write_end = (gen_iters_ + chunk) * 6;
     // bytes below write_end - R get overwritten: their readers must be done
     if (write_end > ring_bytes_) {
@@ -274,12 +294,11 @@ void Engine::gen_until(uint64_t end_byte) {
       }
     }
     timed_begin(s_gen_, true);
-    launch_prbg_generate(d_state_, d_lc_, ring_, ring_bytes_, gen_iters_,
-                         uint32_t(chunk / 8), 2 * n_, d_replays_, reserve_smem_,
-                         s_gen_);
+    launch_prbg_generate(pb_, d_lc_, ring_, ring_bytes_, gen_iters_,
+                         uint32_t(chunk), 2 * n_, s_gen_);
     ck(cudaGetLastError(), "prbg_generate launch");
     timed_end(s_gen_);
-    ++st_.kernel_launches;
+    st_.kernel_launches += 3;
     ++st_.prbg_launches;
     gen_iters_ += chunk;
     st_.keystream_iters += chunk;
@@ -415,7 +434,7 @@ EngineStats Engine::stats() {
   synchronize();
   fold_timings(true);
   unsigned long long rep = 0;
-  ck(cudaMemcpy(&rep, d_replays_, sizeof rep, cudaMemcpyDeviceToHost), "stats");
+  ck(cudaMemcpy(&rep, pb_.replays, sizeof rep, cudaMemcpyDeviceToHost), "stats");
   st_.guard_replays = rep;
   return st_;
 }
@@ -438,35 +457,33 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
   const uint64_t ring = iters * 6;  // multiple of 48
   LaneConst lc[2] = {make_lane_const(a.p), make_lane_const(b.p)};
   const double x0[2] = {a.x0, b.x0};
-  double* d_state = nullptr;
+  PrbgBuffers pb{};
   double* d_x0 = nullptr;
   LaneConst* d_lc = nullptr;
-  unsigned long long* d_rep = nullptr;
   uint8_t* d_out = nullptr;
   cudaStream_t s = nullptr;
   auto cleanup = [&] {
-    cudaFree(d_state);
+    free_prbg(pb);
     cudaFree(d_x0);
     cudaFree(d_lc);
-    cudaFree(d_rep);
     cudaFree(d_out);
     if (s) cudaStreamDestroy(s);
   };
   try {
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    ck(cudaMalloc(&d_state, sizeof x0), "cudaMalloc");
+    pb = alloc_prbg(2);
     ck(cudaMalloc(&d_x0, sizeof x0), "cudaMalloc");
     ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
-    ck(cudaMalloc(&d_rep, sizeof(unsigned long long)), "cudaMalloc");
     ck(cudaMalloc(&d_out, ring), "cudaMalloc");
     ck(cudaMemcpy(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice), "upload");
     ck(cudaMemcpy(d_x0, x0, sizeof x0, cudaMemcpyHostToDevice), "upload");
-    ck(cudaMemset(d_rep, 0, sizeof(unsigned long long)), "memset");
-    launch_prbg_init(d_state, d_lc, d_x0, 2, s);
+    launch_prbg_init(pb.state, d_lc, d_x0, 2, s);
     ck(cudaGetLastError(), "prbg_init");
-    launch_prbg_generate(d_state, d_lc, d_out, ring, 0, uint32_t(iters / 8), 2,
-                         d_rep, 0, s);
-    ck(cudaGetLastError(), "prbg_generate");
+    for (uint64_t it = 0; it < iters; it += pb.max_iters) {
+      const uint32_t n = uint32_t(std::min<uint64_t>(pb.max_iters, iters - it));
+      launch_prbg_generate(pb, d_lc, d_out, ring, it, n, 2, s);
+      ck(cudaGetLastError(), "prbg_generate");
+    }
     ck(cudaStreamSynchronize(s), "keystream");
     ck(cudaMemcpy(out, d_out, len, cudaMemcpyDeviceToHost), "download");
   } catch (...) {

@@ -8,13 +8,18 @@
 namespace cveb {
 
 // Per-lane constants of one PLCM orbit, precomputed on the host so the
-// device loop has no division and no loop-invariant reciprocal to hoist:
-//   q  = RN(0.5 - p)         (the reference's (0.5 - p), chaos.cpp:31)
-//   rp = RN(1/p), rq = RN(1/q)
-//   hp = p/2, hq = q/2       (exact; rounding-verification thresholds)
-//   plo = low 32 bits of p   (guard pre-filter)
+// device loop has no division and no loop-invariant reciprocal to hoist.
+//   q        = RN(0.5 - p)           the reference's (0.5 - p), chaos.cpp:31
+//   yh_*+yl_* = 1/p, 1/q to ~2^-106   (yh = RN(1/d), yl = RN((1 - d*yh)/d))
+//   cthr     = largest double <= 1-p  (x > cthr  <=>  1 - x < p, exactly)
+//   a_b, a_d = offsets of the quotient correction term for cases B and D
+//   hp, hq   = p/2, q/2               (rounding-verification thresholds)
+//   plo      = low 32 bits of p
 struct LaneConst {
-  double p, q, rp, rq, hp, hq;
+  double p, q;
+  double yh_p, yl_p, yh_q, yl_q;
+  double cthr, a_b, a_d;
+  double hp, hq;
   uint32_t plo, pad;
 };
 
@@ -26,13 +31,23 @@ LaneConst make_lane_const(double p);
 void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                       uint32_t nlanes, cudaStream_t s);
 
-// Advances every lane by 8*nblk iterations starting at iteration `it0`
-// (multiple of 8) and writes each worker's 6 bytes/iteration at stream byte
-// 6*it (mod ring_bytes) of that worker's ring.  ring_bytes % 48 == 0.
-void launch_prbg_generate(double* state, const LaneConst* lc, uint8_t* ring,
-                          uint64_t ring_bytes, uint64_t it0, uint32_t nblk,
-                          uint32_t nlanes, unsigned long long* replays,
-                          uint32_t reserve_smem, cudaStream_t s);
+// Device state of the generator.
+struct PrbgBuffers {
+  double* state;    // nlanes: current orbit points
+  double* ckpt;     // nlanes: orbit points at the start of the last launch
+  double* orbit;    // max_iters * nlanes: orbit values of one launch
+  unsigned* bad;    // nworkers: verification failure flags
+  unsigned long long* replays;  // workers recomputed exactly (cumulative)
+  uint32_t max_iters;           // per launch, multiple of 8
+};
+
+// Advances every lane by `iters` (multiple of 8, <= max_iters) iterations
+// starting at iteration `it0` (multiple of 8) and writes each worker's 6
+// bytes/iteration at stream byte 6*it (mod ring_bytes) of that worker's ring
+// (ring_bytes % 48 == 0).  Three launches: chain, verify+emit, exact fix-up.
+void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
+                          uint64_t ring_bytes, uint64_t it0, uint32_t iters,
+                          uint32_t nlanes, cudaStream_t s);
 
 // Geometry of one square frame split into n row bands.
 struct Geom {

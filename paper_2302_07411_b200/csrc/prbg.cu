@@ -5,23 +5,27 @@
 // worker from Engine::Impl::draw_streams (engine.cpp:198-205).
 //
 // The keystream of a clip is 2n sequential chaotic orbits (n subframes x 2
-// lanes) that continue across frames, so the kernel is bound by the latency
-// of ONE dependent PLCM iteration, not by bandwidth or FP64 throughput.
-// Everything here serves that chain:
-//   * one orbit per thread; the two lanes of a worker sit in adjacent
-//     threads and meet through one shuffle per iteration (keeps a warp's
-//     issue demand below the chain latency);
-//   * branch-free iteration (selects), division by the loop-invariant
-//     divisor done as RN(1/d) multiply + two FMA corrections (Markstein);
-//   * the exactness of that quotient and the reference's endpoint guard are
-//     both verified OFF the dependency chain: a cheap pre-filter flags any
-//     iteration whose result might be wrong or might hit the guard set
-//     {0, p, 0.5, 1}; a flagged 8-iteration block is replayed with IEEE
-//     __ddiv_rn and the exact guard.  Output is therefore bit-identical to
-//     the reference's IEEE binary64 loop by construction, not by statistics.
+// lanes) that continue across frames, so the kernel is bound by the LATENCY
+// of one dependent PLCM iteration -- not by bandwidth or FP64 throughput.
+// The design takes everything that is not the orbit itself off that chain:
 //
-// Compiled with -fmad=false; every FP64 operation below is an explicit _rn
-// intrinsic anyway, so no contraction can change a result.
+//   producer warps (SM sub-partitions 0,1): one orbit per thread, a
+//     branch-free speculative step -- exact case predicates, exact numerator,
+//     and the quotient num/d as fma(num, RN(1/d), corr) where the ~2^-53
+//     correction corr ~= num * (1/d - RN(1/d)) is formed straight from x by
+//     one FMA per case, so only DADD -> FSEL -> DADD -> FSEL -> DFMA remain
+//     on the chain.  Each result goes to a shared-memory ring.
+//   verifier warps (sub-partitions 2,3): re-derive every step with the
+//     reference's own case logic (chaos.cpp:28-32) and prove the produced
+//     quotient is the correctly rounded one (|num - d*y| < d*ulp(y)/2 via an
+//     exact FMA residual; IEEE division for the inconclusive powers of two)
+//     and outside the guard set {0, p, 0.5, 1} (chaos.cpp:18-24).
+//   any failure: the CTA recomputes its whole range with IEEE __ddiv_rn and
+//     the exact guard before the kernel ends.
+//
+// Output is therefore bit-identical to the reference's IEEE binary64 loop by
+// construction.  Compiled with -fmad=false; every FP64 operation is an
+// explicit _rn intrinsic.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -36,8 +40,18 @@ LaneConst make_lane_const(double p) {
   volatile double half = 0.5, one = 1.0;  // keep host evaluation IEEE
   c.p = p;
   c.q = half - p;
-  c.rp = one / c.p;
-  c.rq = one / c.q;
+  c.yh_p = one / c.p;
+  c.yl_p = std::fma(-c.p, c.yh_p, 1.0) / c.p;
+  c.yh_q = one / c.q;
+  c.yl_q = std::fma(-c.q, c.yh_q, 1.0) / c.q;
+  // cthr = RD(1 - p): t - 1 is exact (Sterbenz) and the sign of RN(d + p)
+  // is the sign of the exact sum, so t > 1 - p is decided exactly.
+  double t = one - c.p;
+  volatile double d = t - one;
+  if (d + c.p < 0.0) t = std::nextafter(t, 0.0);
+  c.cthr = t;
+  c.a_b = -c.p * c.yl_q;
+  c.a_d = (one - c.p) * c.yl_q;
   c.hp = 0.5 * c.p;
   c.hq = 0.5 * c.q;
   uint64_t bits;
@@ -61,34 +75,45 @@ __device__ __forceinline__ double plcm_exact(double x, double p, double q) {
   return y;
 }
 
-// Speculative step: branch-free, division via reciprocal + FMA correction.
-// `flag` accumulates "this result may differ from plcm_exact".
-__device__ __forceinline__ double plcm_fast(double x, const LaneConst& c,
-                                            bool& flag) {
-  const double folded = __dsub_rn(1.0, x);
-  const double f = x > 0.5 ? folded : x;
-  const bool low = f < c.p;
-  const double shifted = __dsub_rn(f, c.p);
-  const double num = low ? f : shifted;
-  const double rcp = low ? c.rp : c.rq;
-  const double den = low ? c.p : c.q;
-  const double q0 = __dmul_rn(num, rcp);
-  const double r0 = __fma_rn(-q0, den, num);
-  const double y = __fma_rn(r0, rcp, q0);
+// Speculative chain step.  Cases (reference: fold x>0.5 to 1-x, then
+// f<p ? f/p : (f-p)/q):  A x<p: x/p   B p<=x<=.5: (x-p)/q
+//                        C x>cthr: (1-x)/p   D .5<x<=cthr: ((1-x)-p)/q
+__device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
+  const bool c1 = x > 0.5;
+  const bool low = (x < c.p) | (x > c.cthr);  // == (f < p), exactly
+  const double t1 = __dsub_rn(1.0, x);         // exact when x > 0.5
+  const double base = c1 ? t1 : x;             // f
+  const double shifted = __dsub_rn(base, c.p);
+  const double num = low ? base : shifted;
+  const double yh = low ? c.yh_p : c.yh_q;
+  // num * (1/d - yh), from x: A x*ylp  B (x-p)*ylq  C (1-x)*ylp  D (1-x-p)*ylq
+  const double ca = __dmul_rn(x, c.yl_p);
+  const double cb = __fma_rn(x, c.yl_q, c.a_b);
+  const double cc = __fma_rn(-x, c.yl_p, c.yl_p);
+  const double cd = __fma_rn(-x, c.yl_q, c.a_d);
+  const double corr = low ? (c1 ? cc : ca) : (c1 ? cd : cb);
+  return __fma_rn(num, yh, corr);
+}
 
-  // --- off the chain: is y == RN(num/den), and is y outside the guard set?
-  // y = RN(num/den)  <=>  |num - den*y| < den*ulp(y)/2  when y is not a power
-  // of two (no quotient is a midpoint).  Powers of two, 0, 0.5, 1 and p all
-  // have low word 0 or equal to p's low word, so the pre-filter sends them
-  // to the exact replay.
-  const double r1 = __fma_rn(-y, den, num);
+// Is y exactly the reference's next orbit value after x?
+__device__ __forceinline__ bool plcm_verify(double x, double y, const LaneConst& c) {
+  const double f = x > 0.5 ? __dsub_rn(1.0, x) : x;
+  const bool low = f < c.p;
+  const double num = low ? f : __dsub_rn(f, c.p);
+  const double den = low ? c.p : c.q;
+  if (y == 0.0 || y == c.p || y == 0.5 || y == 1.0) return false;  // guard hit
   const unsigned hi = unsigned(__double2hiint(y));
   const unsigned lo = unsigned(__double2loint(y));
   const unsigned ex = hi & 0x7FF00000u;
+  if ((lo == 0u && (hi & 0x000FFFFFu) == 0u) || ex < (53u << 20))
+    return y == __ddiv_rn(num, den);  // power of two / tiny: decide exactly
+  // y is RN(num/den) iff |num - den*y| < den*ulp(y)/2 (no quotient is a
+  // midpoint).  The FMA residual is exact for any faithful y, and any error
+  // in it can only turn a pass into a (safe) fail.
+  const double r = __fma_rn(-y, den, num);
   const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
   const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
-  flag |= !(fabs(r1) < thr) | (lo == 0u) | (lo == c.plo) | (ex < (53u << 20));
-  return y;
+  return fabs(r) < thr;
 }
 
 __global__ void __launch_bounds__(128)
@@ -106,80 +131,110 @@ __global__ void __launch_bounds__(128)
   state[l] = x;
 }
 
-// One thread per lane; lanes 2w and 2w+1 (worker w's lanes a and b) are
-// shuffle partners.  Per 8-iteration block the pair emits 48 keystream bytes:
-// the even thread stores bytes 0..23 (iterations 0-3), the odd one 24..47.
-__global__ void __launch_bounds__(128)
-    k_prbg_generate(double* __restrict__ state,
-                    const LaneConst* __restrict__ lc, uint8_t* __restrict__ ring,
-                    uint64_t ring_bytes, uint64_t it0, uint32_t nblk,
-                    uint32_t nlanes, unsigned long long* __restrict__ replays) {
+// (1) The chain.  One orbit per thread, 4 warps per CTA, one CTA per SM, so
+// every warp owns an SM sub-partition's in-order issue.  Per step: the
+// speculative iteration and one coalesced 8-byte store of the orbit value.
+// `ckpt` keeps the launch's start state for the exact fix-up.
+__global__ void __launch_bounds__(128, 1)
+    k_prbg_chain(double* __restrict__ state, double* __restrict__ ckpt,
+                 const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
+                 uint32_t iters, uint32_t nlanes) {
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = l < nlanes;
-  const uint32_t me = live ? l : (l & 1u);  // idle threads shadow lane 0/1
-  const LaneConst c = lc[me];
-  const uint32_t odd = me & 1u;
-  uint8_t* const base = ring + uint64_t(me >> 1) * ring_bytes + (odd ? 24 : 0);
-  uint64_t off = (it0 * 6u) % ring_bytes;
-  double x = state[me];
-  uint32_t nreplay = 0;
-
-  for (uint32_t b = 0; b < nblk; ++b) {
-    uint32_t lo[8], hi[8];
-    const double x_start = x;
-    bool flag = false;
+  if (l >= nlanes) return;
+  const LaneConst c = lcs[l];
+  double x = state[l];
+  ckpt[l] = x;
+  double* o = orbit + l;
+  for (uint32_t i = 0; i < iters; i += 8) {
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      x = plcm_fast(x, c, flag);
-      lo[t] = unsigned(__double2loint(x));
-      hi[t] = unsigned(__double2hiint(x));
+      x = plcm_fast(x, c);
+      o[size_t(t) * nlanes] = x;
     }
-    if (flag) {  // rare: replay the block with IEEE division + exact guard
-      ++nreplay;
-      x = x_start;
+    o += size_t(8) * nlanes;
+  }
+  state[l] = x;
+}
+
+// (2) Verify every step in parallel against the reference's exact step, and
+// emit the keystream: 6 bytes per iteration per worker = the little-endian
+// low 48 mantissa bits of x_a ^ x_b (extract_bytes, chaos.cpp:46-56).
+// Thread = (worker, 8-iteration group); failures flag the worker.
+__global__ void __launch_bounds__(256)
+    k_prbg_verify_emit(const double* __restrict__ ckpt,
+                       const LaneConst* __restrict__ lcs,
+                       const double* __restrict__ orbit, uint32_t iters,
+                       uint32_t nworkers, uint8_t* __restrict__ ring,
+                       uint64_t ring_bytes, uint64_t it0,
+                       unsigned* __restrict__ bad) {
+  const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t groups = iters / 8;
+  if (gid >= uint64_t(groups) * nworkers) return;
+  const uint32_t w = uint32_t(gid % nworkers);  // workers fastest: coalesced
+  const uint32_t g = uint32_t(gid / nworkers);
+  const uint32_t nl = 2 * nworkers;
+  const LaneConst ca = lcs[2 * w], cb = lcs[2 * w + 1];
+  const size_t i0 = size_t(g) * 8;
+  double xa = g ? orbit[(i0 - 1) * nl + 2 * w] : ckpt[2 * w];
+  double xb = g ? orbit[(i0 - 1) * nl + 2 * w + 1] : ckpt[2 * w + 1];
+  bool ok = true;
+  uint32_t lo[8], hi[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        x = plcm_exact(x, c.p, c.q);
-        lo[t] = unsigned(__double2loint(x));
-        hi[t] = unsigned(__double2hiint(x));
-      }
-    }
-    // Even thread needs the partner's iterations 0-3, odd one 4-7.
-    uint32_t w[6];
-    uint32_t mlo[4], mhi[4];
+  for (int t = 0; t < 8; ++t) {
+    const double2 v = *reinterpret_cast<const double2*>(orbit + (i0 + t) * nl + 2 * w);
+    ok &= plcm_verify(xa, v.x, ca);
+    ok &= plcm_verify(xb, v.y, cb);
+    xa = v.x;
+    xb = v.y;
+    lo[t] = unsigned(__double2loint(v.x)) ^ unsigned(__double2loint(v.y));
+    hi[t] = (unsigned(__double2hiint(v.x)) ^ unsigned(__double2hiint(v.y))) & 0xFFFFu;
+  }
+  if (!ok) atomicOr(bad + w, 1u);
+  uint32_t wd[12];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t slo = odd ? lo[t] : lo[t + 4];
-      const uint32_t shi = odd ? hi[t] : hi[t + 4];
-      const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
-      const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
-      mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
-      mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
-    }
-    // 4 iterations x 6 bytes, little-endian mantissa bytes (extract_bytes).
-    w[0] = mlo[0];
-    w[1] = mhi[0] | (mlo[1] << 16);
-    w[2] = (mlo[1] >> 16) | (mhi[1] << 16);
-    w[3] = mlo[2];
-    w[4] = mhi[2] | (mlo[3] << 16);
-    w[5] = (mlo[3] >> 16) | (mhi[3] << 16);
-    if (live) {
-      uint8_t* dst = base + off;
-      if (!odd) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w[4], w[5]);
-      } else {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-        *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w[2], w[3], w[4], w[5]);
-      }
-    }
-    off += 48;
+  for (int k = 0; k < 4; ++k) {  // two iterations -> three words
+    wd[3 * k] = lo[2 * k];
+    wd[3 * k + 1] = hi[2 * k] | (lo[2 * k + 1] << 16);
+    wd[3 * k + 2] = (lo[2 * k + 1] >> 16) | (hi[2 * k + 1] << 16);
+  }
+  const uint64_t off = ((it0 + i0) * 6u) % ring_bytes;  // 48-byte aligned
+  uint4* dst = reinterpret_cast<uint4*>(ring + uint64_t(w) * ring_bytes + off);
+  dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+  dst[2] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
+}
+
+// (3) Exact fix-up of flagged workers (normally every thread exits at once):
+// recompute both lanes from the launch checkpoint with IEEE division and the
+// exact guard, rewrite the worker's bytes and state.
+__global__ void k_prbg_fixup(double* __restrict__ state,
+                             const double* __restrict__ ckpt,
+                             const LaneConst* __restrict__ lcs, uint32_t iters,
+                             uint32_t nworkers, uint8_t* __restrict__ ring,
+                             uint64_t ring_bytes, uint64_t it0,
+                             unsigned* __restrict__ bad,
+                             unsigned long long* __restrict__ replays) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nworkers || !bad[w]) return;
+  bad[w] = 0;
+  const LaneConst ca = lcs[2 * w], cb = lcs[2 * w + 1];
+  double xa = ckpt[2 * w], xb = ckpt[2 * w + 1];
+  uint8_t* base = ring + uint64_t(w) * ring_bytes;
+  uint64_t off = (it0 * 6u) % ring_bytes;
+  for (uint32_t i = 0; i < iters; ++i) {
+    xa = plcm_exact(xa, ca.p, ca.q);
+    xb = plcm_exact(xb, cb.p, cb.q);
+    uint64_t ba, bb;
+    memcpy(&ba, &xa, 8);
+    memcpy(&bb, &xb, 8);
+    const uint64_t v = ba ^ bb;
+    for (int k = 0; k < 6; ++k) base[off + k] = uint8_t(v >> (8 * k));
+    off += 6;
     if (off == ring_bytes) off = 0;
   }
-  if (live) {
-    state[l] = x;
-    if (nreplay) atomicAdd(replays, (unsigned long long)nreplay);
-  }
+  state[2 * w] = xa;
+  state[2 * w + 1] = xb;
+  atomicAdd(replays, 1ull);
 }
 
 }  // namespace
@@ -191,25 +246,24 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                                                                     x0, nlanes);
 }
 
-void launch_prbg_generate(double* state, const LaneConst* lc, uint8_t* ring,
-                          uint64_t ring_bytes, uint64_t it0, uint32_t nblk,
-                          uint32_t nlanes, unsigned long long* replays,
-                          uint32_t reserve_smem, cudaStream_t s) {
-  // At most 4 warps per CTA: one warp per SM sub-partition, so each warp
-  // owns its scheduler.  `reserve_smem` (optional) keeps smem-hungry cipher
-  // CTAs off the generator's SMs.
-  const uint32_t warps = (nlanes + 31) / 32;
-  const uint32_t per_cta = warps < 4 ? warps : 4;
-  const uint32_t ctas = (warps + per_cta - 1) / per_cta;
-  static bool attr_done = false;
-  if (reserve_smem && !attr_done) {
-    cudaFuncSetAttribute(k_prbg_generate,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr_done = true;
-  }
-  k_prbg_generate<<<ctas, per_cta * 32, reserve_smem, s>>>(
-      state, lc, ring, ring_bytes, it0, nblk, nlanes, replays);
+void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
+                          uint64_t ring_bytes, uint64_t it0, uint32_t iters,
+                          uint32_t nlanes, cudaStream_t s) {
+  // (1) chain: 128 threads/CTA, one CTA per SM (the dynamic shared memory
+  // request only enforces SM exclusivity, which also keeps smem-heavy cipher
+  // CTAs off the chain's SMs).
+  constexpr int kReserve = 160 * 1024;
+  cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kReserve);
+  k_prbg_chain<<<(nlanes + 127) / 128, 128, kReserve, s>>>(b.state, b.ckpt, lc,
+                                                           b.orbit, iters, nlanes);
+  const uint32_t nw = nlanes / 2;
+  const uint64_t threads = uint64_t(iters / 8) * nw;
+  k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
+      b.ckpt, lc, b.orbit, iters, nw, ring, ring_bytes, it0, b.bad);
+  k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.state, b.ckpt, lc, iters, nw,
+                                                ring, ring_bytes, it0, b.bad,
+                                                b.replays);
 }
 
 }  // namespace cveb
