@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-frame chaotic confusion/diffusion cipher on B200.
+
+Metric (BASELINE.json): encrypted frames/s and GB/s (5 rounds), % of roofline.
+Workload: config C4 -- a 1920x1080 RGB24 clip, zero-padded to 1920^2
+(reference frame.cpp:19-39), n = 64 subframes, r = 5 rounds, one PLCM key per
+clip -- the largest BASELINE config whose headline target names it (1080p at
+1 GPU).  A step = one batch of `--frames` consecutive frames of the clip
+(default 25; 20 steps + 3 warm-up = 575 frames of the 1000-frame clip).
+
+  value -- frames/s with the frames already resident in HBM, through the
+           device-resident API (cve_cipher_encrypt_frames_async); CUDA events
+           on the calling stream bracket the K timed steps; max over ranks.
+  e2e   -- the same metric through the drop-in host API
+           (cve_cipher_encrypt_frames) on pinned host buffers: every step
+           copies its frames host->device and the ciphertext back.
+
+Multi-GPU (torchrun, one rank per GPU): the keystream of one clip is 2n
+sequential chaotic orbits, so a single clip does not shard; every rank
+encrypts its own clip with its own key (replicas, scaling "weak"); the only
+collectives are the barrier and the max-over-ranks of the timings.
+
+--impl reference times the reference's own CPU library (oracle/_ref, the
+reference sources compiled by oracle/Makefile) on the same config with all
+the host threads it uses (n = 64 worker threads), a bounded number of frames
+per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2302_07411_b200 import synth  # noqa: E402
+
+CONFIG = "C4"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when PEAKS is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--frames", type=int, default=25, help="frames per step")
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ---- distributed plumbing ----------------------------------------------------
+
+class Dist:
+    def __init__(self, use_cuda: bool):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            backend = "nccl" if use_cuda else "gloo"
+            if use_cuda:
+                import torch
+                torch.cuda.set_device(self.local)
+            td.init_process_group(backend=backend)
+            self.pg = td
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ---- clocks during the timed region -------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx, self.rows, self.proc, self.thr = gpu_index, [], None, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thr.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---- workload --------------------------------------------------------------------
+
+def frame_pool(name: str, count: int):
+    return np.stack([synth.config_frame(name, 2 + t) for t in range(count)])
+
+
+def peaks():
+    try:
+        with open(PEAKS) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(name: str, seconds: float) -> dict:
+    """The reference library (oracle/_ref) on host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Reference  # checker / CPU baseline only
+    if not Reference.available():
+        return {"value": None, "unit": "frames/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref/libcve_ref.so not built"}
+    c = synth.CONFIGS[name]
+    ref = Reference(synth.config_key(name), c["workers"], synth.ROUNDS, 1)
+    pool = frame_pool(name, 4)
+    frames, t0 = 0, time.perf_counter()
+    while True:
+        f = pool[frames % len(pool)].copy()
+        assert ref.encrypt(f) == 0
+        frames += 1
+        el = time.perf_counter() - t0
+        if (el >= seconds and frames >= 3) or frames >= 400:
+            break
+    cores = min(c["workers"], os.cpu_count() or 1)
+    return {"value": frames / el, "unit": "frames/s", "cores": cores, "kind": "reference",
+            "sample": f"{frames} consecutive {name} frames ({synth.config_side(name)}^2, "
+                      f"n={c['workers']}, r=5) in {el:.2f} s via cve_cipher_encrypt_frame, "
+                      f"parallel=1 ({c['workers']} threads on {os.cpu_count()} host cpus)"}
+
+
+def config_dict(name: str, frames: int, world: int) -> dict:
+    c = synth.CONFIGS[name]
+    side = synth.config_side(name)
+    return {"workload": f"{name}: {c['frames']}-frame {c['width']}x{c['height']} RGB24 clip, "
+                        f"zero-padded to {side}^2, n={c['workers']} subframes, r=5 rounds, "
+                        f"PLCM key per clip; one clip per rank",
+            "side": side, "workers": c["workers"], "rounds": synth.ROUNDS,
+            "frames_per_step": frames, "frame_bytes": side * side * 3,
+            "l2": f"inputs larger than L2 ({frames * side * side * 3 / 1e6:.0f} MB per step)",
+            "parallelism": f"replicas x{world}"}
+
+
+# ---- reference arm ------------------------------------------------------------------
+
+def run_reference(args) -> None:
+    dist = Dist(use_cuda=False)
+    if dist.rank != 0:
+        dist.close()
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Reference
+    name = args.config
+    c = synth.CONFIGS[name]
+    side = synth.config_side(name)
+    line = {"impl": "reference", "metric": "encrypted frames/s (5 rounds)", "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/u8", "data": "synthetic",
+            "config": config_dict(name, 2, 1)}
+    if not Reference.available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libcve_ref.so was not built"}))
+        return
+    ref = Reference(synth.config_key(name), c["workers"], synth.ROUNDS, 1)
+    pool = frame_pool(name, 4)
+    per_step = 2
+    k = 0
+
+    def step():
+        nonlocal k
+        for _ in range(per_step):
+            f = pool[k % len(pool)].copy()
+            assert ref.encrypt(f) == 0
+            k += 1
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    fps = args.steps * per_step / el
+    cores = min(c["workers"], os.cpu_count() or 1)
+    line.update({"value": fps, "ms_per_step": el * 1e3 / args.steps,
+                 "gbps": fps * side * side * 3 / 1e9,
+                 "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores,
+                                  "kind": "reference",
+                                  "sample": f"{per_step} frames per step of the {name} clip, "
+                                            f"reference libcve (oracle/_ref) with parallel=1 "
+                                            f"({c['workers']} threads, {os.cpu_count()} host cpus)"},
+                 "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    print(json.dumps(line))
+
+
+# ---- B200 arm -------------------------------------------------------------------------
+
+def run_b200(args) -> None:
+    import torch
+    dist = Dist(use_cuda=True)
+    torch.cuda.set_device(dist.local)
+    import paper_2302_07411_b200 as cve
+    cve.set_device(dist.local)
+
+    name = args.config
+    c = synth.CONFIGS[name]
+    side, n, F = synth.config_side(name), c["workers"], args.frames
+    fb = side * side * 3
+    key = synth.det_key(c["key_seed"] + 1000 * dist.rank)  # one clip per rank
+    pool = frame_pool(name, 8)
+    host = torch.empty((F, side, side, 3), dtype=torch.uint8, pin_memory=True)
+    hnp = host.numpy()
+    for t in range(F):
+        hnp[t] = pool[t % len(pool)]
+    dev = host.to(f"cuda:{dist.local}")
+    stream = torch.cuda.current_stream()
+
+    # ---- value: device-resident frames ----
+    enc = cve.Cipher(key, n, synth.ROUNDS)
+    for _ in range(args.warmup):
+        enc.encrypt_frames_device(dev.data_ptr(), side, F, stream.cuda_stream)
+    torch.cuda.synchronize()
+    enc.take_prbg_times()
+    st0 = enc.stats()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dist.local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            enc.encrypt_frames_device(dev.data_ptr(), side, F, stream.cuda_stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = dist.max(ev0.elapsed_time(ev1))
+    st1 = enc.stats()
+    chain_times = enc.take_prbg_times()
+    frames_all = args.steps * F * dist.world
+    value = frames_all / (ms / 1e3)
+
+    # ---- e2e: drop-in host API on pinned buffers ----
+    e2e_enc = cve.Cipher(key, n, synth.ROUNDS)
+    for _ in range(args.warmup):
+        e2e_enc.encrypt_frames(hnp)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_enc.encrypt_frames(hnp)  # H2D + keystream + rounds + D2H, synchronous
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = frames_all / e2e_s
+
+    # ---- roofline / evidence ----
+    hbm, hbm_src = peaks()
+    frames_timed = args.steps * F
+    alg_bytes = 2 * fb  # plaintext read + ciphertext write per frame
+    step_gbs = frames_timed * dist.world * alg_bytes / (ms / 1e3) / 1e9
+    iters_timed = st1["keystream_iters"] - st0["keystream_iters"]
+    chain_ms = st1["chain_ms"] - st0["chain_ms"]
+    prbg_ms = st1["prbg_ms"] - st0["prbg_ms"]
+    cipher_ms = st1["cipher_ms"] - st0["cipher_ms"]
+    ns_iter = chain_ms * 1e6 / max(iters_timed, 1)
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+    cipher_gbs = frames_timed * alg_bytes / (cipher_ms / 1e3) / 1e9 if cipher_ms else None
+    line = {
+        "metric": "encrypted frames/s (5 rounds)", "value": value, "unit": "frames/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/u8", "data": "synthetic",
+        "config": config_dict(name, F, dist.world),
+        "gbps": value * fb / 1e9,
+        "gbps_payload": value * c["width"] * c["height"] * 3 / 1e9,
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": F * fb,
+                "d2h_bytes_per_step": F * fb, "api": "cve_cipher_encrypt_frames (pinned)"},
+        "gpu_launches": launches,
+        "roofline": {
+            "bound": "hbm", "kernel": "whole step vs BASELINE.json roofline "
+            "(2*side^2*3 B/frame at peak HBM; the FP64-throughput bound is not the binding one)",
+            "achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
+            "peak_source": hbm_src, "traffic": None},
+        "chain": {
+            "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
+            "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
+            "launches": int(len(chain_times)),
+            "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
+            "share_of_step": chain_ms / ms if ms else None,
+            "verify_emit_fixup_ms": prbg_ms - chain_ms},
+        "cipher": {"kernel": "k_encrypt_round x5 + k_shift per frame",
+                   "ms_per_frame": cipher_ms / frames_timed,
+                   "achieved_gbs_2F": cipher_gbs,
+                   "frac_of_hbm_2F": (cipher_gbs / hbm) if cipher_gbs else None},
+        "guard_replays": st1["guard_replays"],
+        "clocks": clk.summary(),
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
+    if dist.rank == 0:
+        print(json.dumps(line))
+    dist.close()
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               "--master-port=29531", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

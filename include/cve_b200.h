@@ -160,6 +160,7 @@ typedef struct cve_cipher_stats {
   uint64_t prbg_launches;    /* of which keystream-generator launches */
   uint64_t guard_replays;    /* 8-iteration blocks replayed exactly */
   double prbg_ms;            /* device time of generator launches */
+  double chain_ms;           /* of which the sequential chain kernel */
   double cipher_ms;          /* device time of cipher-round launches */
 } cve_cipher_stats;
 
@@ -188,8 +189,8 @@ CVE_B200_API cve_status cve_derive_worker_lanes(const char* key_hex,
                                                 uint32_t* seeds_out,
                                                 size_t nseeds);
 
-/* Device times (ms) of the keystream-generator launches since the previous
- * call, oldest first; *count receives the number available, at most `cap`
+/* Device times (ms) of the keystream generator's chain kernel, one per
+ * generator launch since the previous call, oldest first; *count receives the number available, at most `cap`
  * are copied to `out` (which may be NULL to query).  Synchronizes. */
 CVE_B200_API cve_status cve_cipher_take_prbg_times(cve_cipher* cipher,
                                                    float* out, size_t cap,

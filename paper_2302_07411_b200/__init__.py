@@ -52,7 +52,7 @@ class Stats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("keystream_iters", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("prbg_launches", C.c_uint64),
                 ("guard_replays", C.c_uint64), ("prbg_ms", C.c_double),
-                ("cipher_ms", C.c_double)]
+                ("chain_ms", C.c_double), ("cipher_ms", C.c_double)]
 
 
 def _load() -> C.CDLL:
@@ -267,7 +267,7 @@ class Cipher:
         return {k: getattr(s, k) for k, _ in Stats._fields_}
 
     def take_prbg_times(self, cap: int = 1 << 20) -> np.ndarray:
-        """Device times (ms) of keystream-generator launches since last call."""
+        """Device times (ms) of the chain kernel, one per generator launch."""
         out = np.zeros(cap, dtype=np.float32)
         n = C.c_size_t()
         _check(lib.cve_cipher_take_prbg_times(

@@ -241,6 +241,7 @@ cve_status cve_cipher_get_stats(cve_cipher* cipher, cve_cipher_stats* out) {
     out->prbg_launches = s.prbg_launches;
     out->guard_replays = s.guard_replays;
     out->prbg_ms = s.prbg_ms;
+    out->chain_ms = s.chain_ms;
     out->cipher_ms = s.cipher_ms;
   });
 }

@@ -45,9 +45,11 @@ struct PrbgBuffers {
 // starting at iteration `it0` (multiple of 8) and writes each worker's 6
 // bytes/iteration at stream byte 6*it (mod ring_bytes) of that worker's ring
 // (ring_bytes % 48 == 0).  Three launches: chain, verify+emit, exact fix-up.
+// `after_chain` (optional) is recorded between the chain and verify kernels.
 void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
                           uint64_t ring_bytes, uint64_t it0, uint32_t iters,
-                          uint32_t nlanes, cudaStream_t s);
+                          uint32_t nlanes, cudaStream_t s,
+                          cudaEvent_t after_chain = nullptr);
 
 // Geometry of one square frame split into n row bands.
 struct Geom {

@@ -248,7 +248,7 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
 
 void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
                           uint64_t ring_bytes, uint64_t it0, uint32_t iters,
-                          uint32_t nlanes, cudaStream_t s) {
+                          uint32_t nlanes, cudaStream_t s, cudaEvent_t after_chain) {
   // (1) chain: 128 threads/CTA, one CTA per SM (the dynamic shared memory
   // request only enforces SM exclusivity, which also keeps smem-heavy cipher
   // CTAs off the chain's SMs).
@@ -257,6 +257,7 @@ void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ri
                        kReserve);
   k_prbg_chain<<<(nlanes + 127) / 128, 128, kReserve, s>>>(b.state, b.ckpt, lc,
                                                            b.orbit, iters, nlanes);
+  if (after_chain) cudaEventRecord(after_chain, s);
   const uint32_t nw = nlanes / 2;
   const uint64_t threads = uint64_t(iters / 8) * nw;
   k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
