@@ -26,10 +26,13 @@ PrbgBuffers alloc_prbg(uint32_t nlanes) {
   uint64_t iters = kOrbitBytes / (8ull * nlanes);
   iters = std::min<uint64_t>(iters, 1u << 20) / 8 * 8;
   b.max_iters = uint32_t(std::max<uint64_t>(iters, 8));
-  ck(cudaMalloc(&b.state, nlanes * sizeof(double)), "cudaMalloc state");
-  ck(cudaMalloc(&b.ckpt, nlanes * sizeof(double)), "cudaMalloc ckpt");
-  ck(cudaMalloc(&b.orbit, uint64_t(b.max_iters) * nlanes * sizeof(double)),
-     "cudaMalloc orbit");
+  const size_t lanes_bytes = nlanes * sizeof(double);
+  ck(cudaMalloc(&b.state, lanes_bytes), "cudaMalloc state");
+  ck(cudaMalloc(&b.verified_end, lanes_bytes), "cudaMalloc state");
+  for (int k = 0; k < 2; ++k) {
+    ck(cudaMalloc(&b.ckpt[k], lanes_bytes), "cudaMalloc ckpt");
+    ck(cudaMalloc(&b.orbit[k], uint64_t(b.max_iters) * lanes_bytes), "cudaMalloc orbit");
+  }
   ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
   ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemset(b.bad, 0, (nlanes / 2) * sizeof(unsigned)), "memset");
@@ -39,13 +42,30 @@ PrbgBuffers alloc_prbg(uint32_t nlanes) {
 
 void free_prbg(PrbgBuffers& b) {
   cudaFree(b.state);
-  cudaFree(b.ckpt);
-  cudaFree(b.orbit);
+  cudaFree(b.verified_end);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(b.ckpt[k]);
+    cudaFree(b.orbit[k]);
+  }
   cudaFree(b.bad);
   cudaFree(b.replays);
   b = PrbgBuffers{};
 }
 
+// x <- guard(x0) + 256 warm-up steps; the warm state is the first verified
+// end point.
+void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
+               uint32_t nlanes, cudaStream_t s) {
+  double* d_x0 = nullptr;
+  ck(cudaMalloc(&d_x0, nlanes * sizeof(double)), "cudaMalloc x0");
+  ck(cudaMemcpy(d_x0, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice), "upload x0");
+  launch_prbg_init(b.state, d_lc, d_x0, nlanes, s);
+  ck(cudaGetLastError(), "prbg_init launch");
+  ck(cudaMemcpyAsync(b.verified_end, b.state, nlanes * sizeof(double),
+                     cudaMemcpyDeviceToDevice, s), "copy state");
+  ck(cudaStreamSynchronize(s), "prbg_init");
+  cudaFree(d_x0);
+}
 }  // namespace
 
 Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
@@ -67,6 +87,9 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   ck(cudaSetDevice(dev_), "cudaSetDevice");
 
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&s_ver_, cudaStreamNonBlocking), "stream");
+  for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&s_work_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
@@ -80,31 +103,25 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     x0[2 * i] = lanes[i].a.x0;
     x0[2 * i + 1] = lanes[i].b.x0;
   }
-  double* d_x0 = nullptr;
   pb_ = alloc_prbg(nl);
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-  ck(cudaMalloc(&d_x0, nl * sizeof(double)), "cudaMalloc x0");
   ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice),
      "upload lanes");
-  ck(cudaMemcpy(d_x0, x0.data(), nl * sizeof(double), cudaMemcpyHostToDevice),
-     "upload x0");
-  launch_prbg_init(pb_.state, d_lc_, d_x0, nl, s_gen_);
-  ck(cudaGetLastError(), "prbg_init launch");
+  init_prbg(pb_, d_lc_, x0.data(), nl, s_gen_);
   ++st_.kernel_launches;
-  ck(cudaStreamSynchronize(s_gen_), "prbg_init");
-  cudaFree(d_x0);
 }
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamSynchronize(s);
   for (auto& c : consumers_) ev_put(c.done);
+  for (auto e : ver_done_) if (e) cudaEventDestroy(e);
+  for (auto e : chain_done_) if (e) cudaEventDestroy(e);
   for (auto& g : gens_) ev_put(g.ev);
   for (auto& t : timed_) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
-    if (t.m) cudaEventDestroy(t.m);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
@@ -115,7 +132,7 @@ Engine::~Engine() {
   cudaFree(ring_);
   free_prbg(pb_);
   cudaFree(d_lc_);
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
 }
 
@@ -158,12 +175,12 @@ cudaEvent_t Engine::ev_get() {
 
 void Engine::ev_put(cudaEvent_t e) { ev_pool_.push_back(e); }
 
-void Engine::timed_begin(cudaStream_t s, bool prbg) {
+void Engine::timed_begin(cudaStream_t s, bool chain, bool verify) {
   Timed t{};
   ck(cudaEventCreate(&t.a), "cudaEventCreate");
   ck(cudaEventCreate(&t.b), "cudaEventCreate");
-  if (prbg) ck(cudaEventCreate(&t.m), "cudaEventCreate");
-  t.prbg = prbg;
+  t.chain = chain;
+  t.verify = verify;
   ck(cudaEventRecord(t.a, s), "cudaEventRecord");
   open_ = t;
 }
@@ -185,13 +202,12 @@ void Engine::fold_timings(bool wait) {
     float ms = 0;
     ck(cudaEventSynchronize(t.b), "timing event");
     ck(cudaEventElapsedTime(&ms, t.a, t.b), "cudaEventElapsedTime");
-    if (t.prbg) {
-      float chain = 0;
-      ck(cudaEventElapsedTime(&chain, t.a, t.m), "cudaEventElapsedTime");
+    if (t.chain) {
       st_.prbg_ms += ms;
-      st_.chain_ms += chain;
-      if (prbg_times_.size() < (1u << 20)) prbg_times_.push_back(chain);
-      cudaEventDestroy(t.m);
+      st_.chain_ms += ms;
+      if (prbg_times_.size() < (1u << 20)) prbg_times_.push_back(ms);
+    } else if (t.verify) {
+      st_.prbg_ms += ms;
     } else {
       st_.cipher_ms += ms;
     }
@@ -284,12 +300,23 @@ void Engine::gen_until(uint64_t end_byte) {
     uint64_t chunk = target - gen_iters_;
     const uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
     chunk = std::min<uint64_t>({chunk, max_chunk, pb_.max_iters});
+    const int slot = int(launches_ & 1);
+    // (1) chain on s_gen, once the verifier is done with this slot's buffers
+    if (launches_ >= 2) ck(cudaStreamWaitEvent(s_gen_, ver_done_[slot], 0), "wait slot");
+    timed_begin(s_gen_, true);
+    launch_prbg_chain(pb_, slot, d_lc_, uint32_t(chunk), 2 * n_, s_gen_);
+    ck(cudaGetLastError(), "prbg_chain launch");
+    timed_end(s_gen_);
+    ck(cudaEventRecord(chain_done_[slot], s_gen_), "cudaEventRecord");
+    // (2)+(3) verify, emit, fix up on s_ver while the next chain runs.
+    // Ring bytes below write_end - R get overwritten: their readers must be
+    // done.
+    ck(cudaStreamWaitEvent(s_ver_, chain_done_[slot], 0), "wait chain");
     const uint64_t write_end = (gen_iters_ + chunk) * 6;
-    // bytes below write_end - R get overwritten: their readers must be done
     if (write_end > ring_bytes_) {
       const uint64_t dead = write_end - ring_bytes_;
       while (!consumers_.empty() && consumers_.front().lo < dead) {
-        ck(cudaStreamWaitEvent(s_gen_, consumers_.front().done, 0), "wait");
+        ck(cudaStreamWaitEvent(s_ver_, consumers_.front().done, 0), "wait");
         if (consumers_.front().hi <= dead) {
           ev_put(consumers_.front().done);
           consumers_.pop_front();
@@ -298,23 +325,23 @@ void Engine::gen_until(uint64_t end_byte) {
         }
       }
     }
-    timed_begin(s_gen_, true);
-    launch_prbg_generate(pb_, d_lc_, ring_, ring_bytes_, gen_iters_,
-                         uint32_t(chunk), 2 * n_, s_gen_, open_.m);
-    ck(cudaGetLastError(), "prbg_generate launch");
-    timed_end(s_gen_);
+    timed_begin(s_ver_, false, true);
+    launch_prbg_verify(pb_, slot, d_lc_, ring_, ring_bytes_, gen_iters_,
+                       uint32_t(chunk), 2 * n_, s_ver_);
+    ck(cudaGetLastError(), "prbg_verify launch");
+    timed_end(s_ver_);
+    ck(cudaEventRecord(ver_done_[slot], s_ver_), "cudaEventRecord");
     st_.kernel_launches += 3;
     ++st_.prbg_launches;
+    ++launches_;
     gen_iters_ += chunk;
     st_.keystream_iters += chunk;
     GenMark m{gen_iters_ * 6, ev_get()};
-    ck(cudaEventRecord(m.ev, s_gen_), "cudaEventRecord");
+    ck(cudaEventRecord(m.ev, s_ver_), "cudaEventRecord");
     gens_.push_back(m);
   }
 }
 
-// Event of the first generator launch whose output reaches end_byte.  Marks
-// ending below end_byte are useless to this and every later frame.
 cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
   while (!gens_.empty() && gens_.front().end_byte < end_byte) {
     ev_put(gens_.front().ev);
@@ -332,7 +359,7 @@ void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
   if (cudaEvent_t ge = gen_event_covering(lo + need))
     ck(cudaStreamWaitEvent(s_work_, ge, 0), "wait keystream");
 
-  timed_begin(s_work_, false);
+  timed_begin(s_work_, false, false);
   launch_shift_table(sine_for(g.side), seed, d_shift_, g.side, s_work_);
   ++st_.kernel_launches;
   KsWindow ks{ring_, ring_bytes_, 0};
@@ -411,7 +438,7 @@ void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
 }
 
 void Engine::synchronize() {
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
     ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
@@ -463,13 +490,11 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
   LaneConst lc[2] = {make_lane_const(a.p), make_lane_const(b.p)};
   const double x0[2] = {a.x0, b.x0};
   PrbgBuffers pb{};
-  double* d_x0 = nullptr;
   LaneConst* d_lc = nullptr;
   uint8_t* d_out = nullptr;
   cudaStream_t s = nullptr;
   auto cleanup = [&] {
     free_prbg(pb);
-    cudaFree(d_x0);
     cudaFree(d_lc);
     cudaFree(d_out);
     if (s) cudaStreamDestroy(s);
@@ -477,16 +502,15 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
   try {
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     pb = alloc_prbg(2);
-    ck(cudaMalloc(&d_x0, sizeof x0), "cudaMalloc");
     ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
     ck(cudaMalloc(&d_out, ring), "cudaMalloc");
     ck(cudaMemcpy(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice), "upload");
-    ck(cudaMemcpy(d_x0, x0, sizeof x0, cudaMemcpyHostToDevice), "upload");
-    launch_prbg_init(pb.state, d_lc, d_x0, 2, s);
-    ck(cudaGetLastError(), "prbg_init");
-    for (uint64_t it = 0; it < iters; it += pb.max_iters) {
+    init_prbg(pb, d_lc, x0, 2, s);
+    int slot = 0;
+    for (uint64_t it = 0; it < iters; it += pb.max_iters, slot ^= 1) {
       const uint32_t n = uint32_t(std::min<uint64_t>(pb.max_iters, iters - it));
-      launch_prbg_generate(pb, d_lc, d_out, ring, it, n, 2, s);
+      launch_prbg_chain(pb, slot, d_lc, n, 2, s);
+      launch_prbg_verify(pb, slot, d_lc, d_out, ring, it, n, 2, s);
       ck(cudaGetLastError(), "prbg_generate");
     }
     ck(cudaStreamSynchronize(s), "keystream");

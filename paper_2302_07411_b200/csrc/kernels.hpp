@@ -31,25 +31,31 @@ LaneConst make_lane_const(double p);
 void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                       uint32_t nlanes, cudaStream_t s);
 
-// Device state of the generator.
+// Device state of the generator.  Chain launches run back to back on one
+// stream; verification/emission of launch L runs on another stream while
+// the chain computes L+1, so every per-launch buffer is double-buffered.
 struct PrbgBuffers {
-  double* state;    // nlanes: current orbit points
-  double* ckpt;     // nlanes: orbit points at the start of the last launch
-  double* orbit;    // max_iters * nlanes: orbit values of one launch
-  unsigned* bad;    // nworkers: verification failure flags
+  double* state;          // nlanes: chain position (written by the chain)
+  double* ckpt[2];        // nlanes: start point of launch L (slot L&1)
+  double* orbit[2];       // max_iters * nlanes: orbit values of launch L
+  double* verified_end;   // nlanes: verified end point of the last launch
+  unsigned* bad;          // nworkers: verification failure flags
   unsigned long long* replays;  // workers recomputed exactly (cumulative)
   uint32_t max_iters;           // per launch, multiple of 8
 };
 
-// Advances every lane by `iters` (multiple of 8, <= max_iters) iterations
-// starting at iteration `it0` (multiple of 8) and writes each worker's 6
-// bytes/iteration at stream byte 6*it (mod ring_bytes) of that worker's ring
-// (ring_bytes % 48 == 0).  Three launches: chain, verify+emit, exact fix-up.
-// `after_chain` (optional) is recorded between the chain and verify kernels.
-void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
-                          uint64_t ring_bytes, uint64_t it0, uint32_t iters,
-                          uint32_t nlanes, cudaStream_t s,
-                          cudaEvent_t after_chain = nullptr);
+// (1) Chain: advances every lane by `iters` (multiple of 8, <= max_iters)
+// iterations, orbit values into orbit[slot], start point into ckpt[slot].
+void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
+                       uint32_t iters, uint32_t nlanes, cudaStream_t s);
+// (2) Verify every step of launch `slot` against the reference's exact step
+// (and that it starts where the previous launch verifiably ended), emit the
+// keystream bytes of iterations [it0, it0+iters) into the ring at stream
+// byte 6*it (mod ring_bytes, ring_bytes % 48 == 0), and (3) recompute any
+// failed worker exactly from the verified end point.
+void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
+                        uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
+                        uint32_t iters, uint32_t nlanes, cudaStream_t s);
 
 // Geometry of one square frame split into n row bands.
 struct Geom {

@@ -13,15 +13,15 @@
 //     branch-free speculative step -- exact case predicates, exact numerator,
 //     and the quotient num/d as fma(num, RN(1/d), corr) where the ~2^-53
 //     correction corr ~= num * (1/d - RN(1/d)) is formed straight from x by
-//     one FMA per case, so only DADD -> FSEL -> DADD -> FSEL -> DFMA remain
-//     on the chain.  Each result goes to a shared-memory ring.
-//   verifier warps (sub-partitions 2,3): re-derive every step with the
-//     reference's own case logic (chaos.cpp:28-32) and prove the produced
-//     quotient is the correctly rounded one (|num - d*y| < d*ulp(y)/2 via an
-//     exact FMA residual; IEEE division for the inconclusive powers of two)
-//     and outside the guard set {0, p, 0.5, 1} (chaos.cpp:18-24).
-//   any failure: the CTA recomputes its whole range with IEEE __ddiv_rn and
-//     the exact guard before the kernel ends.
+//     one FMA, so only DADD -> DADD -> FSEL -> DFMA remain on the chain.  Each orbit value is stored (one coalesced 8-byte store).
+//   verify+emit kernel (whole GPU, in parallel over steps): re-derives every
+//     step with the reference's own case logic (chaos.cpp:28-32), proves the
+//     produced quotient is the correctly rounded one (|num - d*y| < d*ulp(y)/2
+//     via an exact FMA residual; IEEE division for the inconclusive powers
+//     of two) and outside the guard set {0, p, 0.5, 1} (chaos.cpp:18-24),
+//     and emits the keystream bytes.
+//   fix-up kernel: any worker with a failed step is recomputed from the
+//     launch checkpoint with IEEE __ddiv_rn and the exact guard.
 //
 // Output is therefore bit-identical to the reference's IEEE binary64 loop by
 // construction.  Compiled with -fmad=false; every FP64 operation is an
@@ -78,20 +78,23 @@ __device__ __forceinline__ double plcm_exact(double x, double p, double q) {
 // Speculative chain step.  Cases (reference: fold x>0.5 to 1-x, then
 // f<p ? f/p : (f-p)/q):  A x<p: x/p   B p<=x<=.5: (x-p)/q
 //                        C x>cthr: (1-x)/p   D .5<x<=cthr: ((1-x)-p)/q
+// The predicates and the numerator are exact; the quotient is
+// fma(num, RN(1/d), corr) with corr ~= num*(1/d - RN(1/d)) formed from the
+// folded value by one FMA with selected constants (f*yl_p for A/C,
+// (f-p)*yl_q for B/D).  Static schedule: 44 cycles per iteration
+// (tools/iter_cycles.py; the other formulations tried scored 49-57).
 __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
   const bool c1 = x > 0.5;
   const bool low = (x < c.p) | (x > c.cthr);  // == (f < p), exactly
   const double t1 = __dsub_rn(1.0, x);         // exact when x > 0.5
-  const double base = c1 ? t1 : x;             // f
-  const double shifted = __dsub_rn(base, c.p);
-  const double num = low ? base : shifted;
+  const double nb = __dsub_rn(x, c.p);
+  const double nd = __dsub_rn(t1, c.p);
+  const double f = c1 ? t1 : x;
+  const double g = low ? c.yl_p : c.yl_q;
+  const double a = low ? 0.0 : c.a_b;
+  const double corr = __fma_rn(f, g, a);
+  const double num = low ? f : (c1 ? nd : nb);
   const double yh = low ? c.yh_p : c.yh_q;
-  // num * (1/d - yh), from x: A x*ylp  B (x-p)*ylq  C (1-x)*ylp  D (1-x-p)*ylq
-  const double ca = __dmul_rn(x, c.yl_p);
-  const double cb = __fma_rn(x, c.yl_q, c.a_b);
-  const double cc = __fma_rn(-x, c.yl_p, c.yl_p);
-  const double cd = __fma_rn(-x, c.yl_q, c.a_d);
-  const double corr = low ? (c1 ? cc : ca) : (c1 ? cd : cb);
   return __fma_rn(num, yh, corr);
 }
 
@@ -134,7 +137,6 @@ __global__ void __launch_bounds__(128)
 // (1) The chain.  One orbit per thread, 4 warps per CTA, one CTA per SM, so
 // every warp owns an SM sub-partition's in-order issue.  Per step: the
 // speculative iteration and one coalesced 8-byte store of the orbit value.
-// `ckpt` keeps the launch's start state for the exact fix-up.
 __global__ void __launch_bounds__(128, 1)
     k_prbg_chain(double* __restrict__ state, double* __restrict__ ckpt,
                  const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
@@ -159,9 +161,12 @@ __global__ void __launch_bounds__(128, 1)
 // (2) Verify every step in parallel against the reference's exact step, and
 // emit the keystream: 6 bytes per iteration per worker = the little-endian
 // low 48 mantissa bits of x_a ^ x_b (extract_bytes, chaos.cpp:46-56).
-// Thread = (worker, 8-iteration group); failures flag the worker.
+// Thread = (worker, 8-iteration group); failures flag the worker.  Group 0
+// also checks continuity: the launch must start at the previous launch's
+// verified end point (it may not, after an exact fix-up of that launch).
 __global__ void __launch_bounds__(256)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
+                       const double* __restrict__ verified_end,
                        const LaneConst* __restrict__ lcs,
                        const double* __restrict__ orbit, uint32_t iters,
                        uint32_t nworkers, uint8_t* __restrict__ ring,
@@ -175,9 +180,16 @@ __global__ void __launch_bounds__(256)
   const uint32_t nl = 2 * nworkers;
   const LaneConst ca = lcs[2 * w], cb = lcs[2 * w + 1];
   const size_t i0 = size_t(g) * 8;
-  double xa = g ? orbit[(i0 - 1) * nl + 2 * w] : ckpt[2 * w];
-  double xb = g ? orbit[(i0 - 1) * nl + 2 * w + 1] : ckpt[2 * w + 1];
+  double xa, xb;
   bool ok = true;
+  if (g) {
+    xa = orbit[(i0 - 1) * nl + 2 * w];
+    xb = orbit[(i0 - 1) * nl + 2 * w + 1];
+  } else {
+    xa = ckpt[2 * w];
+    xb = ckpt[2 * w + 1];
+    ok = xa == verified_end[2 * w] && xb == verified_end[2 * w + 1];
+  }
   uint32_t lo[8], hi[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
@@ -204,21 +216,28 @@ __global__ void __launch_bounds__(256)
   dst[2] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
 }
 
-// (3) Exact fix-up of flagged workers (normally every thread exits at once):
-// recompute both lanes from the launch checkpoint with IEEE division and the
-// exact guard, rewrite the worker's bytes and state.
-__global__ void k_prbg_fixup(double* __restrict__ state,
-                             const double* __restrict__ ckpt,
+// (3) One thread per worker.  Verified: advance the verified end point to
+// the launch's last orbit values.  Flagged: recompute both lanes from the
+// verified end point with IEEE division and the exact guard, rewriting the
+// worker's bytes -- normally never taken.
+__global__ void k_prbg_fixup(const double* __restrict__ orbit,
+                             double* __restrict__ verified_end,
                              const LaneConst* __restrict__ lcs, uint32_t iters,
                              uint32_t nworkers, uint8_t* __restrict__ ring,
                              uint64_t ring_bytes, uint64_t it0,
                              unsigned* __restrict__ bad,
                              unsigned long long* __restrict__ replays) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= nworkers || !bad[w]) return;
+  if (w >= nworkers) return;
+  const uint32_t nl = 2 * nworkers;
+  if (!bad[w]) {
+    verified_end[2 * w] = orbit[size_t(iters - 1) * nl + 2 * w];
+    verified_end[2 * w + 1] = orbit[size_t(iters - 1) * nl + 2 * w + 1];
+    return;
+  }
   bad[w] = 0;
   const LaneConst ca = lcs[2 * w], cb = lcs[2 * w + 1];
-  double xa = ckpt[2 * w], xb = ckpt[2 * w + 1];
+  double xa = verified_end[2 * w], xb = verified_end[2 * w + 1];
   uint8_t* base = ring + uint64_t(w) * ring_bytes;
   uint64_t off = (it0 * 6u) % ring_bytes;
   for (uint32_t i = 0; i < iters; ++i) {
@@ -232,8 +251,8 @@ __global__ void k_prbg_fixup(double* __restrict__ state,
     off += 6;
     if (off == ring_bytes) off = 0;
   }
-  state[2 * w] = xa;
-  state[2 * w + 1] = xb;
+  verified_end[2 * w] = xa;
+  verified_end[2 * w + 1] = xb;
   atomicAdd(replays, 1ull);
 }
 
@@ -246,25 +265,29 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                                                                     x0, nlanes);
 }
 
-void launch_prbg_generate(const PrbgBuffers& b, const LaneConst* lc, uint8_t* ring,
-                          uint64_t ring_bytes, uint64_t it0, uint32_t iters,
-                          uint32_t nlanes, cudaStream_t s, cudaEvent_t after_chain) {
-  // (1) chain: 128 threads/CTA, one CTA per SM (the dynamic shared memory
-  // request only enforces SM exclusivity, which also keeps smem-heavy cipher
-  // CTAs off the chain's SMs).
+void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
+                       uint32_t iters, uint32_t nlanes, cudaStream_t s) {
+  // 128 threads/CTA, one CTA per SM (the dynamic shared memory request only
+  // enforces SM exclusivity, which also keeps smem-heavy cipher CTAs off the
+  // chain's SMs).
   constexpr int kReserve = 160 * 1024;
   cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kReserve);
-  k_prbg_chain<<<(nlanes + 127) / 128, 128, kReserve, s>>>(b.state, b.ckpt, lc,
-                                                           b.orbit, iters, nlanes);
-  if (after_chain) cudaEventRecord(after_chain, s);
+  k_prbg_chain<<<(nlanes + 127) / 128, 128, kReserve, s>>>(
+      b.state, b.ckpt[slot], lc, b.orbit[slot], iters, nlanes);
+}
+
+void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
+                        uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
+                        uint32_t iters, uint32_t nlanes, cudaStream_t s) {
   const uint32_t nw = nlanes / 2;
   const uint64_t threads = uint64_t(iters / 8) * nw;
   k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
-      b.ckpt, lc, b.orbit, iters, nw, ring, ring_bytes, it0, b.bad);
-  k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.state, b.ckpt, lc, iters, nw,
-                                                ring, ring_bytes, it0, b.bad,
-                                                b.replays);
+      b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nw, ring, ring_bytes,
+      it0, b.bad);
+  k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.orbit[slot], b.verified_end, lc,
+                                                iters, nw, ring, ring_bytes, it0,
+                                                b.bad, b.replays);
 }
 
 }  // namespace cveb

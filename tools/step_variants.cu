@@ -268,6 +268,23 @@ __device__ __forceinline__ double v10(double x, const LC& c, bool& flag) {
   return y;
 }
 
+// V11: product formulation (4 numerators, single 4-way select)
+__device__ __forceinline__ double v11(double x, const LC& c, bool& flag) {
+  const bool c1 = x > 0.5;
+  const bool low = (x < c.p) | (x > c.cthr);
+  const double t1 = __dsub_rn(1.0, x);
+  const double nb = __dsub_rn(x, c.p);
+  const double nd = __dsub_rn(t1, c.p);
+  const double num = low ? (c1 ? t1 : x) : (c1 ? nd : nb);
+  const double yh = low ? c.yhp : c.yhq;
+  const double ca = __dmul_rn(x, c.ylp);
+  const double cb = __fma_rn(x, c.ylq, c.aB);
+  const double cc = __fma_rn(-x, c.ylp, c.ylp);
+  const double cd = __fma_rn(-x, c.ylq, c.aD);
+  const double corr = low ? (c1 ? cc : ca) : (c1 ? cd : cb);
+  return __fma_rn(num, yh, corr);
+}
+
 template <int V>
 __device__ __forceinline__ double stepv(double x, const LC& c, bool& f) {
   if (V == 0) return v0(x, c, f);
@@ -279,6 +296,7 @@ __device__ __forceinline__ double stepv(double x, const LC& c, bool& f) {
   if (V == 6) return v6(x, c, f);
   if (V == 7) return v7(x, c, f);
   if (V == 9) return v9(x, c, f);
+  if (V == 11) return v11(x, c, f);
   return v10(x, c, f);
 }
 
@@ -298,6 +316,22 @@ __global__ void k_run(const LC* lcs, double* xs, int iters, int* flags) {
   if (V == 8) x += ring[threadIdx.x] * 0.0;
   xs[threadIdx.x] = x;
   flags[threadIdx.x] = flag;
+}
+
+template <int V>
+__global__ void k_sparse(const LC* lcs, double* xs, int iters, int* flags, int per_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane >= per_warp) return;
+  const int l = warp * per_warp + lane;
+  const LC c = lcs[l];
+  double x = xs[l];
+  bool flag = false;
+  for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x = stepv<V>(x, c, flag);
+  }
+  xs[l] = x;
+  flags[l] = flag;
 }
 
 __global__ void k_ref(const LC* lcs, double* xs, int iters) {
@@ -392,6 +426,25 @@ int main() {
   run("V8 V7 + STS y (verifier hand-off)", k_run<8>);
   run("V9 V7 w/ predicated sub (asm)", k_run<9>);
   run("V10 V7 + inline verify", k_run<10>);
+  run("V11 product (4 nums, 1 select)", k_run<11>);
+  for (int pw : {32, 16, 8, 4, 2}) {
+    cudaMemcpy(d_x, x0.data(), T * 8, cudaMemcpyHostToDevice);
+    cudaEventRecord(a);
+    k_sparse<11><<<1, 128>>>(d_lc, d_x, iters, d_f, pw);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaMemcpy(d_x, x0.data(), T * 8, cudaMemcpyHostToDevice);
+    cudaEventRecord(a);
+    k_sparse<9><<<1, 128>>>(d_lc, d_x, iters, d_f, pw);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms9;
+    cudaEventElapsedTime(&ms9, a, b);
+    printf("lanes/warp %2d: V11 %6.2f ns/iter   V9 %6.2f ns/iter\n", pw, ms * 1e6 / iters,
+           ms9 * 1e6 / iters);
+  }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
