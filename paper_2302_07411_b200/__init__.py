@@ -193,7 +193,8 @@ class Cipher:
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:
-            lib.cve_cipher_destroy(self._h)
+            if lib is not None:  # interpreter shutdown may have cleared it
+                lib.cve_cipher_destroy(self._h)
             self._h = None
 
     __del__ = close

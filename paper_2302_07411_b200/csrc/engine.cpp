@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 
 namespace cveb {
@@ -68,6 +70,17 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
 }
 }  // namespace
 
+void configure_kernels_once(int device) {
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(device)) return;
+  configure_prbg_kernels();
+  configure_cipher_kernels();
+  ck(cudaGetLastError(), "kernel attributes");
+  done.insert(device);
+}
+
 Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     : key_(key), n_(workers), r_(rounds), dev_(device), coord_(key) {
   // engine.cpp:168-179: coordinator first, then workers/rounds checks.
@@ -85,6 +98,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     raise(Errc::internal, std::string("engine is built for sm_100a; device is ") +
                               prop.name);
   ck(cudaSetDevice(dev_), "cudaSetDevice");
+  configure_kernels_once(dev_);
 
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&s_ver_, cudaStreamNonBlocking), "stream");
@@ -124,6 +138,7 @@ Engine::~Engine() {
     cudaEventDestroy(t.b);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : tev_pool_) cudaEventDestroy(e);
   for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
   for (uint8_t* p : slots_) cudaFree(p);
   for (auto& kv : sines_) cudaFree(kv.second);
@@ -175,10 +190,21 @@ cudaEvent_t Engine::ev_get() {
 
 void Engine::ev_put(cudaEvent_t e) { ev_pool_.push_back(e); }
 
+cudaEvent_t Engine::tev_get() {
+  if (!tev_pool_.empty()) {
+    cudaEvent_t e = tev_pool_.back();
+    tev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
 void Engine::timed_begin(cudaStream_t s, bool chain, bool verify) {
   Timed t{};
-  ck(cudaEventCreate(&t.a), "cudaEventCreate");
-  ck(cudaEventCreate(&t.b), "cudaEventCreate");
+  t.a = tev_get();
+  t.b = tev_get();
   t.chain = chain;
   t.verify = verify;
   ck(cudaEventRecord(t.a, s), "cudaEventRecord");
@@ -189,7 +215,7 @@ void Engine::timed_end(cudaStream_t s) {
   ck(cudaEventRecord(open_.b, s), "cudaEventRecord");
   timed_.push_back(open_);
   open_ = Timed{};
-  if (timed_.size() > 4096) fold_timings(false);
+  if (timed_.size() > 256) fold_timings(false);
 }
 
 void Engine::fold_timings(bool wait) {
@@ -211,8 +237,8 @@ void Engine::fold_timings(bool wait) {
     } else {
       st_.cipher_ms += ms;
     }
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
+    tev_pool_.push_back(t.a);
+    tev_pool_.push_back(t.b);
   }
   timed_.swap(keep);
 }
@@ -500,6 +526,9 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
     if (s) cudaStreamDestroy(s);
   };
   try {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    configure_kernels_once(dev);
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     pb = alloc_prbg(2);
     ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");

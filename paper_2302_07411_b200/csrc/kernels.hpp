@@ -25,6 +25,11 @@ struct LaneConst {
 
 LaneConst make_lane_const(double p);
 
+// Kernel attributes (dynamic smem limits, cluster sizes); once per device.
+void configure_prbg_kernels();
+void configure_cipher_kernels();
+void configure_kernels_once(int device);
+
 // Lane layout: lane l = 2*worker + (0 for the reference's lane a, 1 for b).
 
 // x <- guard(x0); 256 exact warm-up iterations (chaos.cpp:79-91).

@@ -265,15 +265,19 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                                                                     x0, nlanes);
 }
 
+constexpr int kChainReserve = 160 * 1024;
+
+void configure_prbg_kernels() {
+  cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kChainReserve);
+}
+
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
                        uint32_t iters, uint32_t nlanes, cudaStream_t s) {
   // 128 threads/CTA, one CTA per SM (the dynamic shared memory request only
   // enforces SM exclusivity, which also keeps smem-heavy cipher CTAs off the
   // chain's SMs).
-  constexpr int kReserve = 160 * 1024;
-  cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kReserve);
-  k_prbg_chain<<<(nlanes + 127) / 128, 128, kReserve, s>>>(
+  k_prbg_chain<<<(nlanes + 127) / 128, 128, kChainReserve, s>>>(
       b.state, b.ckpt[slot], lc, b.orbit[slot], iters, nlanes);
 }
 

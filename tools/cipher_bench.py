@@ -1,0 +1,27 @@
+"""Cipher-round kernels alone (K2/K3 + K4): keystream prefetched first, then
+frames encrypted/decrypted from device memory; device time per frame from the
+handle's CUDA events.  Tool (not the bench)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2302_07411_b200 as cve
+from paper_2302_07411_b200 import synth
+
+for name in sys.argv[1:] or ["C1", "C3", "C4", "C5"]:
+    c = synth.CONFIGS[name]; n = c["workers"]; side = synth.config_side(name)
+    F = side * side * 3
+    need = 5 * (side // n) * side * 3
+    frames = torch.from_numpy(np.stack([synth.config_frame(name, t) for t in range(3)])).cuda()
+    out = {}
+    for mode in ("enc", "dec"):
+        h = cve.Cipher(synth.config_key(name), n, 5)
+        h.prefetch_keystream(3 * need); h.synchronize()
+        s0 = h.stats()
+        fn = h.encrypt_frames_device if mode == "enc" else h.decrypt_frames_device
+        fn(frames.data_ptr(), side, 3, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        s1 = h.stats()
+        out[mode] = (s1["cipher_ms"] - s0["cipher_ms"]) / 3
+    print(f"{name}: side={side} n={n}  encrypt {out['enc']*1e3:.1f} us/frame "
+          f"({2*F/out['enc']/1e6:.0f} GB/s of 2F, {15*F/out['enc']/1e6:.0f} GB/s moved)  "
+          f"decrypt {out['dec']*1e3:.1f} us/frame")
