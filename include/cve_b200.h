@@ -95,7 +95,70 @@ CVE_B200_API cve_status cve_cipher_decrypt_frame(cve_cipher* cipher,
 CVE_B200_API cve_status cve_cipher_seeds_drawn(const cve_cipher* cipher,
                                                uint64_t* out);
 
+/* ---- reference file pipelines -------------------- */
+
+/* Same layout and defaults as the reference (cve.h:86-93). */
+typedef struct cve_io_options {
+  uint32_t workers;    /* 0 -> 8 */
+  uint32_t rounds;     /* 0 -> 5 */
+  int serial;          /* accepted, ignored (scheduling only) */
+  uint16_t fps;        /* 0 -> 20; recorded in the container */
+  uint32_t raw_width;  /* nonzero -> input is raw RGB24 of these dims */
+  uint32_t raw_height;
+} cve_io_options;
+
+typedef enum cve_out_format {
+  CVE_OUT_AUTO = 0,
+  CVE_OUT_PPM = 1,
+  CVE_OUT_RAW = 2
+} cve_out_format;
+
+/* replaces cve.h:97-99.  P6 file, directory of P6 frames, or raw RGB24 ->
+ * CVE1 container (27-byte header + frame_count padded-square ciphertexts).
+ * Frames are padded on the device; the container is byte-identical to the
+ * reference's for PLCM keys. */
+CVE_B200_API cve_status cve_encrypt_file(const char* key_hex,
+                                         const cve_io_options* io,
+                                         const char* in_path,
+                                         const char* out_path);
+
+/* replaces cve.h:110-113.  CVE1 -> one P6 (single frame), a directory of
+ * frame_NNNNNN.ppm, or raw RGB24; cropped to the original dimensions.
+ * Explicit workers/rounds must match the header (MISMATCH), as must the key's
+ * map kind. */
+CVE_B200_API cve_status cve_decrypt_file(const char* key_hex,
+                                         const cve_io_options* io,
+                                         cve_out_format format,
+                                         const char* in_path,
+                                         const char* out_path);
+
 /* ---- additive: batched / device-resident / introspection ---------------- */
+
+/* The reference's padded_side (frame.cpp:19-26): smallest multiple of
+ * `workers` covering max(width, height). */
+CVE_B200_API cve_status cve_padded_side(uint32_t width, uint32_t height,
+                                        uint32_t workers, uint32_t* side_out);
+
+/* `count` unpadded width x height RGB24 frames (packed) -> `count` padded
+ * side x side ciphertexts (side = cve_padded_side(width, height, workers)).
+ * Padding (zero rows bottom, zero columns right, frame.cpp:28-39) is done on
+ * the device, so only width*height*3 bytes per frame cross PCIe. */
+CVE_B200_API cve_status cve_cipher_encrypt_frames_wh(cve_cipher* cipher,
+                                                     const uint8_t* rgb,
+                                                     uint32_t width,
+                                                     uint32_t height,
+                                                     uint32_t count,
+                                                     uint8_t* out_square);
+
+/* Inverse: `count` side x side ciphertexts -> `count` cropped width x height
+ * plaintexts (frame.cpp:41-51), cropped on the device. */
+CVE_B200_API cve_status cve_cipher_decrypt_frames_wh(cve_cipher* cipher,
+                                                     const uint8_t* square,
+                                                     uint32_t side,
+                                                     uint32_t width,
+                                                     uint32_t height,
+                                                     uint32_t count,
+                                                     uint8_t* out_rgb);
 
 /* `count` consecutive square frames, contiguous in host memory
  * (count*side*side*3 bytes), processed in place as frames k..k+count-1 of

@@ -48,6 +48,12 @@ class CveError(RuntimeError):
         super().__init__(f"cve status {status}: {detail}")
 
 
+class IoOptions(C.Structure):
+    """cve_io_options (reference cve.h:86-93)."""
+    _fields_ = [("workers", C.c_uint32), ("rounds", C.c_uint32), ("serial", C.c_int),
+                ("fps", C.c_uint16), ("raw_width", C.c_uint32), ("raw_height", C.c_uint32)]
+
+
 class Stats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("keystream_iters", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("prbg_launches", C.c_uint64),
@@ -86,6 +92,13 @@ def _load() -> C.CDLL:
         "cve_cipher_get_stats": (C.c_int, [vp, C.POINTER(Stats)]),
         "cve_cipher_take_prbg_times": (C.c_int, [vp, C.POINTER(C.c_float), C.c_size_t,
                                                  C.POINTER(C.c_size_t)]),
+        "cve_encrypt_file": (C.c_int, [C.c_char_p, C.POINTER(IoOptions), C.c_char_p, C.c_char_p]),
+        "cve_decrypt_file": (C.c_int, [C.c_char_p, C.POINTER(IoOptions), C.c_int, C.c_char_p,
+                                       C.c_char_p]),
+        "cve_padded_side": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]),
+        "cve_cipher_encrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]),
+        "cve_cipher_decrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                   C.c_uint32, vp]),
         "cve_keystream_generate": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
         "cve_derive_worker_lanes": (C.c_int, [C.c_char_p, C.c_uint32,
                                               C.POINTER(C.c_double),
@@ -145,13 +158,38 @@ def keystream_generate(lanes, length: int) -> np.ndarray:
     return out
 
 
+# ---- file pipelines (reference cve.h:84-113) ----------------------------------
+
+CVE_OUT_AUTO, CVE_OUT_PPM, CVE_OUT_RAW = 0, 1, 2
+
+
+def _io(workers=0, rounds=0, fps=0, raw=None) -> IoOptions:
+    w, h = raw if raw else (0, 0)
+    return IoOptions(workers, rounds, 0, fps, w, h)
+
+
+def encrypt_file(key_hex, in_path: str, out_path: str, workers: int = 0, rounds: int = 0,
+                 fps: int = 0, raw=None) -> None:
+    """P6 / directory of P6 / raw RGB24 (raw=(w, h)) -> CVE1 container."""
+    io = _io(workers, rounds, fps, raw)
+    _check(lib.cve_encrypt_file(_as_key(key_hex), C.byref(io), in_path.encode(),
+                                out_path.encode()))
+
+
+def decrypt_file(key_hex, in_path: str, out_path: str, fmt: int = CVE_OUT_AUTO,
+                 workers: int = 0, rounds: int = 0, io: bool = True) -> None:
+    """CVE1 -> P6 / directory of P6 / raw RGB24 (cropped)."""
+    opts = _io(workers, rounds) if io else None
+    _check(lib.cve_decrypt_file(_as_key(key_hex), C.byref(opts) if opts else None, fmt,
+                                in_path.encode(), out_path.encode()))
+
+
 # ---- frame model (reference frame.cpp:19-51) --------------------------------
 
 def padded_side(width: int, height: int, workers: int) -> int:
-    if width == 0 or height == 0 or workers == 0:
-        raise CveError(CVE_ERROR_INVALID_ARGUMENT, "dimensions and workers must be >= 1")
-    m = max(width, height)
-    return (m + workers - 1) // workers * workers
+    out = C.c_uint32()
+    _check(lib.cve_padded_side(width, height, workers, C.byref(out)))
+    return out.value
 
 
 def pad_to_square(rgb: np.ndarray, workers: int) -> np.ndarray:
@@ -244,6 +282,30 @@ class Cipher:
     def decrypt_frames_device(self, ptr: int, side: int, count: int, stream: int = 0) -> None:
         _check(lib.cve_cipher_decrypt_frames_async(self.handle, C.c_void_p(ptr), side,
                                                    count, C.c_void_p(stream)))
+
+    def encrypt_frames_wh(self, rgb: np.ndarray) -> np.ndarray:
+        """(count, h, w, 3) unpadded frames -> (count, side, side, 3) ciphertexts,
+        padded on the device."""
+        if rgb.ndim == 3:
+            rgb = rgb[None]
+        if rgb.dtype != np.uint8 or not rgb.flags.c_contiguous:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "need a C-contiguous uint8 array")
+        count, h, w = rgb.shape[:3]
+        side = padded_side(w, h, self.workers)
+        out = np.empty((count, side, side, 3), dtype=np.uint8)
+        _check(lib.cve_cipher_encrypt_frames_wh(self.handle, rgb.ctypes.data, w, h, count,
+                                                out.ctypes.data))
+        return out
+
+    def decrypt_frames_wh(self, square: np.ndarray, width: int, height: int) -> np.ndarray:
+        """(count, side, side, 3) ciphertexts -> (count, height, width, 3) plaintexts."""
+        if square.ndim == 3:
+            square = square[None]
+        count, side = square.shape[0], square.shape[1]
+        out = np.empty((count, height, width, 3), dtype=np.uint8)
+        _check(lib.cve_cipher_decrypt_frames_wh(self.handle, square.ctypes.data, side, width,
+                                                height, count, out.ctypes.data))
+        return out
 
     def synchronize(self) -> None:
         _check(lib.cve_cipher_synchronize(self.handle))

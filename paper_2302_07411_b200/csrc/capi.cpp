@@ -14,6 +14,8 @@
 
 #include "../../include/cve_b200.h"
 #include "engine.hpp"
+#include "fileio.hpp"
+#include "files.hpp"
 #include "keying.hpp"
 
 struct cve_cipher {
@@ -53,7 +55,12 @@ void require(bool ok, const char* what) {
 struct DeviceScope {
   int prev = -1;
   explicit DeviceScope(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    // No usable device: leave it to the engine to report INTERNAL once the
+    // host-side checks (files, keys) have run, as the reference orders them.
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      return;
+    }
     if (prev != dev && cudaSetDevice(dev) != cudaSuccess)
       cveb::raise(cveb::Errc::internal, "cannot select the handle's CUDA device");
   }
@@ -85,6 +92,12 @@ cve_status run_frames_async(cve_cipher* c, uint8_t* d_px, uint32_t side,
     c->engine->run_device(d_px, side, count, decrypt,
                           static_cast<cudaStream_t>(stream));
   });
+}
+
+int current_device() {
+  int dev = g_device;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  return dev;
 }
 
 }  // namespace
@@ -143,10 +156,8 @@ cve_status cve_cipher_create(const char* key_hex, uint32_t workers,
     require(out != nullptr, "out is null");
     require(key_hex != nullptr, "key_hex is null");
     const cveb::Key key = cveb::parse_key(key_hex);
-    int dev = g_device;
-    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) dev = 0;
     auto c = std::make_unique<cve_cipher>();
-    c->engine = std::make_unique<cveb::Engine>(key, workers, rounds, dev);
+    c->engine = std::make_unique<cveb::Engine>(key, workers, rounds, current_device());
     *out = c.release();
   });
 }
@@ -191,6 +202,79 @@ cve_status cve_cipher_decrypt_frames_async(cve_cipher* cipher,
                                            uint8_t* d_pixels, uint32_t side,
                                            uint32_t count, void* stream) {
   return run_frames_async(cipher, d_pixels, side, count, stream, true);
+}
+
+cve_status cve_encrypt_file(const char* key_hex, const cve_io_options* io,
+                            const char* in_path, const char* out_path) {
+  return guarded([&] {
+    cveb::FileOptions o;  // capi.cpp:143-164 defaults
+    if (io) {
+      if (io->workers) o.workers = io->workers;
+      if (io->rounds) o.rounds = io->rounds;
+      if (io->fps) o.fps = io->fps;
+      o.raw_width = io->raw_width;
+      o.raw_height = io->raw_height;
+    }
+    if (!key_hex) require(false, "key_hex is null");
+    if (!in_path || !out_path) require(false, "path is null");
+    if ((o.raw_width || o.raw_height) && !(o.raw_width && o.raw_height))
+      require(false, "raw input needs both dimensions");
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    cveb::encrypt_file(key_hex, o, in_path, out_path, dev);
+  });
+}
+
+cve_status cve_decrypt_file(const char* key_hex, const cve_io_options* io,
+                            cve_out_format format, const char* in_path,
+                            const char* out_path) {
+  return guarded([&] {
+    cveb::FileOptions o;
+    if (io) {
+      o.workers = io->workers;  // 0: follow the header
+      o.rounds = io->rounds;
+    }
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    cveb::decrypt_file(key_hex, io ? &o : nullptr, int(format), in_path, out_path, dev);
+  });
+}
+
+cve_status cve_padded_side(uint32_t width, uint32_t height, uint32_t workers,
+                           uint32_t* side_out) {
+  return guarded([&] {
+    require(side_out != nullptr, "side_out is null");
+    *side_out = cveb::padded_side_of(width, height, workers);
+  });
+}
+
+cve_status cve_cipher_encrypt_frames_wh(cve_cipher* cipher, const uint8_t* rgb,
+                                        uint32_t width, uint32_t height,
+                                        uint32_t count, uint8_t* out_square) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(rgb != nullptr && out_square != nullptr, "buffer is null");
+    require(count != 0, "count must be >= 1");
+    const uint32_t side = cveb::padded_side_of(width, height, cipher->engine->workers());
+    DeviceScope scope(cipher->engine->device());
+    cipher->engine->run_host_io(
+        cveb::Engine::HostIo{rgb, width, height, out_square, side, side}, side, count, false);
+  });
+}
+
+cve_status cve_cipher_decrypt_frames_wh(cve_cipher* cipher, const uint8_t* square,
+                                        uint32_t side, uint32_t width,
+                                        uint32_t height, uint32_t count,
+                                        uint8_t* out_rgb) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(square != nullptr && out_rgb != nullptr, "buffer is null");
+    require(side != 0 && width != 0 && height != 0, "dimensions must be >= 1");
+    require(count != 0, "count must be >= 1");
+    DeviceScope scope(cipher->engine->device());
+    cipher->engine->run_host_io(
+        cveb::Engine::HostIo{square, side, side, out_rgb, width, height}, side, count, true);
+  });
 }
 
 cve_status cve_cipher_synchronize(cve_cipher* cipher) {

@@ -420,27 +420,52 @@ void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
 }
 
 void Engine::run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt) {
+  run_host_io(HostIo{px, side, side, px, side, side}, side, count, decrypt);
+}
+
+void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool decrypt) {
   draw_and_check(side, count);
+  if (io.in_w > side || io.in_h > side || io.out_w > side || io.out_h > side ||
+      !io.in_w || !io.in_h || !io.out_w || !io.out_h)
+    raise(Errc::invalid_argument, "frame region exceeds the padded side");
   const Geom g = geometry(side);
   ensure_ring(uint64_t(r_) * g.region);
   ensure_buffers(g, kSlots);
+  const uint64_t row = uint64_t(side) * 3;
+  const uint64_t in_fb = uint64_t(io.in_w) * io.in_h * 3;
+  const uint64_t out_fb = uint64_t(io.out_w) * io.out_h * 3;
 
   for (uint32_t f = 0; f < count; ++f) {
     const uint32_t seed = coord_.next_seed();
     const uint32_t slot = f % kSlots;
-    uint8_t* host = px + uint64_t(f) * g.frame_bytes;
+    const uint8_t* hin = io.in + uint64_t(f) * in_fb;
+    uint8_t* hout = io.out + uint64_t(f) * out_fb;
     uint8_t* dbuf = slots_[slot];
     ck(cudaStreamWaitEvent(s_h2d_, slot_free_[slot], 0), "wait slot");
-    ck(cudaMemcpyAsync(dbuf, host, g.frame_bytes, cudaMemcpyHostToDevice, s_h2d_),
-       "H2D");
+    if (io.in_w == side && io.in_h == side) {
+      ck(cudaMemcpyAsync(dbuf, hin, g.frame_bytes, cudaMemcpyHostToDevice, s_h2d_), "H2D");
+    } else {  // pad on the device: only the w*h payload crosses PCIe
+      ck(cudaMemcpy2DAsync(dbuf, row, hin, uint64_t(io.in_w) * 3, uint64_t(io.in_w) * 3,
+                           io.in_h, cudaMemcpyHostToDevice, s_h2d_), "H2D 2D");
+      if (io.in_w < side)
+        ck(cudaMemset2DAsync(dbuf + uint64_t(io.in_w) * 3, row, 0,
+                             uint64_t(side - io.in_w) * 3, io.in_h, s_h2d_), "pad right");
+      if (io.in_h < side)
+        ck(cudaMemsetAsync(dbuf + uint64_t(io.in_h) * row, 0,
+                           uint64_t(side - io.in_h) * row, s_h2d_), "pad bottom");
+    }
     cudaEvent_t in = ev_get();
     ck(cudaEventRecord(in, s_h2d_), "record");
     ck(cudaStreamWaitEvent(s_work_, in, 0), "wait H2D");
     ev_put(in);
     enqueue_frame(dbuf, g, seed, decrypt);
     ck(cudaStreamWaitEvent(s_d2h_, consumers_.back().done, 0), "wait work");
-    ck(cudaMemcpyAsync(host, dbuf, g.frame_bytes, cudaMemcpyDeviceToHost, s_d2h_),
-       "D2H");
+    if (io.out_w == side && io.out_h == side) {
+      ck(cudaMemcpyAsync(hout, dbuf, g.frame_bytes, cudaMemcpyDeviceToHost, s_d2h_), "D2H");
+    } else {  // crop on the way out
+      ck(cudaMemcpy2DAsync(hout, uint64_t(io.out_w) * 3, dbuf, row, uint64_t(io.out_w) * 3,
+                           io.out_h, cudaMemcpyDeviceToHost, s_d2h_), "D2H 2D");
+    }
     ck(cudaEventRecord(slot_free_[slot], s_d2h_), "record");
   }
   ck(cudaStreamSynchronize(s_d2h_), "frame pipeline");

@@ -56,6 +56,17 @@ class Engine {
 
   // `count` frames in host memory, in place.
   void run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt);
+  // Host frames whose input/output may be smaller than the side x side
+  // working square: input w*h regions are padded on the device (zero rows
+  // bottom, zero columns right, frame.cpp:28-39); output regions are the
+  // top-left w*h crop (frame.cpp:41-51).  Frames are packed densely.
+  struct HostIo {
+    const uint8_t* in;
+    uint32_t in_w, in_h;
+    uint8_t* out;
+    uint32_t out_w, out_h;
+  };
+  void run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool decrypt);
   // `count` frames in device memory, in place, ordered on `user` stream.
   void run_device(uint8_t* d_px, uint32_t side, uint32_t count, bool decrypt,
                   cudaStream_t user);

@@ -1,0 +1,143 @@
+// File pipelines on the GPU engine: plaintext frames
+// (P6 / directory / raw) -> CVE1 container and back, through the same Engine
+// as the per-frame ABI.  Order of checks and error codes follow the
+// reference's cve_encrypt_file / cve_decrypt_file (capi.cpp:143-164,
+// 262-333).  Differences: frames travel to the GPU unpadded and are padded
+// (and, on decrypt, cropped) on the device; the next batch is read from disk
+// while the GPU works on the current one.
+#include "files.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <future>
+
+#include "engine.hpp"
+#include "fileio.hpp"
+
+namespace cveb {
+namespace {
+
+constexpr uint64_t kBatchBytes = 64ull << 20;  // host staging per batch
+
+struct Pinned {
+  uint8_t* p = nullptr;
+  explicit Pinned(size_t n) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1),
+                      cudaHostAllocDefault) != cudaSuccess)
+      raise(Errc::internal, "cudaHostAlloc failed");
+  }
+  ~Pinned() { cudaFreeHost(p); }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+};
+
+uint32_t batch_frames(uint64_t frame_bytes, uint32_t total) {
+  const uint64_t b = std::max<uint64_t>(1, kBatchBytes / std::max<uint64_t>(frame_bytes, 1));
+  return uint32_t(std::min<uint64_t>(b, std::max<uint32_t>(total, 1)));
+}
+
+}  // namespace
+
+void encrypt_file(const char* key_hex, const FileOptions& opt, const char* in_path,
+                  const char* out_path, int device) {
+  if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
+  if (!in_path || !out_path) raise(Errc::invalid_argument, "path is null");
+  if (opt.raw_width || opt.raw_height) {
+    if (!opt.raw_width || !opt.raw_height)
+      raise(Errc::invalid_argument, "raw input needs both dimensions");
+  }
+  if (opt.workers > 0xFFFF) raise(Errc::invalid_argument, "workers must fit the container header");
+  if (opt.rounds < 1 || opt.rounds > 255) raise(Errc::invalid_argument, "rounds must be in 1..255");
+  const Key key = parse_key(key_hex);
+
+  PlainSource src(in_path, opt.raw_width, opt.raw_height);
+  CveHeader h;
+  h.map_kind = uint8_t(key.kind);
+  h.side = padded_side_of(src.width(), src.height(), opt.workers);
+  h.orig_width = src.width();
+  h.orig_height = src.height();
+  h.workers = uint16_t(opt.workers);
+  h.rounds = uint8_t(opt.rounds);
+  h.fps = opt.fps;
+  h.frame_count = src.count();
+
+  Engine engine(key, opt.workers, opt.rounds, device);
+  ContainerOut out(out_path, h);
+  const uint64_t in_fb = uint64_t(h.orig_width) * h.orig_height * 3;
+  const uint64_t sq_fb = uint64_t(h.side) * h.side * 3;
+  const uint32_t B = batch_frames(sq_fb, h.frame_count);
+  Pinned in_buf[2] = {Pinned(B * in_fb), Pinned(B * in_fb)};
+  Pinned out_buf(B * sq_fb);
+
+  auto read_batch = [&](uint8_t* dst, uint32_t nb) {
+    for (uint32_t i = 0; i < nb; ++i) src.next(dst + i * in_fb);
+  };
+  uint32_t done = 0, cur = 0;
+  uint32_t nb = std::min(B, h.frame_count);
+  read_batch(in_buf[0].p, nb);
+  while (done < h.frame_count) {
+    const uint32_t next_nb = std::min(B, h.frame_count - done - nb);
+    std::future<void> prefetch;
+    if (next_nb)
+      prefetch = std::async(std::launch::async, read_batch, in_buf[cur ^ 1].p, next_nb);
+    engine.run_host_io(Engine::HostIo{in_buf[cur].p, h.orig_width, h.orig_height,
+                                      out_buf.p, h.side, h.side},
+                       h.side, nb, /*decrypt=*/false);
+    out.put(out_buf.p, nb);
+    if (prefetch.valid()) prefetch.get();
+    done += nb;
+    nb = next_nb;
+    cur ^= 1;
+  }
+  out.finish();
+}
+
+void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
+                  const char* in_path, const char* out_path, int device) {
+  if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
+  if (!in_path || !out_path) raise(Errc::invalid_argument, "path is null");
+  if (format < 0 || format > 2) raise(Errc::invalid_argument, "unknown output format");
+  const Key key = parse_key(key_hex);
+
+  ContainerIn in(in_path);
+  const CveHeader h = in.header();
+  if (uint8_t(key.kind) != h.map_kind)
+    raise(Errc::mismatch, "key map kind does not match the container");
+  if (opt) {
+    if (opt->workers && opt->workers != h.workers)
+      raise(Errc::mismatch, "workers does not match the container");
+    if (opt->rounds && opt->rounds != h.rounds)
+      raise(Errc::mismatch, "rounds does not match the container");
+  }
+  Engine engine(key, h.workers, h.rounds, device);
+  PlainSink sink(out_path, /*raw=*/format == 2, h.frame_count);
+  const uint64_t out_fb = uint64_t(h.orig_width) * h.orig_height * 3;
+  const uint64_t sq_fb = uint64_t(h.side) * h.side * 3;
+  const uint32_t B = batch_frames(sq_fb, h.frame_count);
+  Pinned in_buf[2] = {Pinned(B * sq_fb), Pinned(B * sq_fb)};
+  Pinned out_buf(B * out_fb);
+
+  uint32_t done = 0, cur = 0;
+  uint32_t nb = std::min(B, h.frame_count);
+  in.next(in_buf[0].p, nb);
+  while (done < h.frame_count) {
+    const uint32_t next_nb = std::min(B, h.frame_count - done - nb);
+    std::future<void> prefetch;
+    if (next_nb)
+      prefetch = std::async(std::launch::async,
+                            [&, dst = in_buf[cur ^ 1].p, k = next_nb] { in.next(dst, k); });
+    engine.run_host_io(Engine::HostIo{in_buf[cur].p, h.side, h.side, out_buf.p,
+                                      h.orig_width, h.orig_height},
+                       h.side, nb, /*decrypt=*/true);
+    for (uint32_t i = 0; i < nb; ++i)
+      sink.put(out_buf.p + i * out_fb, h.orig_width, h.orig_height);
+    if (prefetch.valid()) prefetch.get();
+    done += nb;
+    nb = next_nb;
+    cur ^= 1;
+  }
+  sink.finish();
+}
+
+}  // namespace cveb

@@ -99,6 +99,11 @@ def plcm_stream(xa, pa, xb, pb, n) -> np.ndarray:
     return out
 
 
+class RefIo(C.Structure):
+    _fields_ = [("workers", C.c_uint32), ("rounds", C.c_uint32), ("serial", C.c_int),
+                ("fps", C.c_uint16), ("raw_width", C.c_uint32), ("raw_height", C.c_uint32)]
+
+
 class Reference:
     """The reference's own C ABI (cve.h) from oracle/_ref/libcve_ref.so."""
     lib = None
@@ -119,6 +124,9 @@ class Reference:
             L.cve_cipher_decrypt_frame.argtypes = [vp, vp, C.c_uint32]
             L.cve_cipher_seeds_drawn.argtypes = [vp, C.POINTER(C.c_uint64)]
             L.cve_last_error.restype = C.c_char_p
+            L.cve_encrypt_file.argtypes = [C.c_char_p, C.POINTER(RefIo), C.c_char_p, C.c_char_p]
+            L.cve_decrypt_file.argtypes = [C.c_char_p, C.POINTER(RefIo), C.c_int, C.c_char_p,
+                                           C.c_char_p]
             cls.lib = L
         return cls.lib
 
@@ -142,3 +150,15 @@ class Reference:
 
     def decrypt(self, frame: np.ndarray) -> int:
         return Reference.lib.cve_cipher_decrypt_frame(self.h, _ptr(frame), frame.shape[0])
+
+
+def ref_encrypt_file(key_hex, in_path, out_path, workers=0, rounds=0, fps=0, raw=None):
+    w, h = raw if raw else (0, 0)
+    io = RefIo(workers, rounds, 0, fps, w, h)
+    return Reference.load().cve_encrypt_file(key_hex.encode(), C.byref(io), in_path.encode(),
+                                             out_path.encode())
+
+
+def ref_decrypt_file(key_hex, in_path, out_path, fmt=0):
+    return Reference.load().cve_decrypt_file(key_hex.encode(), None, fmt, in_path.encode(),
+                                             out_path.encode())
