@@ -132,6 +132,15 @@ CVE_B200_API cve_status cve_decrypt_file(const char* key_hex,
                                          const char* in_path,
                                          const char* out_path);
 
+/* replaces cve.h:149-150 (row f3).  byte_count generator bytes for external
+ * statistical suites: split over the `workers` (0 -> 8) generators derived
+ * from the key, the first byte_count % workers getting one extra byte, each
+ * worker's fresh stream written in worker order -- byte-identical to the
+ * reference.  The generators run concurrently on the GPU. */
+CVE_B200_API cve_status cve_nist_export(const char* key_hex, uint32_t workers,
+                                        uint64_t byte_count,
+                                        const char* out_path);
+
 /* ---- additive: batched / device-resident / introspection ---------------- */
 
 /* The reference's padded_side (frame.cpp:19-26): smallest multiple of

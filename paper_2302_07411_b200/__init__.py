@@ -95,6 +95,7 @@ def _load() -> C.CDLL:
         "cve_encrypt_file": (C.c_int, [C.c_char_p, C.POINTER(IoOptions), C.c_char_p, C.c_char_p]),
         "cve_decrypt_file": (C.c_int, [C.c_char_p, C.POINTER(IoOptions), C.c_int, C.c_char_p,
                                        C.c_char_p]),
+        "cve_nist_export": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint64, C.c_char_p]),
         "cve_padded_side": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]),
         "cve_cipher_encrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]),
         "cve_cipher_decrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -182,6 +183,12 @@ def decrypt_file(key_hex, in_path: str, out_path: str, fmt: int = CVE_OUT_AUTO,
     opts = _io(workers, rounds) if io else None
     _check(lib.cve_decrypt_file(_as_key(key_hex), C.byref(opts) if opts else None, fmt,
                                 in_path.encode(), out_path.encode()))
+
+
+def nist_export(key_hex, workers: int, byte_count: int, out_path: str) -> None:
+    """Raw generator bytes for statistical suites (reference cve_nist_export)."""
+    _check(lib.cve_nist_export(_as_key(key_hex) if key_hex is not None else None, workers,
+                               byte_count, out_path.encode()))
 
 
 # ---- frame model (reference frame.cpp:19-51) --------------------------------

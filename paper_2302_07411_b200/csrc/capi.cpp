@@ -240,6 +240,15 @@ cve_status cve_decrypt_file(const char* key_hex, const cve_io_options* io,
   });
 }
 
+cve_status cve_nist_export(const char* key_hex, uint32_t workers,
+                           uint64_t byte_count, const char* out_path) {
+  return guarded([&] {
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    cveb::keystream_export(key_hex, workers, byte_count, out_path, dev);
+  });
+}
+
 cve_status cve_padded_side(uint32_t width, uint32_t height, uint32_t workers,
                            uint32_t* side_out) {
   return guarded([&] {

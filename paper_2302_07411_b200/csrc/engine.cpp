@@ -576,4 +576,57 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
   cleanup();
 }
 
+KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, int device)
+    : n_(uint32_t(lanes.size())) {
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  configure_kernels_once(device);
+  const uint32_t nl = 2 * n_;
+  std::vector<LaneConst> lc(nl);
+  std::vector<double> x0(nl);
+  for (uint32_t i = 0; i < n_; ++i) {
+    lc[2 * i] = make_lane_const(lanes[i].a.p);
+    lc[2 * i + 1] = make_lane_const(lanes[i].b.p);
+    x0[2 * i] = lanes[i].a.x0;
+    x0[2 * i + 1] = lanes[i].b.x0;
+  }
+  ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+  pb_ = alloc_prbg(nl);
+  ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
+  ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice), "upload");
+  init_prbg(pb_, d_lc_, x0.data(), nl, s_);
+  ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
+}
+
+KeystreamSource::~KeystreamSource() {
+  if (s_) cudaStreamSynchronize(s_);
+  free_prbg(pb_);
+  cudaFree(d_lc_);
+  cudaFree(d_buf_);
+  if (s_) cudaStreamDestroy(s_);
+}
+
+// Generates whole chunks of max_iters iterations; a request that does not
+// end on a chunk boundary leaves the rest of the chunk for the next call.
+void KeystreamSource::next(uint8_t* host, uint64_t bytes) {
+  const uint64_t cb = chunk_bytes();
+  if (bytes > cb) raise(Errc::invalid_argument, "request larger than a chunk");
+  uint64_t got = 0;
+  while (got < bytes) {
+    if (carry_ == have_) {
+      launch_prbg_chain(pb_, slot_, d_lc_, pb_.max_iters, 2 * n_, s_);
+      launch_prbg_verify(pb_, slot_, d_lc_, d_buf_, cb, 0, pb_.max_iters, 2 * n_, s_);
+      ck(cudaGetLastError(), "keystream launch");
+      slot_ ^= 1;
+      carry_ = 0;
+      have_ = cb;
+    }
+    const uint64_t take = std::min(bytes - got, have_ - carry_);
+    ck(cudaMemcpy2DAsync(host + got, cb, d_buf_ + carry_, cb, take, n_,
+                         cudaMemcpyDeviceToHost, s_), "D2H keystream");
+    ck(cudaStreamSynchronize(s_), "keystream");
+    carry_ += take;
+    got += take;
+  }
+}
+
 }  // namespace cveb

@@ -147,4 +147,28 @@ class Engine {
 // Reference Prbg with explicit lanes, generated by K1 on the current device.
 void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len);
 
+// Fresh generators for a set of workers (reference WorkerParams::make_prbg,
+// keying.cpp:154-162), advanced together on the GPU; next() copies the next
+// `bytes` (<= chunk_bytes()) of every worker to host memory, worker-major
+// with a stride of chunk_bytes().
+class KeystreamSource {
+ public:
+  KeystreamSource(const std::vector<WorkerLanes>& lanes, int device);
+  ~KeystreamSource();
+  KeystreamSource(const KeystreamSource&) = delete;
+  KeystreamSource& operator=(const KeystreamSource&) = delete;
+  uint64_t chunk_bytes() const { return uint64_t(pb_.max_iters) * 6; }
+  void next(uint8_t* host, uint64_t bytes);
+
+ private:
+  uint32_t n_;
+  PrbgBuffers pb_{};
+  LaneConst* d_lc_ = nullptr;
+  uint8_t* d_buf_ = nullptr;
+  cudaStream_t s_ = nullptr;
+  int slot_ = 0;
+  uint64_t carry_ = 0;   // bytes of the current chunk already handed out
+  uint64_t have_ = 0;    // bytes generated in the current chunk
+};
+
 }  // namespace cveb

@@ -140,4 +140,52 @@ void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
   sink.finish();
 }
 
+// Reference cve_nist_export (capi.cpp:385-415): the byte budget split over
+// the n workers derived from the key (the first byte_count % n workers get
+// one extra byte); each worker's fresh generator stream is written in
+// worker order.  All n generators run at once on the GPU (K1); chunks are
+// copied back and written at each worker's file offset.
+void keystream_export(const char* key_hex, uint32_t workers, uint64_t byte_count,
+                      const char* out_path, int device) {
+  if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
+  if (!out_path) raise(Errc::invalid_argument, "path is null");
+  if (byte_count == 0) raise(Errc::invalid_argument, "byte_count must be >= 1");
+  const uint32_t n = workers ? workers : 8;
+  const Key key = parse_key(key_hex);
+  Coordinator coord(key);
+  const std::vector<WorkerLanes> lanes = coord.derive_workers(n);
+
+  std::FILE* out = std::fopen(out_path, "wb");
+  if (!out) raise(Errc::io, "cannot open output file");
+  struct Closer {
+    std::FILE* f;
+    ~Closer() {
+      if (f) std::fclose(f);
+    }
+  } closer{out};
+
+  const uint64_t base = byte_count / n, extra = byte_count % n;
+  const uint64_t longest = base + (extra ? 1 : 0);
+  std::vector<uint64_t> start(n), len(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    len[i] = base + (i < extra ? 1 : 0);
+    start[i] = i ? start[i - 1] + len[i - 1] : 0;
+  }
+  KeystreamSource src(lanes, device);
+  const uint64_t chunk = src.chunk_bytes();
+  Pinned host(size_t(chunk) * n);
+  for (uint64_t done = 0; done < longest; done += chunk) {
+    const uint64_t now = std::min(chunk, longest - done);
+    src.next(host.p, now);  // now bytes per worker, worker-major
+    for (uint32_t i = 0; i < n; ++i) {
+      if (done >= len[i]) continue;
+      const uint64_t take = std::min(now, len[i] - done);
+      if (std::fseek(out, long(start[i] + done), SEEK_SET) != 0 ||
+          std::fwrite(host.p + uint64_t(i) * chunk, 1, take, out) != take)
+        raise(Errc::io, "short write");
+    }
+  }
+  if (std::fflush(out) != 0) raise(Errc::io, "short write");
+}
+
 }  // namespace cveb

@@ -20,4 +20,9 @@ void encrypt_file(const char* key_hex, const FileOptions& opt, const char* in_pa
 void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
                   const char* in_path, const char* out_path, int device);
 
+// Reference cve_nist_export: byte_count generator bytes split over the
+// workers derived from the key, written worker after worker.
+void keystream_export(const char* key_hex, uint32_t workers, uint64_t byte_count,
+                      const char* out_path, int device);
+
 }  // namespace cveb

@@ -127,6 +127,7 @@ class Reference:
             L.cve_encrypt_file.argtypes = [C.c_char_p, C.POINTER(RefIo), C.c_char_p, C.c_char_p]
             L.cve_decrypt_file.argtypes = [C.c_char_p, C.POINTER(RefIo), C.c_int, C.c_char_p,
                                            C.c_char_p]
+            L.cve_nist_export.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, C.c_char_p]
             cls.lib = L
         return cls.lib
 

@@ -137,7 +137,30 @@ def test_raw_video_round_trip_and_auto_directory(tmp_path):
     assert (tmp_path / "frames" / "frame_000001.ppm").exists()
 
 
+@pytest.mark.gpu
+@need_ref
+@pytest.mark.parametrize("workers,count", [(2, 100000), (3, 1000001), (0, 5 << 20), (64, 999)])
+def test_nist_export_matches_reference(tmp_path, workers, count):
+    # row f3; reference capi.cpp:385-415, test_capi.cpp:399-418
+    key = synth.config_key("C4")
+    cve.nist_export(key, workers, count, str(tmp_path / "ours.bin"))
+    assert Reference.load().cve_nist_export(key.encode(), workers, count,
+                                            str(tmp_path / "ref.bin").encode()) == 0
+    ours = blob(tmp_path / "ours.bin")
+    assert len(ours) == count
+    assert ours == blob(tmp_path / "ref.bin")
+
+
 # ---- CPU: argument and format checks (raised before any device work) --------
+
+def test_nist_export_argument_errors(tmp_path):
+    for args, st in (((PLCM, 2, 0), cve.CVE_ERROR_INVALID_ARGUMENT),
+                     ((None, 2, 100), cve.CVE_ERROR_INVALID_ARGUMENT),
+                     (("00ff", 2, 100), cve.CVE_ERROR_BAD_KEY)):
+        with pytest.raises(cve.CveError) as e:
+            cve.nist_export(*args, str(tmp_path / "x.bin"))
+        assert e.value.status == st
+
 
 def status_of(fn, *a, **k):
     try:
