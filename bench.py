@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--clips", type=int, default=32,
+    ap.add_argument("--clips", type=int, default=16,
                     help="independent clips for the labelled multi-clip line (0: skip)")
     return ap.parse_args()
 

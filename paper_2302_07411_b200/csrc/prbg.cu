@@ -98,25 +98,27 @@ __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
   return __fma_rn(num, yh, corr);
 }
 
-// Is y exactly the reference's next orbit value after x?
+// Is y exactly the reference's next orbit value after x?  The common path is
+// one FMA residual test; values whose low word is 0 or p's (the guard set
+// {0, 0.5, 1, p}, powers of two) or that are tiny are decided exactly.
 __device__ __forceinline__ bool plcm_verify(double x, double y, const LaneConst& c) {
   const double f = x > 0.5 ? __dsub_rn(1.0, x) : x;
   const bool low = f < c.p;
   const double num = low ? f : __dsub_rn(f, c.p);
   const double den = low ? c.p : c.q;
-  if (y == 0.0 || y == c.p || y == 0.5 || y == 1.0) return false;  // guard hit
   const unsigned hi = unsigned(__double2hiint(y));
   const unsigned lo = unsigned(__double2loint(y));
   const unsigned ex = hi & 0x7FF00000u;
-  if ((lo == 0u && (hi & 0x000FFFFFu) == 0u) || ex < (53u << 20))
-    return y == __ddiv_rn(num, den);  // power of two / tiny: decide exactly
-  // y is RN(num/den) iff |num - den*y| < den*ulp(y)/2 (no quotient is a
-  // midpoint).  The FMA residual is exact for any faithful y, and any error
-  // in it can only turn a pass into a (safe) fail.
+  // y is RN(num/den) iff |num - den*y| < den*ulp(y)/2 when y is not a power
+  // of two (no quotient is a midpoint).  The FMA residual is exact for any
+  // faithful y, and any error in it can only turn a pass into a (safe) fail.
   const double r = __fma_rn(-y, den, num);
   const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
   const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
-  return fabs(r) < thr;
+  bool ok = fabs(r) < thr;
+  if (lo == 0u || lo == c.plo || ex < (53u << 20))  // rare: decide exactly
+    ok = y == __ddiv_rn(num, den) && !(y == 0.0 || y == c.p || y == 0.5 || y == 1.0);
+  return ok;
 }
 
 __global__ void __launch_bounds__(128)
@@ -161,59 +163,70 @@ __global__ void __launch_bounds__(128, 1)
 // (2) Verify every step in parallel against the reference's exact step, and
 // emit the keystream: 6 bytes per iteration per worker = the little-endian
 // low 48 mantissa bits of x_a ^ x_b (extract_bytes, chaos.cpp:46-56).
-// Thread = (worker, 8-iteration group); failures flag the worker.  Group 0
-// also checks continuity: the launch must start at the previous launch's
-// verified end point (it may not, after an exact fix-up of that launch).
+// Thread = (lane, 8-iteration group), lanes fastest (coalesced orbit loads);
+// lanes a/b of a worker are shuffle partners: the even one emits iterations
+// 0-3 of the group, the odd one 4-7.  Group 0 also checks continuity: the
+// launch must start where the previous launch verifiably ended.
 __global__ void __launch_bounds__(256)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
                        const double* __restrict__ verified_end,
                        const LaneConst* __restrict__ lcs,
                        const double* __restrict__ orbit, uint32_t iters,
-                       uint32_t nworkers, uint8_t* __restrict__ ring,
+                       uint32_t nlanes, uint8_t* __restrict__ ring,
                        uint64_t ring_bytes, uint64_t it0,
                        unsigned* __restrict__ bad) {
   const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint32_t groups = iters / 8;
-  if (gid >= uint64_t(groups) * nworkers) return;
-  const uint32_t w = uint32_t(gid % nworkers);  // workers fastest: coalesced
-  const uint32_t g = uint32_t(gid / nworkers);
-  const uint32_t nl = 2 * nworkers;
-  const LaneConst ca = lcs[2 * w], cb = lcs[2 * w + 1];
+  const bool live = gid < uint64_t(groups) * nlanes;
+  // idle threads of the last warp shadow a real (lane, group) so that the
+  // shuffles see full warps; they store nothing
+  const uint64_t me = live ? gid : gid % nlanes;
+  const uint32_t l = uint32_t(me % nlanes);
+  const uint32_t g = uint32_t(me / nlanes);
+  const LaneConst c = lcs[l];
   const size_t i0 = size_t(g) * 8;
-  double xa, xb;
+  double x;
   bool ok = true;
   if (g) {
-    xa = orbit[(i0 - 1) * nl + 2 * w];
-    xb = orbit[(i0 - 1) * nl + 2 * w + 1];
+    x = orbit[(i0 - 1) * nlanes + l];
   } else {
-    xa = ckpt[2 * w];
-    xb = ckpt[2 * w + 1];
-    ok = xa == verified_end[2 * w] && xb == verified_end[2 * w + 1];
+    x = ckpt[l];
+    ok = x == verified_end[l];
   }
   uint32_t lo[8], hi[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
-    const double2 v = *reinterpret_cast<const double2*>(orbit + (i0 + t) * nl + 2 * w);
-    ok &= plcm_verify(xa, v.x, ca);
-    ok &= plcm_verify(xb, v.y, cb);
-    xa = v.x;
-    xb = v.y;
-    lo[t] = unsigned(__double2loint(v.x)) ^ unsigned(__double2loint(v.y));
-    hi[t] = (unsigned(__double2hiint(v.x)) ^ unsigned(__double2hiint(v.y))) & 0xFFFFu;
+    const double y = orbit[(i0 + t) * nlanes + l];
+    ok &= plcm_verify(x, y, c);
+    x = y;
+    lo[t] = unsigned(__double2loint(y));
+    hi[t] = unsigned(__double2hiint(y));
   }
-  if (!ok) atomicOr(bad + w, 1u);
-  uint32_t wd[12];
+  if (!ok && live) atomicOr(bad + (l >> 1), 1u);
+  const uint32_t odd = l & 1u;
+  uint32_t mlo[4], mhi[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {  // two iterations -> three words
-    wd[3 * k] = lo[2 * k];
-    wd[3 * k + 1] = hi[2 * k] | (lo[2 * k + 1] << 16);
-    wd[3 * k + 2] = (lo[2 * k + 1] >> 16) | (hi[2 * k + 1] << 16);
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t slo = odd ? lo[t] : lo[t + 4];
+    const uint32_t shi = odd ? hi[t] : hi[t + 4];
+    const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
+    const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
+    mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
+    mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
   }
+  const uint32_t w0 = mlo[0], w1 = mhi[0] | (mlo[1] << 16),
+                 w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
+                 w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
+  if (!live) return;
   const uint64_t off = ((it0 + i0) * 6u) % ring_bytes;  // 48-byte aligned
-  uint4* dst = reinterpret_cast<uint4*>(ring + uint64_t(w) * ring_bytes + off);
-  dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-  dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
-  dst[2] = make_uint4(wd[8], wd[9], wd[10], wd[11]);
+  uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
+  if (!odd) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+    *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w4, w5);
+  } else {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+    *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w2, w3, w4, w5);
+  }
 }
 
 // (3) One thread per worker.  Verified: advance the verified end point to
@@ -285,9 +298,9 @@ void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
                         uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
                         uint32_t iters, uint32_t nlanes, cudaStream_t s) {
   const uint32_t nw = nlanes / 2;
-  const uint64_t threads = uint64_t(iters / 8) * nw;
+  const uint64_t threads = uint64_t(iters / 8) * nlanes;
   k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
-      b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nw, ring, ring_bytes,
+      b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nlanes, ring, ring_bytes,
       it0, b.bad);
   k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.orbit[slot], b.verified_end, lc,
                                                 iters, nw, ring, ring_bytes, it0,
