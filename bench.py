@@ -352,6 +352,20 @@ def run_b200(args) -> None:
     ns_iter = chain_ms * 1e6 / max(iters_timed, 1)
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     cipher_gbs = frames_timed * alg_bytes / (cipher_ms / 1e3) / 1e9 if cipher_ms else None
+    # dominant kernel, per launch: algorithmic bytes of the frames its
+    # iterations serve / its mean CUDA-event duration on its own stream
+    iters_per_frame = synth.ROUNDS * side * side // (2 * n)
+    launch_iters = iters_timed / max(len(chain_times), 1)
+    alg_per_launch = alg_bytes * launch_iters / iters_per_frame
+    chain_gbs = (alg_per_launch / (float(np.mean(chain_times)) / 1e3) / 1e9
+                 if len(chain_times) else None)
+    traffic_per_launch = None
+    try:  # DRAM bytes of the chain kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)["k_prbg_chain"]
+        traffic_per_launch = tr["dram_bytes"] / tr["iterations"] * launch_iters
+    except (OSError, KeyError, ValueError, ZeroDivisionError):
+        pass
     line = {
         "metric": "encrypted frames/s (5 rounds)", "value": value, "unit": "frames/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
@@ -364,13 +378,21 @@ def run_b200(args) -> None:
                 "d2h_bytes_per_step": F * fb, "api": "cve_cipher_encrypt_frames (pinned)"},
         "gpu_launches": launches,
         "roofline": {
-            "bound": "hbm", "kernel": "whole step vs BASELINE.json roofline "
-            "(2*side^2*3 B/frame at peak HBM; the FP64-throughput bound is not the binding one)",
-            "achieved": step_gbs, "peak": hbm, "unit": "GB/s", "frac": step_gbs / hbm,
-            "peak_source": hbm_src, "traffic": None},
+            "bound": "hbm", "kernel": "k_prbg_chain (dominant: %.0f%% of the step)"
+            % (100 * chain_ms / ms if ms else 0),
+            "achieved": chain_gbs, "peak": hbm, "unit": "GB/s",
+            "frac": chain_gbs / hbm if chain_gbs else None, "peak_source": hbm_src,
+            "traffic": traffic_per_launch,
+            "algorithmic_bytes_per_launch": alg_per_launch,
+            "note": "BASELINE.json roofline: 2*side^2*3 B per frame (SURVEY 8(d)) at peak "
+                    "HBM; the kernel is bound by the FP64 dependency latency of 2n "
+                    "sequential orbits instead (see 'chain')"},
         "chain": {
             "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
             "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
+            "cycles_per_iteration": ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3,
+            "static_schedule_cycles": 44,
+            "frac_of_static_schedule": 44 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
             "launches": int(len(chain_times)),
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,
