@@ -13,7 +13,8 @@
 //     branch-free speculative step -- exact case predicates, exact numerator,
 //     and the quotient num/d as fma(num, RN(1/d), corr) where the ~2^-53
 //     correction corr ~= num * (1/d - RN(1/d)) is formed straight from x by
-//     one FMA, so only DADD -> DADD -> FSEL -> DFMA remain on the chain.  Each orbit value is stored (one coalesced 8-byte store).
+//     one FMA per case, so only DADD -> DADD -> DFMA -> FSEL remain on the
+//     chain.  Each orbit value is stored (one coalesced 8-byte store).
 //   verify+emit kernel (whole GPU, in parallel over steps): re-derives every
 //     step with the reference's own case logic (chaos.cpp:28-32), proves the
 //     produced quotient is the correctly rounded one (|num - d*y| < d*ulp(y)/2
@@ -78,24 +79,22 @@ __device__ __forceinline__ double plcm_exact(double x, double p, double q) {
 // Speculative chain step.  Cases (reference: fold x>0.5 to 1-x, then
 // f<p ? f/p : (f-p)/q):  A x<p: x/p   B p<=x<=.5: (x-p)/q
 //                        C x>cthr: (1-x)/p   D .5<x<=cthr: ((1-x)-p)/q
-// The predicates and the numerator are exact; the quotient is
-// fma(num, RN(1/d), corr) with corr ~= num*(1/d - RN(1/d)) formed from the
-// folded value by one FMA with selected constants (f*yl_p for A/C,
-// (f-p)*yl_q for B/D).  Static schedule: 44 cycles per iteration
-// (tools/iter_cycles.py; the other formulations tried scored 49-57).
+// The case predicates and every numerator are exact; each quotient is
+// fma(num, RN(1/d), corr) with corr ~= num*(1/d - RN(1/d)) formed from x by
+// one FMA, and one select tree picks the case.  The chain is
+// DADD -> DADD -> DFMA -> FSEL (case D).  Static schedule: 42 cycles per
+// iteration (tools/iter_cycles.py; other formulations tried scored 44-57,
+// tools/chain_search.py).
 __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
-  const bool c1 = x > 0.5;
-  const bool low = (x < c.p) | (x > c.cthr);  // == (f < p), exactly
-  const double t1 = __dsub_rn(1.0, x);         // exact when x > 0.5
+  const bool a = x < c.p, cc = x > c.cthr, fold = x > 0.5;
+  const double t1 = __dsub_rn(1.0, x);  // exact when x > 0.5
   const double nb = __dsub_rn(x, c.p);
   const double nd = __dsub_rn(t1, c.p);
-  const double f = c1 ? t1 : x;
-  const double g = low ? c.yl_p : c.yl_q;
-  const double a = low ? 0.0 : c.a_b;
-  const double corr = __fma_rn(f, g, a);
-  const double num = low ? f : (c1 ? nd : nb);
-  const double yh = low ? c.yh_p : c.yh_q;
-  return __fma_rn(num, yh, corr);
+  const double ya = __fma_rn(x, c.yh_p, __dmul_rn(x, c.yl_p));
+  const double yb = __fma_rn(nb, c.yh_q, __fma_rn(x, c.yl_q, c.a_b));
+  const double yc = __fma_rn(t1, c.yh_p, __fma_rn(-x, c.yl_p, c.yl_p));
+  const double yd = __fma_rn(nd, c.yh_q, __fma_rn(-x, c.yl_q, c.a_d));
+  return fold ? (cc ? yc : yd) : (a ? ya : yb);
 }
 
 // Is y exactly the reference's next orbit value after x?  The common path is

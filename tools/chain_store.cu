@@ -20,6 +20,18 @@ __device__ __forceinline__ double step(double x, const LaneConst& c) {
   const double yh = low ? c.yh_p : c.yh_q;
   return __fma_rn(num, yh, corr);
 }
+__device__ __forceinline__ double step4(double x, const LaneConst& c) {
+  const bool pA = x < c.p, pC = x > c.cthr, c1 = x > 0.5;
+  const double t1 = __dsub_rn(1.0, x);
+  const double nb = __dsub_rn(x, c.p);
+  const double nd = __dsub_rn(t1, c.p);
+  const double yA = __fma_rn(x, c.yh_p, __dmul_rn(x, c.yl_p));
+  const double yB = __fma_rn(nb, c.yh_q, __fma_rn(x, c.yl_q, c.a_b));
+  const double yC = __fma_rn(t1, c.yh_p, __fma_rn(-x, c.yl_p, c.yl_p));
+  const double yD = __fma_rn(nd, c.yh_q, __fma_rn(-x, c.yl_q, c.a_d));
+  return c1 ? (pC ? yC : yD) : (pA ? yA : yB);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) k(double* state, const LaneConst* lcs, double* orbit, uint32_t iters, uint32_t nl) {
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
@@ -46,6 +58,13 @@ __global__ void __launch_bounds__(128, 1) k(double* state, const LaneConst* lcs,
       for (int t = 0; t < 8; ++t) { x = step(x, c); v[t] = x; }
 #pragma unroll
       for (int t = 0; t < 8; t += 2) *reinterpret_cast<double2*>(o + t) = make_double2(v[t], v[t + 1]);
+      o += size_t(8) * nl;
+    }
+  } else if (MODE == 4) {  // 4-quotient formulation, STG.64 per step
+    double* o = orbit + l;
+    for (uint32_t i = 0; i < iters; i += 8) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { x = step4(x, c); o[size_t(t) * nl] = x; }
       o += size_t(8) * nl;
     }
   } else {  // 8 steps buffered then 8 STG.64 (iteration-major)
@@ -80,9 +99,9 @@ int main() {
   cudaMalloc(&dl, T * sizeof(LaneConst)); cudaMalloc(&dx, T * 8); cudaMalloc(&dorb, size_t(iters) * T * 8);
   cudaMemcpy(dl, h.data(), T * sizeof(LaneConst), cudaMemcpyHostToDevice);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  void (*ks[])(double*, const LaneConst*, double*, uint32_t, uint32_t) = {k<0>, k<1>, k<2>, k<3>};
-  const char* names[] = {"no stores", "STG.64 per step", "4x STG.128 per 8 (lane-major)", "8x STG.64 per 8 buffered"};
-  for (int m = 0; m < 4; ++m) {
+  void (*ks[])(double*, const LaneConst*, double*, uint32_t, uint32_t) = {k<0>, k<1>, k<2>, k<3>, k<4>};
+  const char* names[] = {"no stores", "STG.64 per step", "4x STG.128 per 8 (lane-major)", "8x STG.64 per 8 buffered", "4-quotient step, STG.64"};
+  for (int m = 0; m < 5; ++m) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemcpy(dx, x0.data(), T * 8, cudaMemcpyHostToDevice);
       cudaEventRecord(a);
