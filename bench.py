@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines")
     ap.add_argument("--clips", type=int, default=16,
                     help="independent clips for the labelled multi-clip line (0: skip)")
     return ap.parse_args()
@@ -314,6 +315,47 @@ def run_b200(args) -> None:
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e_value = frames_all / e2e_s
 
+    # ---- labelled decrypt line: the same clip decrypted (fresh handle) ----
+    dec = cve.Cipher(key, n, synth.ROUNDS)
+    for _ in range(args.warmup):
+        dec.decrypt_frames_device(dev.data_ptr(), side, F, stream.cuda_stream)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        dec.decrypt_frames_device(dev.data_ptr(), side, F, stream.cuda_stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dec_ms = dist.max(ev0.elapsed_time(ev1))
+    decrypt_line = {"value": args.steps * F * dist.world / (dec_ms / 1e3), "unit": "frames/s",
+                    "note": "labelled: decryption of the same workload, device-resident"}
+    del dec
+
+    # ---- per-config lines (value only, device-resident, short clips) ----
+    per_config = {}
+    if not args.no_configs:
+        for cname in ("C1", "C2", "C3", "C4", "C5"):
+            cc = synth.CONFIGS[cname]
+            cside = synth.config_side(cname)
+            # one frame of keystream run-ahead precedes the timed region, so
+            # a clip of N frames reads ~N/(N-1) high: N >= 24 keeps that <= 4 %
+            nfr = {"C1": 64, "C2": 48, "C3": 48, "C4": 24, "C5": 24}[cname]
+            buf = torch.from_numpy(np.stack([synth.config_frame(cname, 2 + t) for t in range(2)]))
+            buf = buf.repeat(nfr // 2, 1, 1, 1).contiguous().cuda()
+            hh = cve.Cipher(synth.det_key(cc["key_seed"] + 1000 * dist.rank), cc["workers"],
+                            synth.ROUNDS)
+            hh.encrypt_frames_device(buf.data_ptr(), cside, 2, stream.cuda_stream)  # warm-up
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            hh.encrypt_frames_device(buf.data_ptr(), cside, nfr, stream.cuda_stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            cms = dist.max(ev0.elapsed_time(ev1))
+            per_config[cname] = {"side": cside, "workers": cc["workers"], "frames": nfr,
+                                 "value": nfr * dist.world / (cms / 1e3), "unit": "frames/s",
+                                 "ms_per_frame": cms / nfr,
+                                 "note": "includes one run-ahead frame: reads <= N/(N-1) high"}
+            del hh, buf
+
     # ---- labelled multi-clip line: M independent clips (keys) on this GPU ----
     multi = None
     if args.clips > 0:
@@ -403,6 +445,8 @@ def run_b200(args) -> None:
                    "frac_of_hbm_2F": (cipher_gbs / hbm) if cipher_gbs else None},
         "guard_replays": st1["guard_replays"],
         "multi_clip": multi,
+        "decrypt": decrypt_line,
+        "configs": per_config,
         "clocks": clk.summary(),
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
