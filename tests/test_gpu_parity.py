@@ -237,3 +237,51 @@ def test_stats_and_launch_accounting():
     assert s["keystream_iters"] * 6 >= 5 * 480 * 480 * 3 // 8
     assert s["kernel_launches"] >= 1 + 5 + s["prbg_launches"]
     assert s["prbg_ms"] > 0 and s["cipher_ms"] > 0
+
+
+@pytest.mark.parametrize("side,n,r", [(1, 1, 5), (2, 1, 3), (2, 2, 5), (3, 3, 1), (3, 1, 255),
+                                      (5, 5, 7), (1536, 1, 1)])
+def test_degenerate_and_extreme_geometries_vs_oracle(side, n, r):
+    # 1-pixel frames (region = 3 bytes), one row per band, 255 rounds, and a
+    # single 1536-row band (generic multi-kernel path)
+    key = synth.det_key(side * 7 + n + r)
+    frames = rand_frames(side, 2, side * 13 + r)
+    o, c = Oracle(key, n, r), cve.Cipher(key, n, r)
+    for f in frames:
+        a, b = f.copy(), f.copy()
+        assert o.encrypt(a) == 0
+        c.encrypt_frame(b)
+        assert np.array_equal(a, b)
+    d = cve.Cipher(key, n, r)
+    ct = frames.copy()
+    cve.Cipher(key, n, r).encrypt_frames(ct)
+    d.decrypt_frames(ct)
+    assert np.array_equal(ct, frames)
+
+
+def test_concurrent_handles_from_threads():
+    # cve.h:5-6: distinct handles are independent; one thread per handle
+    import threading
+    shapes = [(96, 8), (120, 4), (64, 16), (90, 3)]
+    results = {}
+
+    def run(k, side, n):
+        key = synth.det_key(900 + k)
+        frames = rand_frames(side, 6, k)
+        ct = frames.copy()
+        c = cve.Cipher(key, n, 5)
+        for t in range(len(ct)):
+            c.encrypt_frame(ct[t])
+        results[k] = (key, n, frames, ct)
+
+    ths = [threading.Thread(target=run, args=(k, s, n)) for k, (s, n) in enumerate(shapes)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for k, (key, n, frames, ct) in results.items():
+        o = Oracle(key, n, 5)
+        for f, g in zip(frames, ct):
+            a = f.copy()
+            assert o.encrypt(a) == 0
+            assert np.array_equal(a, g), k
