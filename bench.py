@@ -209,8 +209,9 @@ def config_dict(name: str, frames: int, world: int) -> dict:
 
 def run_reference(args) -> None:
     dist = Dist(use_cuda=False)
-    if dist.rank != 0:
-        dist.close()
+    rank = dist.rank
+    dist.close()  # no collectives: the reference arm runs on rank 0 only
+    if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _oracle import Reference
