@@ -97,10 +97,12 @@ __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
   return fold ? (cc ? yc : yd) : (a ? ya : yb);
 }
 
-// Is y exactly the reference's next orbit value after x?  The common path is
-// one FMA residual test; values whose low word is 0 or p's (the guard set
-// {0, 0.5, 1, p}, powers of two) or that are tiny are decided exactly.
-__device__ __forceinline__ bool plcm_verify(double x, double y, const LaneConst& c) {
+// Is y exactly the reference's next orbit value after x?  Branch-free common
+// path: one FMA residual test.  Values whose low word is 0 or p's (the guard
+// set {0, 0.5, 1, p} and powers of two) or that are tiny only raise
+// `suspect`; the caller re-decides those exactly with plcm_verify_exact.
+__device__ __forceinline__ bool plcm_verify_fast(double x, double y, const LaneConst& c,
+                                                 bool& suspect) {
   const double f = x > 0.5 ? __dsub_rn(1.0, x) : x;
   const bool low = f < c.p;
   const double num = low ? f : __dsub_rn(f, c.p);
@@ -114,10 +116,13 @@ __device__ __forceinline__ bool plcm_verify(double x, double y, const LaneConst&
   const double r = __fma_rn(-y, den, num);
   const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
   const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
-  bool ok = fabs(r) < thr;
-  if (lo == 0u || lo == c.plo || ex < (53u << 20))  // rare: decide exactly
-    ok = y == __ddiv_rn(num, den) && !(y == 0.0 || y == c.p || y == 0.5 || y == 1.0);
-  return ok;
+  suspect |= (lo == 0u) | (lo == c.plo) | (ex < (53u << 20));
+  return fabs(r) < thr;
+}
+
+// Exact decision: the reference step itself (IEEE division + guard).
+__device__ __noinline__ bool plcm_verify_exact(double x, double y, const LaneConst& c) {
+  return y == plcm_exact(x, c.p, c.q);
 }
 
 __global__ void __launch_bounds__(128)
@@ -185,23 +190,31 @@ __global__ void __launch_bounds__(256)
   const LaneConst c = lcs[l];
   const size_t i0 = size_t(g) * 8;
   double x;
-  bool ok = true;
+  bool cont = true;  // continuity with the previous launch (group 0 only)
   if (g) {
     x = orbit[(i0 - 1) * nlanes + l];
   } else {
     x = ckpt[l];
-    ok = x == verified_end[l];
+    cont = x == verified_end[l];
   }
+  double y[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) y[t] = __ldg(orbit + (i0 + t) * nlanes + l);  // all in flight
+  bool suspect = false;
+  bool ok = plcm_verify_fast(x, y[0], c, suspect);
+#pragma unroll
+  for (int t = 1; t < 8; ++t) ok &= plcm_verify_fast(y[t - 1], y[t], c, suspect);
+  if (suspect) {  // rare: decide this group exactly
+    ok = true;
+    for (int t = 0; t < 8; ++t) ok &= plcm_verify_exact(t ? y[t - 1] : x, y[t], c);
+  }
+  if (!(ok && cont) && live) atomicOr(bad + (l >> 1), 1u);
   uint32_t lo[8], hi[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
-    const double y = orbit[(i0 + t) * nlanes + l];
-    ok &= plcm_verify(x, y, c);
-    x = y;
-    lo[t] = unsigned(__double2loint(y));
-    hi[t] = unsigned(__double2hiint(y));
+    lo[t] = unsigned(__double2loint(y[t]));
+    hi[t] = unsigned(__double2hiint(y[t]));
   }
-  if (!ok && live) atomicOr(bad + (l >> 1), 1u);
   const uint32_t odd = l & 1u;
   uint32_t mlo[4], mhi[4];
 #pragma unroll
