@@ -38,8 +38,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# Each cipher handle drives 5 CUDA streams; with the default 8 hardware work
-# queues, independent handles would falsely serialise (multi-clip line).
+# Each cipher handle drives 2 CUDA streams (4 with the host API); with the
+# default 8 hardware work queues, independent handles would falsely serialise
+# (multi-clip line).
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np  # noqa: E402

@@ -101,12 +101,14 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   configure_kernels_once(dev_);
 
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&s_ver_, cudaStreamNonBlocking), "stream");
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-  ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
   ck(cudaStreamCreateWithFlags(&s_work_, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+  // Verification shares s_work: every frame's rounds wait for their
+  // keystream's verify anyway, and a device-API handle then occupies two
+  // hardware queues, so 16 concurrent handles fit CUDA_DEVICE_MAX_CONNECTIONS
+  // = 32 without sharing a queue with another handle's long chain launches.
+  s_ver_ = s_work_;
 
   const uint32_t nl = 2 * n_;
   std::vector<LaneConst> lc(nl);
@@ -127,7 +129,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamSynchronize(s);
   for (auto& c : consumers_) ev_put(c.done);
   for (auto e : ver_done_) if (e) cudaEventDestroy(e);
@@ -147,7 +149,7 @@ Engine::~Engine() {
   cudaFree(ring_);
   free_prbg(pb_);
   cudaFree(d_lc_);
-  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
 }
 
@@ -429,6 +431,10 @@ void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool d
       !io.in_w || !io.in_h || !io.out_w || !io.out_h)
     raise(Errc::invalid_argument, "frame region exceeds the padded side");
   const Geom g = geometry(side);
+  if (!s_h2d_) {  // copy streams only for handles that use the host API
+    ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+  }
   ensure_ring(uint64_t(r_) * g.region);
   ensure_buffers(g, kSlots);
   const uint64_t row = uint64_t(side) * 3;
@@ -489,8 +495,8 @@ void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
 }
 
 void Engine::synchronize() {
-  for (cudaStream_t s : {s_gen_, s_ver_, s_h2d_, s_work_, s_d2h_})
-    ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+    if (s) ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
 }
 
 void Engine::peek(uint32_t worker, uint8_t* out, size_t len) {

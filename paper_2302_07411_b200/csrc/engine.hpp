@@ -112,6 +112,7 @@ class Engine {
   int dev_;
   Coordinator coord_;
 
+  // s_ver_ aliases s_work_; s_h2d_/s_d2h_ are created on first host-API use.
   cudaStream_t s_gen_ = nullptr, s_ver_ = nullptr, s_h2d_ = nullptr,
                s_work_ = nullptr, s_d2h_ = nullptr;
   cudaEvent_t chain_done_[2] = {nullptr, nullptr};
