@@ -353,6 +353,302 @@ __global__ void __launch_bounds__(kEncThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K2s: the forward round for side % 16 == 0 with 16-byte aligned frames and
+// keystream.  Same work split as K2 (one CTA per chunk of cr <= 16
+// destination rows al0 .. al0+cr-1, the h chunks of a band in one cluster):
+//
+//  1. Staging.  Source row sr holds the chunk's pixels at columns
+//     o0 .. o0+cr-1, o0 = (al0 - sr) mod side -- one contiguous run of 3*cr
+//     bytes (pixel k belongs to destination row al0 + k).  The runs' aligned
+//     64-byte windows are copied global -> shared with cp.async (four threads
+//     per row, so a warp covers 8 rows per instruction), 512 rows per stage,
+//     double-buffered.  Each stage is then repacked by thread = row: the
+//     window is realigned in registers and pixel k is stored as one 32-bit
+//     slot at k*side + (o0 + c_k) mod side, c_k = (k + shift[al0+k]) mod side
+//     (consecutive rows -> consecutive columns: no bank conflicts).  Runs
+//     that wrap past the row end (cr - 1 rows per chunk) are read pixel by
+//     pixel from global.
+//  2. Scan.  One 48-byte granule (16 slots -> 12 packed words) per thread per
+//     super-tile, 32-bit SWAR diffusion, the next super-tile's keystream in
+//     flight during the current one; one CTA-wide XOR scan per super-tile.
+//  3. Band prefix across the cluster (DSMEM), 4. 16-byte stores.
+//
+// Slot layout: granule u = slots [16u, 16u+16); its 4-slot quarter c lives
+// at quarter c ^ ((u >> 1) & 3), so the 8 granules a quarter-warp reads with
+// one LDS.128 cover all 32 banks.  Window layout: row r's 16-byte chunk c at
+// chunk c ^ ((r >> 1) & 3) of its 64-byte slot, same reason.
+constexpr uint32_t kSlotThreads = 512;
+constexpr uint32_t kMaxChunkRows = 16;
+constexpr uint32_t kStageRows = kSlotThreads;  // rows per staging stage
+constexpr uint32_t kWinBytes = 64;
+constexpr uint32_t kStageBytes = kStageRows * kWinBytes;
+constexpr size_t kSlotSmemMax = 224 * 1024;
+
+__device__ __forceinline__ uint32_t slot_word(uint32_t s) {
+  return s ^ ((s >> 3) & 12u);  // quarter bits (2,3) ^= granule bits (5,6)
+}
+
+// t = b ^ ((y + b) mod 256) per byte, then the inclusive XOR prefix across the
+// word's bytes (little-endian order).
+__device__ __forceinline__ uint32_t t_prefix4(uint32_t y, uint32_t b) {
+  uint32_t t = b ^ add_bytes(y, b);
+  t ^= t << 8;
+  t ^= t << 16;
+  return t;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kSlotThreads, 1)
+    k_encrypt_round_slots(const EncArgs a) {
+  extern __shared__ uint4 smem[];
+  __shared__ uint32_t cks[kMaxChunkRows];
+  __shared__ uint32_t wsum[64];
+  __shared__ uint32_t agg_in[16];  // aggregates of earlier chunks (cluster rank j)
+  __shared__ uint32_t agg_share;
+  __shared__ uint32_t prefix_share;
+
+  const uint32_t tid = threadIdx.x;
+  const uint32_t band = blockIdx.x / a.h;
+  const uint32_t chunk = blockIdx.x - band * a.h;
+  const uint32_t cr = a.chunk_rows, side = a.side;
+  const uint32_t al0 = band * a.rows + chunk * cr;
+  const uint32_t G = (cr * side) >> 4;  // 48-byte granules in the chunk
+  const uint32_t cb = cr * side * 3;
+  const uint32_t slots_base = uint32_t(__cvta_generic_to_shared(smem));
+  const uint32_t win_base = slots_base + cr * side * 4u;  // 2 stages of windows
+  const uint8_t* ks = a.ring + uint64_t(band) * a.ring_bytes;
+  uint64_t kbase = a.pos + uint64_t(chunk) * cb;
+  if (kbase >= a.ring_bytes) kbase -= a.ring_bytes;
+  auto load_ks = [&](uint32_t g, uint4 (&kv)[3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      kv[i] = make_uint4(0, 0, 0, 0);
+      if (g < G) {
+        uint64_t kp = kbase + 48ull * g + 16 * i;
+        if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+        kv[i] = ld_stream(ks + kp);
+      }
+    }
+  };
+  // source run of row sr: first column and byte offset
+  auto run_of = [&](uint32_t sr, uint32_t& o0, uint32_t& b0) {
+    int o = int(al0) - int(sr);
+    o += o < 0 ? int(side) : 0;
+    o0 = uint32_t(o);
+    b0 = (sr * side + o0) * 3u;
+  };
+  const uint32_t nstages = (side + kStageRows - 1) / kStageRows;
+  // Thread tid copies chunk (tid & 3) of rows (tid >> 2) + 128 i of a stage.
+  // b0(sr) = 3 (sr (side - 1) + al0) (+ 3 side once sr > al0).
+  const uint32_t cpc = tid & 3u, cpr = tid >> 2;
+  const uint32_t cp_dst = win_base + cpr * kWinBytes + 16u * (cpc ^ ((cpr >> 1) & 3u));
+  auto issue_stage = [&](uint32_t st) {
+    const uint32_t dst0 = cp_dst + (st & 1u) * kStageBytes;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t sr = st * kStageRows + cpr + 128u * i;
+      const uint32_t b0 = 3u * (sr * (side - 1) + al0) + (sr > al0 ? 3u * side : 0u);
+      const bool need = sr < side && 16u * cpc < (b0 & 15u) + 3u * cr;
+      cp_async16(dst0 + 128u * kWinBytes * i, a.src + (b0 & ~15u) + 16u * cpc, need);
+    }
+    cp_async_commit();
+  };
+
+  // cluster phase 1 (arrive now, wait before the DSMEM stores): every CTA of
+  // the cluster has started before any remote store lands in it
+  if (a.h > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  issue_stage(0);
+  if (nstages > 1) issue_stage(1);
+  uint4 kv[3];
+  load_ks(tid, kv);  // first super-tile's keystream
+  for (uint32_t t = tid; t < cr; t += kSlotThreads) {
+    uint32_t c = t + uint32_t(a.shift[al0 + t]);
+    cks[t] = c >= side ? c - side : c;
+  }
+  if (tid == 0) prefix_share = seed_byte(a, band);
+  __syncthreads();
+
+  // 1. Staging.
+  {
+    uint32_t dk[kMaxChunkRows], ek[kMaxChunkRows];
+#pragma unroll
+    for (int k = 0; k < int(kMaxChunkRows); ++k) {
+      const uint32_t c = uint32_t(k) < cr ? cks[k] : 0u;
+      dk[k] = uint32_t(k) * side + c;
+      ek[k] = side - c;  // o0 >= ek  <=>  o0 + c_k >= side
+    }
+    auto put = [&](int k, uint32_t o0, uint32_t pix) {
+      const uint32_t sl = dk[k] + o0 - (o0 >= ek[k] ? side : 0u);
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots_base + 4u * slot_word(sl)), "r"(pix));
+    };
+    for (uint32_t st = 0; st < nstages; ++st) {
+      if (st + 1 < nstages)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncthreads();
+      const uint32_t sr = st * kStageRows + tid;
+      if (sr < side) {
+        uint32_t o0, b0;
+        run_of(sr, o0, b0);
+        if (o0 + cr <= side) {
+          const uint32_t w = win_base + (st & 1u) * kStageBytes + tid * kWinBytes;
+          const uint32_t sw = (tid >> 1) & 3u;
+          uint32_t V[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
+                         : "r"(w + 16u * (uint32_t(c) ^ sw)));
+          const uint32_t ws = (b0 >> 2) & 3u, bs = (b0 & 3u) * 8u;
+          uint32_t X[14], U[13], A[12];
+#pragma unroll
+          for (int i = 0; i < 14; ++i) X[i] = (ws & 2u) ? V[i + 2] : V[i];
+#pragma unroll
+          for (int i = 0; i < 13; ++i) U[i] = (ws & 1u) ? X[i + 1] : X[i];
+#pragma unroll
+          for (int i = 0; i < 12; ++i) A[i] = __funnelshift_r(U[i], U[i + 1], bs);
+#pragma unroll
+          for (int k = 0; k < int(kMaxChunkRows); ++k) {
+            if (uint32_t(k) >= cr) break;
+            const int j = (3 * k) >> 2, sh = ((3 * k) & 3) * 8;
+            put(k, o0, sh <= 8 ? (A[j] >> sh) : __funnelshift_r(A[j], A[j + 1], sh));
+          }
+        } else {  // run wraps past the row end
+#pragma unroll
+          for (int k0 = 0; k0 < int(kMaxChunkRows); k0 += 4) {
+            uint32_t pix[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t o = o0 + uint32_t(k0 + j);
+              o -= o >= side ? side : 0u;
+              const uint8_t* sp = a.src + (uint64_t(sr) * side + o) * 3;
+              pix[j] = 0;
+              if (uint32_t(k0 + j) < cr)
+                pix[j] = uint32_t(__ldg(sp)) | (uint32_t(__ldg(sp + 1)) << 8) |
+                         (uint32_t(__ldg(sp + 2)) << 16);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (uint32_t(k0 + j) < cr) put(k0 + j, o0, pix[j]);
+          }
+        }
+      }
+      if (st + 2 < nstages) {
+        __syncthreads();  // every thread is done with this stage's windows
+        issue_stage(st + 2);
+      }
+    }
+  }
+  __syncthreads();
+
+  // 2. Chunk XOR scan, one granule per thread per super-tile.
+  uint32_t carry = 0, excl_last = 0;
+  uint32_t res[12];
+  const uint32_t ntiles = (G + kSlotThreads - 1) / kSlotThreads;
+  for (uint32_t st = 0; st < ntiles; ++st) {
+    const uint32_t g = st * kSlotThreads + tid;
+    uint4 kn[3];
+    if (st + 1 < ntiles) load_ks(g + kSlotThreads, kn);
+    uint32_t y[12];
+    const uint32_t sw = (g >> 1) & 3u;
+    if (g < G) {
+      const uint4* q = smem + 4 * g;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 s = q[c ^ sw];  // 4 slots (3 bytes each) -> 3 packed words
+        y[3 * c] = __byte_perm(s.x, s.y, 0x4210);
+        y[3 * c + 1] = __byte_perm(s.y, s.z, 0x5421);
+        y[3 * c + 2] = __byte_perm(s.z, s.w, 0x6542);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 12; ++i) y[i] = 0;
+    }
+    const uint32_t kw[12] = {kv[0].x, kv[0].y, kv[0].z, kv[0].w, kv[1].x, kv[1].y,
+                             kv[1].z, kv[1].w, kv[2].x, kv[2].y, kv[2].z, kv[2].w};
+    uint32_t E = 0;  // XOR of every earlier t byte, broadcast to 4 bytes
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const uint32_t t = t_prefix4(y[i], kw[i]);
+      res[i] = t ^ E;
+      E ^= __byte_perm(t, 0, 0x3333);
+    }
+    uint32_t total;
+    const uint32_t excl = block_xor_scan(E & 0xFFu, wsum, st, total) ^ carry;
+    if (ntiles > 1) {  // park the results in the granule's own slots
+      if (g < G) {
+        const uint32_t m = excl * 0x01010101u;
+        uint4* q = smem + 4 * g;
+        q[0 ^ sw] = make_uint4(res[0] ^ m, res[1] ^ m, res[2] ^ m, res[3] ^ m);
+        q[1 ^ sw] = make_uint4(res[4] ^ m, res[5] ^ m, res[6] ^ m, res[7] ^ m);
+        q[2 ^ sw] = make_uint4(res[8] ^ m, res[9] ^ m, res[10] ^ m, res[11] ^ m);
+      }
+    } else {
+      excl_last = excl;
+    }
+    carry ^= total;
+    if (st + 1 < ntiles) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) kv[i] = kn[i];
+    }
+  }
+
+  // 3. Band prefix: s_d ^ aggregates of the chunks before this one.  Each
+  //    CTA pushes its aggregate into the later CTAs' agg_in[] (DSMEM stores),
+  //    then one release/acquire cluster barrier.
+  if (a.h > 1) {
+    const uint32_t me = blockIdx.x - band * a.h;  // == cluster rank
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (tid > me && tid < a.h) {
+      const uint32_t local = uint32_t(__cvta_generic_to_shared(&agg_in[me]));
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(tid));
+      asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(carry) : "memory");
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (tid == 0) {
+      uint32_t p = prefix_share;
+      for (uint32_t j = 0; j < me; ++j) p ^= agg_in[j];
+      prefix_share = p;
+    }
+  }
+  __syncthreads();
+
+  // 4. Output (16-byte stores, consecutive threads on consecutive pieces).
+  uint4* out4 = reinterpret_cast<uint4*>(a.dst + uint64_t(band) * a.region +
+                                         uint64_t(chunk) * cb);
+  if (ntiles == 1) {
+    if (tid < G) {
+      const uint32_t m = (prefix_share ^ excl_last) * 0x01010101u;
+      out4[3 * tid] = make_uint4(res[0] ^ m, res[1] ^ m, res[2] ^ m, res[3] ^ m);
+      out4[3 * tid + 1] = make_uint4(res[4] ^ m, res[5] ^ m, res[6] ^ m, res[7] ^ m);
+      out4[3 * tid + 2] = make_uint4(res[8] ^ m, res[9] ^ m, res[10] ^ m, res[11] ^ m);
+    }
+  } else {
+    const uint32_t m = prefix_share * 0x01010101u;
+    for (uint32_t q = tid; q < 3 * G; q += kSlotThreads) {
+      const uint32_t g = q / 3, c = q - 3 * g;
+      const uint4 v = smem[4 * g + (c ^ ((g >> 1) & 3u))];
+      out4[q] = make_uint4(v.x ^ m, v.y ^ m, v.z ^ m, v.w ^ m);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: fused inverse round.  One CTA per tile of T output rows; for every
 // cipher row al it gathers the contiguous run of T pixels that lands in the
 // tile, inverse-diffuses them elementwise, and writes the tile back with
@@ -554,6 +850,9 @@ void configure_cipher_kernels() {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
     cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
+  cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(kSlotSmemMax));
+  cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (auto k : {k_decrypt_round<true>, k_decrypt_round<false>})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
 }
@@ -562,6 +861,31 @@ void launch_shift_table(const double* sine, uint32_t seed, int32_t* shift,
                         uint32_t side, cudaStream_t s) {
   k_shift<<<(side + 255) / 256, 256, 0, s>>>(sine, seed, shift, side);
   check_launch("shift_table");
+}
+
+// Slot-staged plan: chunk rows cr | rows, cr <= 16, h = rows / cr <= 16 (one
+// cluster); shared memory = 4 B of slots per chunk pixel + 2 stages of source
+// windows.  Longer chunks mean longer contiguous source runs; take the
+// largest cr with >= 64 CTAs per frame.
+void plan_slots(const Geom& g, EncPlan& p) {
+  p.slots = false;
+  if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32)) return;
+  uint32_t forced = 0;
+  if (const char* e = std::getenv("CVE_B200_ENC_CR")) forced = uint32_t(std::atoi(e));  // experiments only
+  bool enough = false;
+  for (uint32_t cr = 1; cr <= std::min(g.rows, kMaxChunkRows); ++cr) {
+    if (g.rows % cr || g.rows / cr > 16) continue;
+    const size_t smem = size_t(cr) * g.side * 4 + 2 * kStageBytes;
+    if (smem > kSlotSmemMax) continue;
+    if (forced && cr != forced) continue;
+    const bool ok = uint64_t(g.n) * (g.rows / cr) >= 64;
+    if (!ok && enough) continue;
+    enough = enough || ok;
+    p.slots = true;
+    p.s_rows = cr;
+    p.s_h = g.rows / cr;
+    p.s_smem = smem;
+  }
 }
 
 EncPlan plan_encrypt(const Geom& g) {
@@ -574,32 +898,60 @@ EncPlan plan_encrypt(const Geom& g) {
   auto make = [&](uint32_t h) {
     const uint64_t cb = uint64_t(g.rows / h) * row_bytes;
     const size_t smem = size_t(((cb + 15) & ~uint64_t(15)) + 4 * (g.rows / h));
-    return EncPlan{smem <= kSmemBudget, g.rows / h, h, smem};
+    return EncPlan{smem <= kSmemBudget, g.rows / h, h, smem, false, 0, 0, 0};
   };
+  EncPlan out{false, 0, 0, 0, false, 0, 0, 0};
+  bool done = false;
   if (const char* e = std::getenv("CVE_B200_ENC_H")) {  // experiments only
     const uint32_t h = uint32_t(std::atoi(e));
-    if (h >= 1 && h <= 16 && g.rows % h == 0 && make(h).fused) return make(h);
+    if (h >= 1 && h <= 16 && g.rows % h == 0 && make(h).fused) {
+      out = make(h);
+      done = true;
+    }
   }
-  EncPlan fallback{false, 0, 0, 0};
-  for (uint32_t h = 1; h <= 16; ++h) {
+  for (uint32_t h = 1; h <= 16 && !done; ++h) {
     if (g.rows % h) continue;
     const EncPlan p = make(h);
     if (!p.fused) continue;
-    if (p.smem <= 120 * 1024 && uint64_t(g.n) * h >= 64) return p;
-    fallback = p;  // largest feasible h so far
+    out = p;  // largest feasible h so far
+    if (p.smem <= 120 * 1024 && uint64_t(g.n) * h >= 64) done = true;
   }
-  return fallback;
+  if (!std::getenv("CVE_B200_NO_SLOTS")) plan_slots(g, out);  // experiments only
+  return out;
 }
 
 void launch_encrypt_round(const EncPlan& plan, const Geom& g,
                           const uint8_t* src, uint8_t* dst, KsWindow ks,
                           const int32_t* shift, uint8_t* scratch,
                           cudaStream_t s, uint64_t* launches) {
+  const bool aligned = (g.side % 16 == 0) && (ks.pos % 16 == 0) &&
+                       (ks.ring_bytes % 16 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                         reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
+  if (plan.slots && aligned) {
+    EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
+              g.rows, plan.s_rows, plan.s_h, g.region, make_div(plan.s_rows)};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.n * plan.s_h);
+    cfg.blockDim = dim3(kSlotThreads);
+    cfg.dynamicSmemBytes = plan.s_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = plan.s_h;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_encrypt_round_slots, a);
+    check_launch("encrypt_round_slots");
+    ++*launches;
+    return;
+  }
   if (plan.fused) {
     EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
               g.rows, plan.chunk_rows, plan.h, g.region, make_div(plan.chunk_rows)};
-    const bool vec = (g.side % 16 == 0) && (ks.pos % 16 == 0) &&
-                     (ks.ring_bytes % 16 == 0);
+    const bool vec = aligned;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.n * plan.h);
     cfg.blockDim = dim3(kEncThreads);

@@ -23,7 +23,11 @@ uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
 constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
 
-PrbgBuffers alloc_prbg(uint32_t nlanes) {
+// Every upload / memset below is ordered on the stream that consumes it: the
+// synchronous cudaMemcpy / cudaMemset run on the legacy default stream, which
+// does not order against our non-blocking streams (a pageable H2D cudaMemcpy
+// may even return before its DMA lands).
+PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s) {
   PrbgBuffers b{};
   uint64_t iters = kOrbitBytes / (8ull * nlanes);
   iters = std::min<uint64_t>(iters, 1u << 20) / 8 * 8;
@@ -37,8 +41,8 @@ PrbgBuffers alloc_prbg(uint32_t nlanes) {
   }
   ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
   ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
-  ck(cudaMemset(b.bad, 0, (nlanes / 2) * sizeof(unsigned)), "memset");
-  ck(cudaMemset(b.replays, 0, sizeof(unsigned long long)), "memset");
+  ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
+  ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
   return b;
 }
 
@@ -60,7 +64,8 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
                uint32_t nlanes, cudaStream_t s) {
   double* d_x0 = nullptr;
   ck(cudaMalloc(&d_x0, nlanes * sizeof(double)), "cudaMalloc x0");
-  ck(cudaMemcpy(d_x0, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice), "upload x0");
+  ck(cudaMemcpyAsync(d_x0, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice, s),
+     "upload x0");
   launch_prbg_init(b.state, d_lc, d_x0, nlanes, s);
   ck(cudaGetLastError(), "prbg_init launch");
   ck(cudaMemcpyAsync(b.verified_end, b.state, nlanes * sizeof(double),
@@ -119,10 +124,10 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     x0[2 * i] = lanes[i].a.x0;
     x0[2 * i + 1] = lanes[i].b.x0;
   }
-  pb_ = alloc_prbg(nl);
+  pb_ = alloc_prbg(nl, s_gen_);
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-  ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice),
-     "upload lanes");
+  ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice,
+                     s_gen_), "upload lanes");
   init_prbg(pb_, d_lc_, x0.data(), nl, s_gen_);
   ++st_.kernel_launches;
 }
@@ -311,7 +316,8 @@ const double* Engine::sine_for(uint32_t side) {
   const std::vector<double> s = sine_table(side);
   double* d = nullptr;
   ck(cudaMalloc(&d, sizeof(double) * side), "cudaMalloc sine");
-  ck(cudaMemcpy(d, s.data(), sizeof(double) * side, cudaMemcpyHostToDevice),
+  // ordered before k_shift, which runs on s_work
+  ck(cudaMemcpyAsync(d, s.data(), sizeof(double) * side, cudaMemcpyHostToDevice, s_work_),
      "upload sine");
   sines_[side] = d;
   return d;
@@ -561,10 +567,10 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     configure_kernels_once(dev);
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    pb = alloc_prbg(2);
+    pb = alloc_prbg(2, s);
     ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
     ck(cudaMalloc(&d_out, ring), "cudaMalloc");
-    ck(cudaMemcpy(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemcpyAsync(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice, s), "upload");
     init_prbg(pb, d_lc, x0, 2, s);
     int slot = 0;
     for (uint64_t it = 0; it < iters; it += pb.max_iters, slot ^= 1) {
@@ -596,9 +602,10 @@ KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, int devi
     x0[2 * i + 1] = lanes[i].b.x0;
   }
   ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
-  pb_ = alloc_prbg(nl);
+  pb_ = alloc_prbg(nl, s_);
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-  ck(cudaMemcpy(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice, s_),
+     "upload");
   init_prbg(pb_, d_lc_, x0.data(), nl, s_);
   ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
 }

@@ -87,6 +87,11 @@ struct EncPlan {
   bool fused;
   uint32_t chunk_rows, h;  // h chunks (one cluster) per band
   size_t smem;
+  // slot-staged variant (side % 16 == 0); used when the launch's frames and
+  // keystream window are 16-byte aligned, else the byte-staged one above
+  bool slots;
+  uint32_t s_rows, s_h;
+  size_t s_smem;
 };
 EncPlan plan_encrypt(const Geom& g);
 void launch_encrypt_round(const EncPlan& plan, const Geom& g,

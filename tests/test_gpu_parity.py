@@ -285,3 +285,36 @@ def test_concurrent_handles_from_threads():
             a = f.copy()
             assert o.encrypt(a) == 0
             assert np.array_equal(a, g), k
+
+
+def test_concurrent_handles_stress():
+    # Many handles created and driven at once from threads (setup uploads,
+    # first frames and the keystream generator all contending): every frame
+    # must still match the oracle.  Guards the stream ordering of the
+    # per-handle uploads (lane constants, x0, sine table, flags).
+    import threading
+    shapes = [(96, 8), (120, 4), (64, 16), (90, 3), (128, 8), (48, 4), (160, 16), (72, 6)]
+    for rep in range(3):
+        results = {}
+
+        def run(k, side, n):
+            key = synth.det_key(950 + 10 * rep + k)
+            frames = rand_frames(side, 4, 100 * rep + k)
+            ct = frames.copy()
+            c = cve.Cipher(key, n, 3)
+            for t in range(len(ct)):
+                c.encrypt_frame(ct[t])
+            results[k] = (key, n, frames, ct)
+
+        ths = [threading.Thread(target=run, args=(k, s, n)) for k, (s, n) in enumerate(shapes)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        assert len(results) == len(shapes)
+        for k, (key, n, frames, ct) in results.items():
+            o = Oracle(key, n, 3)
+            for f, g in zip(frames, ct):
+                a = f.copy()
+                assert o.encrypt(a) == 0
+                assert np.array_equal(a, g), (rep, k)

@@ -11,17 +11,23 @@ for name in sys.argv[1:] or ["C1", "C3", "C4", "C5"]:
     c = synth.CONFIGS[name]; n = c["workers"]; side = synth.config_side(name)
     F = side * side * 3
     need = 5 * (side // n) * side * 3
-    frames = torch.from_numpy(np.stack([synth.config_frame(name, t) for t in range(3)])).cuda()
+    NF = 12 if side <= 1920 else 6
+    frames = torch.from_numpy(np.stack([synth.config_frame(name, t % 3) for t in range(NF)])).cuda()
     out = {}
     for mode in ("enc", "dec"):
-        h = cve.Cipher(synth.config_key(name), n, 5)
-        h.prefetch_keystream(3 * need); h.synchronize()
-        s0 = h.stats()
-        fn = h.encrypt_frames_device if mode == "enc" else h.decrypt_frames_device
-        fn(frames.data_ptr(), side, 3, torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        s1 = h.stats()
-        out[mode] = (s1["cipher_ms"] - s0["cipher_ms"]) / 3
+        best = None
+        for rep in range(3):  # best of 3: the keystream is generated first, so
+            h = cve.Cipher(synth.config_key(name), n, 5)  # only cipher time counts
+            h.prefetch_keystream(NF * need); h.synchronize()
+            s0 = h.stats()
+            fn = h.encrypt_frames_device if mode == "enc" else h.decrypt_frames_device
+            fn(frames.data_ptr(), side, NF, torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            s1 = h.stats()
+            v = (s1["cipher_ms"] - s0["cipher_ms"]) / NF
+            best = v if best is None else min(best, v)
+            del h
+        out[mode] = best
     print(f"{name}: side={side} n={n}  encrypt {out['enc']*1e3:.1f} us/frame "
           f"({2*F/out['enc']/1e6:.0f} GB/s of 2F, {15*F/out['enc']/1e6:.0f} GB/s moved)  "
           f"decrypt {out['dec']*1e3:.1f} us/frame")
