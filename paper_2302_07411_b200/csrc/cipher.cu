@@ -431,16 +431,14 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
   const uint8_t* ks = a.ring + uint64_t(band) * a.ring_bytes;
   uint64_t kbase = a.pos + uint64_t(chunk) * cb;
   if (kbase >= a.ring_bytes) kbase -= a.ring_bytes;
+  // kbase and ring_bytes are multiples of 48 (launch condition): a granule
+  // never straddles the ring end
   auto load_ks = [&](uint32_t g, uint4 (&kv)[3]) {
+    uint64_t kp = kbase + 48ull * g;
+    if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    const uint8_t* p = ks + kp;
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      kv[i] = make_uint4(0, 0, 0, 0);
-      if (g < G) {
-        uint64_t kp = kbase + 48ull * g + 16 * i;
-        if (kp >= a.ring_bytes) kp -= a.ring_bytes;
-        kv[i] = ld_stream(ks + kp);
-      }
-    }
+    for (int i = 0; i < 3; ++i) kv[i] = g < G ? ld_stream(p + 16 * i) : make_uint4(0, 0, 0, 0);
   };
   // source run of row sr: first column and byte offset
   auto run_of = [&](uint32_t sr, uint32_t& o0, uint32_t& b0) {
@@ -526,30 +524,31 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
             const int j = (3 * k) >> 2, sh = ((3 * k) & 3) * 8;
             put(k, o0, sh <= 8 ? (A[j] >> sh) : __funnelshift_r(A[j], A[j + 1], sh));
           }
-        } else {  // run wraps past the row end
-#pragma unroll
-          for (int k0 = 0; k0 < int(kMaxChunkRows); k0 += 4) {
-            uint32_t pix[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t o = o0 + uint32_t(k0 + j);
-              o -= o >= side ? side : 0u;
-              const uint8_t* sp = a.src + (uint64_t(sr) * side + o) * 3;
-              pix[j] = 0;
-              if (uint32_t(k0 + j) < cr)
-                pix[j] = uint32_t(__ldg(sp)) | (uint32_t(__ldg(sp + 1)) << 8) |
-                         (uint32_t(__ldg(sp + 2)) << 16);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (uint32_t(k0 + j) < cr) put(k0 + j, o0, pix[j]);
-          }
-        }
+        }  // runs that wrap past the row end: deferred, below
       }
       if (st + 2 < nstages) {
         __syncthreads();  // every thread is done with this stage's windows
         issue_stage(st + 2);
       }
+    }
+    // The cr - 1 source rows whose run wraps past the row end are rows
+    // al0 + i (i = 1 .. cr-1, o0 = side - i): one thread per pixel, every
+    // load in flight at once.
+    const uint32_t nwrap = min(cr, side) - 1;
+    for (uint32_t it = tid; it < nwrap * cr; it += kSlotThreads) {
+      const uint32_t i = it / cr + 1, k = it - (i - 1) * cr;
+      uint32_t sr = al0 + i;
+      sr -= sr >= side ? side : 0u;
+      const uint32_t o0 = side - i;
+      uint32_t o = o0 + k;
+      o -= o >= side ? side : 0u;
+      const uint8_t* sp = a.src + (uint64_t(sr) * side + o) * 3;
+      const uint32_t pix = uint32_t(__ldg(sp)) | (uint32_t(__ldg(sp + 1)) << 8) |
+                           (uint32_t(__ldg(sp + 2)) << 16);
+      uint32_t be = o0 + cks[k];
+      be -= be >= side ? side : 0u;
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots_base + 4u * slot_word(k * side + be)),
+                   "r"(pix));
     }
   }
   __syncthreads();
@@ -736,6 +735,259 @@ __global__ void __launch_bounds__(kDecThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K3s: the inverse round for side % 16 == 0 (16-byte aligned frames and
+// keystream).  One CTA per tile of T destination rows a0 .. a0+tv-1 (no
+// cluster: the inverse diffusion is elementwise).  Source (cipher) row al
+// holds the tile's pixels at columns be_lo .. be_lo+tv-1,
+// be_lo = (al - a0 - tv + 1 + shift[al]) mod side -- one contiguous run; its
+// keystream bytes are one contiguous run of the band's stream too.  Per
+// stage of 256 source rows both 64-byte windows are copied with cp.async
+// (8 threads per row), then thread = row realigns them, inverse-diffuses
+// d = ((b ^ c ^ c_prev) - b) four bytes at a time and stores pixel m as a
+// slot of destination row a0 + tv-1-m, column (al - a0 - tv+1 + m) mod side.
+// Band heads (which need the next band's recovered last byte) and runs that
+// wrap past the row end go byte by byte.  The tile's rows are contiguous in
+// the frame: output is packed 48-byte granules.
+constexpr uint32_t kDecStageRows = 256;
+constexpr uint32_t kDecWin = 128;  // 64 B cipher window + 64 B keystream window
+constexpr uint32_t kDecStageBytes = kDecStageRows * kDecWin;
+constexpr uint32_t kDecDefer = 256;
+
+// bytewise (x - y) mod 256
+__device__ __forceinline__ uint32_t sub_bytes(uint32_t x, uint32_t y) {
+  return ((x | 0x80808080u) - (y & 0x7F7F7F7Fu)) ^ ((x ^ ~y) & 0x80808080u);
+}
+
+// 12 words starting `off` (0..15) bytes into a 16-word window
+__device__ __forceinline__ void realign12(const uint32_t (&V)[16], uint32_t off,
+                                          uint32_t (&A)[12]) {
+  const uint32_t ws = off >> 2, bs = (off & 3u) * 8u;
+  uint32_t X[14], U[13];
+#pragma unroll
+  for (int i = 0; i < 14; ++i) X[i] = (ws & 2u) ? V[i + 2] : V[i];
+#pragma unroll
+  for (int i = 0; i < 13; ++i) U[i] = (ws & 1u) ? X[i + 1] : X[i];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) A[i] = __funnelshift_r(U[i], U[i + 1], bs);
+}
+
+__global__ void __launch_bounds__(kSlotThreads, 1)
+    k_decrypt_round_slots(const DecArgs a) {
+  extern __shared__ uint4 smem[];
+  const uint32_t tid = threadIdx.x, side = a.side, T = a.T;
+  const uint32_t a0 = blockIdx.x * T;
+  const uint32_t tv = min(T, side - a0);
+  const uint32_t slots_base = uint32_t(__cvta_generic_to_shared(smem));
+  int32_t* sht = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(smem) + T * side * 4u);
+  // per-row run info of 3 stages (P0, keystream position, band | fast<<31)
+  uint4* rinfo = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + T * side * 4u +
+                                          side * 4u);
+  const uint32_t win_base = slots_base + T * side * 4u + side * 4u + 3u * kDecStageRows * 16u;
+  const uint32_t region = uint32_t(a.region);
+
+  __shared__ uint32_t dlist[kDecDefer];  // rows deferred to the per-pixel pass
+  __shared__ uint32_t dcount;
+  for (uint32_t i = tid; i < side; i += kSlotThreads) sht[i] = a.shift[i];
+  if (tid == 0) dcount = 0;
+  __syncthreads();
+
+  struct Run {
+    uint32_t band, be_lo, P0;
+    uint64_t kp0;
+    bool fast;
+  };
+  auto run_of = [&](uint32_t al) {
+    Run r;
+    r.band = fdiv(al, a.div_rows);
+    int b = int(al) - int(a0) - int(tv) + 1 + sht[al];  // in (-side, 2 side)
+    b += b < 0 ? int(side) : 0;
+    b -= b >= int(side) ? int(side) : 0;
+    r.be_lo = uint32_t(b);
+    r.P0 = (al * side + r.be_lo) * 3u;
+    uint64_t kp = a.pos + (r.P0 - r.band * region);
+    if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    r.kp0 = kp;
+    const bool head = (al - r.band * a.rows) == 0 && r.be_lo == 0;
+    r.fast = r.be_lo + tv <= side && !head;
+    return r;
+  };
+  const uint32_t nstages = (side + kDecStageRows - 1) / kDecStageRows;
+  auto fill_info = [&](uint32_t st, uint32_t r) {  // r < kDecStageRows
+    const uint32_t al = st * kDecStageRows + r;
+    uint4 e = make_uint4(0, 0, 0, 0);
+    if (al < side) {
+      const Run q = run_of(al);
+      e = make_uint4(q.P0, uint32_t(q.kp0), uint32_t(q.kp0 >> 32),
+                     q.band | (q.fast ? 0x80000000u : 0u));
+    }
+    rinfo[(st % 3u) * kDecStageRows + r] = e;
+  };
+  const uint32_t cps = tid & 7u, cpr = tid >> 3;  // chunk, row (+64 i) of a stage
+  auto issue_stage = [&](uint32_t st) {
+    const uint32_t dst0 = win_base + (st & 1u) * kDecStageBytes;
+    const uint4* info = rinfo + (st % 3u) * kDecStageRows;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t r = cpr + 64u * i;
+      const uint4 e = info[r];
+      const uint32_t dst = dst0 + r * kDecWin + 16u * (cps ^ (r & 7u));
+      bool need = false;
+      const uint8_t* src = a.src;
+      if (e.w >> 31) {  // fast run (implies a row inside the frame)
+        if (cps < 4) {
+          const uint32_t base = (e.x - 1) & ~15u;  // fast runs have P0 >= 1
+          need = base + 16u * cps < e.x + 3u * tv;
+          if (need) src = a.src + base + 16u * cps;
+        } else {
+          const uint32_t c = cps - 4;
+          const uint64_t kp0 = (uint64_t(e.z) << 32) | e.y;
+          uint64_t kp = (kp0 & ~uint64_t(15)) + 16u * c;
+          if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+          need = 16u * c < (e.y & 15u) + 3u * tv;
+          if (need) src = a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes + kp;
+        }
+      }
+      cp_async16(dst, src, need);
+    }
+    cp_async_commit();
+  };
+  if (tid < kDecStageRows)
+    fill_info(0, tid);
+  else if (nstages > 1)
+    fill_info(1, tid - kDecStageRows);
+  __syncthreads();
+  issue_stage(0);
+  if (nstages > 1) issue_stage(1);
+
+  auto put = [&](uint32_t m, uint32_t q0, uint32_t pix) {
+    uint32_t o = q0 + m;
+    o -= o >= side ? side : 0u;
+    const uint32_t sl = (tv - 1u - m) * side + o;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots_base + 4u * slot_word(sl)), "r"(pix));
+  };
+  auto ks_at = [&](uint32_t band, uint32_t j) {  // keystream byte j of the round
+    uint64_t kp = a.pos + j;
+    if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    return uint32_t(__ldg(a.ring + uint64_t(band) * a.ring_bytes + kp));
+  };
+  // pixel m of source row al's run, byte by byte from global
+  auto slow_pixel = [&](uint32_t al, const Run& q, uint32_t m) {
+    const uint32_t nb = q.band + 1 == a.n ? 0 : q.band + 1;
+    uint32_t be = q.be_lo + m;
+    be -= be >= side ? side : 0u;
+    const uint32_t P = (al * side + be) * 3u;
+    uint32_t pix = 0;
+#pragma unroll
+    for (uint32_t ch = 0; ch < 3; ++ch) {
+      const uint32_t j = P + ch - q.band * region;
+      const uint32_t b = ks_at(q.band, j);
+      uint32_t prev;
+      if (j == 0) {  // band head: the next band's recovered last byte
+        const uint32_t L = (nb + 1) * region - 1;
+        const uint32_t bl = ks_at(nb, region - 1);
+        prev = (bl ^ __ldg(a.src + L) ^ __ldg(a.src + L - 1)) - bl;
+      } else {
+        prev = __ldg(a.src + P + ch - 1);
+      }
+      pix |= (((b ^ __ldg(a.src + P + ch) ^ prev) - b) & 0xFFu) << (8 * ch);
+    }
+    return pix;
+  };
+
+  for (uint32_t st = 0; st < nstages; ++st) {
+    if (st + 1 < nstages)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
+    __syncthreads();
+    const uint32_t al = st * kDecStageRows + tid;
+    if (tid >= kDecStageRows) {  // idle during the repack: run info two stages ahead
+      if (st + 2 < nstages) fill_info(st + 2, tid - kDecStageRows);
+    } else if (al < side) {
+      const uint4 e = rinfo[(st % 3u) * kDecStageRows + tid];
+      int q0i = int(al) - int(a0) - int(tv) + 1;  // in (-side, side)
+      q0i += q0i < 0 ? int(side) : 0;
+      const uint32_t q0 = uint32_t(q0i);
+      if (e.w >> 31) {
+        struct {
+          uint32_t P0;
+          uint64_t kp0;
+        } q{e.x, (uint64_t(e.z) << 32) | e.y};
+        const uint32_t w = win_base + (st & 1u) * kDecStageBytes + tid * kDecWin;
+        uint32_t V[16], R[12], K[12];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
+                       : "r"(w + 16u * (uint32_t(c) ^ (tid & 7u))));
+        realign12(V, (q.P0 - 1) & 15u, R);  // R byte 0 = c[P0-1], then c[P0..]
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
+                       : "r"(w + 16u * (uint32_t(c + 4) ^ (tid & 7u))));
+        realign12(V, uint32_t(q.kp0 & 15u), K);
+        uint32_t D[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const uint32_t cur = i < 11 ? __funnelshift_r(R[i], R[i + 1], 8) : (R[11] >> 8);
+          D[i] = sub_bytes(K[i] ^ cur ^ R[i], K[i]);
+        }
+#pragma unroll
+        for (int m = 0; m < int(kMaxChunkRows); ++m) {
+          if (uint32_t(m) >= tv) break;
+          const int j = (3 * m) >> 2, sh = ((3 * m) & 3) * 8;
+          put(m, q0, sh <= 8 ? (D[j] >> sh) : __funnelshift_r(D[j], D[j + 1], sh));
+        }
+      } else {  // band head or wrapping run: deferred (inline if the list is full)
+        const uint32_t i = atomicAdd(&dcount, 1u);
+        if (i < kDecDefer) {
+          dlist[i] = al;
+        } else {
+          const Run q = run_of(al);
+          for (uint32_t m = 0; m < tv; ++m) put(m, q0, slow_pixel(al, q, m));
+        }
+      }
+    }
+    if (st + 2 < nstages) {
+      __syncthreads();
+      issue_stage(st + 2);
+    }
+  }
+  __syncthreads();
+  {  // deferred rows: one thread per pixel
+    const uint32_t nd = min(dcount, kDecDefer);
+    for (uint32_t it = tid; it < nd * tv; it += kSlotThreads) {
+      const uint32_t al = dlist[it / tv], m = it % tv;
+      const Run q = run_of(al);
+      int q0i = int(al) - int(a0) - int(tv) + 1;
+      q0i += q0i < 0 ? int(side) : 0;
+      put(m, uint32_t(q0i), slow_pixel(al, q, m));
+    }
+  }
+  __syncthreads();
+
+  // Output: the tile = rows a0 .. a0+tv-1, contiguous in the frame.
+  const uint32_t G = (tv * side) >> 4;
+  uint4* out4 = reinterpret_cast<uint4*>(a.dst + uint64_t(a0) * side * 3);
+  for (uint32_t g = tid; g < G; g += kSlotThreads) {
+    const uint4* q = smem + 4 * g;
+    const uint32_t sw = (g >> 1) & 3u;
+    uint32_t y[12];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = q[c ^ sw];
+      y[3 * c] = __byte_perm(v.x, v.y, 0x4210);
+      y[3 * c + 1] = __byte_perm(v.y, v.z, 0x5421);
+      y[3 * c + 2] = __byte_perm(v.z, v.w, 0x6542);
+    }
+    out4[3 * g] = make_uint4(y[0], y[1], y[2], y[3]);
+    out4[3 * g + 1] = make_uint4(y[4], y[5], y[6], y[7]);
+    out4[3 * g + 2] = make_uint4(y[8], y[9], y[10], y[11]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic forward round for geometries whose band chunks do not fit one
 // cluster's shared memory: gather -> chunk aggregates -> band prefixes ->
 // chunk scans, through global scratch.
@@ -853,6 +1105,8 @@ void configure_cipher_kernels() {
   cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(kSlotSmemMax));
   cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_decrypt_round_slots, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(kSlotSmemMax));
   for (auto k : {k_decrypt_round<true>, k_decrypt_round<false>})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
 }
@@ -928,7 +1182,7 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
                        (ks.ring_bytes % 16 == 0) &&
                        ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
                          reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
-  if (plan.slots && aligned) {
+  if (plan.slots && aligned && ks.pos % 48 == 0 && ks.ring_bytes % 48 == 0) {
     EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
               g.rows, plan.s_rows, plan.s_h, g.region, make_div(plan.s_rows)};
     cudaLaunchConfig_t cfg = {};
@@ -986,20 +1240,60 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
   *launches += 4;
 }
 
+// Slot-staged inverse round: tile rows T in [6, 15] (<= side) minimising the
+// destination rows per SM, ceil(ceil(side / T) / SMs) * T (ties: larger T),
+// with T*side*4 (slots) + side*4 (shift table) + 2 window stages of shared
+// memory.
+uint32_t plan_decrypt_slots(const Geom& g, size_t& smem) {
+  if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32) || std::getenv("CVE_B200_NO_SLOTS"))
+    return 0;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint32_t best = 0;
+  uint64_t best_load = ~uint64_t(0);
+  for (uint32_t T = std::min<uint32_t>(6, g.side); T <= std::min<uint32_t>(kMaxChunkRows - 1, g.side); ++T) {
+    const size_t need = size_t(T) * g.side * 4 + size_t(g.side) * 4 +
+                        3 * kDecStageRows * 16 + 2 * kDecStageBytes;
+    if (need > kSlotSmemMax) continue;
+    const uint64_t ctas = (g.side + T - 1) / T;
+    const uint64_t load = (ctas + uint64_t(sms) - 1) / uint64_t(sms) * T;
+    if (load <= best_load) {
+      best_load = load;
+      best = T;
+      smem = need;
+    }
+  }
+  return best;
+}
+
 void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
                           KsWindow ks, const int32_t* shift, cudaStream_t s,
                           uint64_t* launches) {
+  const bool aligned = (g.side % 16 == 0) && (ks.pos % 16 == 0) && (ks.ring_bytes % 16 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                         reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
+  size_t smem = 0;
+  const uint32_t Ts = aligned ? plan_decrypt_slots(g, smem) : 0;
+  if (Ts) {
+    DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
+              Ts, g.region, make_div(Ts), make_div(g.rows)};
+    k_decrypt_round_slots<<<(g.side + Ts - 1) / Ts, kSlotThreads, smem, s>>>(a);
+    check_launch("decrypt_round_slots");
+    ++*launches;
+    return;
+  }
   const uint64_t row_bytes = uint64_t(g.side) * 3;
   uint32_t T = uint32_t(std::max<uint64_t>(1, (96 * 1024) / row_bytes));
   const uint32_t want = std::max<uint32_t>(8, (g.side + 147) / 148);
   T = std::min(T, want);
   T = std::min(T, g.side);
-  const size_t smem = ((uint64_t(T) * row_bytes + 15) & ~uint64_t(15));
+  smem = ((uint64_t(T) * row_bytes + 15) & ~uint64_t(15));
   if (smem > kSmemBudget) throw Error(Errc::invalid_argument, "frame side too large");
   DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
             T, g.region, make_div(T), make_div(g.rows)};
   const uint32_t grid = (g.side + T - 1) / T;
-  if (g.side % 16 == 0)
+  if (aligned)
     k_decrypt_round<true><<<grid, kDecThreads, smem, s>>>(a);
   else
     k_decrypt_round<false><<<grid, kDecThreads, smem, s>>>(a);

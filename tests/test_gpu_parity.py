@@ -141,7 +141,11 @@ def test_device_resident_api_matches_host_api():
 @pytest.mark.parametrize("side,n,r", [
     (8, 2, 3), (16, 4, 1), (24, 4, 5), (30, 3, 5), (7, 7, 5), (97, 1, 2),
     (100, 4, 5), (192, 12, 5), (256, 128, 5), (64, 64, 5), (1000, 1, 2),
-    (600, 1, 5), (480, 8, 1), (484, 4, 4)])
+    (600, 1, 5), (480, 8, 1), (484, 4, 4),
+    # side % 16 == 0: slot-staged rounds (K2s/K3s), odd cluster sizes and
+    # partial decrypt tiles
+    (32, 2, 3), (48, 3, 5), (112, 7, 2), (144, 9, 5), (176, 11, 3), (320, 20, 2),
+    (208, 4, 5), (400, 25, 1)])
 def test_random_shapes_vs_oracle(side, n, r):
     key = synth.det_key(side * 131 + n * 7 + r)
     frames = rand_frames(side, 3, side + n)
