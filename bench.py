@@ -435,13 +435,15 @@ def run_b200(args) -> None:
             "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
             "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
             "cycles_per_iteration": ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3,
-            "static_schedule_cycles": 44,
-            "frac_of_static_schedule": 44 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
+            # ptxas stall counts of the unrolled loop (tools/iter_cycles.py on
+            # build/csrc/prbg.o): 7 x 42 + 47 (back-edge) per 8 iterations
+            "static_schedule_cycles": 42.625,
+            "frac_of_static_schedule": 42.625 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
             "launches": int(len(chain_times)),
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,
             "verify_emit_fixup_ms": prbg_ms - chain_ms},
-        "cipher": {"kernel": "k_encrypt_round x5 + k_shift per frame",
+        "cipher": {"kernel": "k_encrypt_round_slots x5 + k_shift per frame",
                    "ms_per_frame": cipher_ms / frames_timed,
                    "achieved_gbs_2F": cipher_gbs,
                    "frac_of_hbm_2F": (cipher_gbs / hbm) if cipher_gbs else None},

@@ -104,6 +104,10 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
                               prop.name);
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   configure_kernels_once(dev_);
+  if (const char* e = std::getenv("CVE_B200_GEN_CHUNK")) {  // experiments only; 0 = unset
+    const uint64_t v = std::strtoull(e, nullptr, 10) / 8 * 8;
+    if (v) gen_chunk_cap_ = v;
+  }
 
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -332,7 +336,8 @@ void Engine::gen_until(uint64_t end_byte) {
   target = std::min(target, cap);
   while (gen_iters_ < target) {
     uint64_t chunk = target - gen_iters_;
-    const uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+    uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+    if (gen_chunk_cap_) max_chunk = std::min(max_chunk, gen_chunk_cap_);
     chunk = std::min<uint64_t>({chunk, max_chunk, pb_.max_iters});
     const int slot = int(launches_ & 1);
     // (1) chain on s_gen, once the verifier is done with this slot's buffers

@@ -118,6 +118,7 @@ class Engine {
   cudaEvent_t chain_done_[2] = {nullptr, nullptr};
   cudaEvent_t ver_done_[2] = {nullptr, nullptr};
   uint64_t launches_ = 0;  // generator launches (slot = launches_ & 1)
+  uint64_t gen_chunk_cap_ = 0;  // optional cap on iterations per generator launch
   PrbgBuffers pb_{};
   LaneConst* d_lc_ = nullptr;
 

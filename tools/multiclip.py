@@ -22,11 +22,13 @@ for M in [int(a) for a in sys.argv[1:]] or [1, 4, 16, 32, 64]:
     for _ in range(steps):
         for h, b, s in zip(hs, bufs, streams):
             h.encrypt_frames_device(b.data_ptr(), side, F, s.cuda_stream)
+    host = time.perf_counter() - t0
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     fps = M * F * steps / el
     st = [h.stats() for h in hs]
     print(f"M={M:3d}: {fps:8.1f} frames/s aggregate ({fps/M:6.1f} per clip), "
-          f"cipher {np.mean([s['cipher_ms'] for s in st])/(F*(steps+1)):.3f} ms/frame", flush=True)
+          f"cipher {np.mean([s['cipher_ms'] for s in st])/(F*(steps+1)):.3f} ms/frame, "
+          f"host enqueue {host/el*100:.0f}% of wall ({host/(M*F*steps)*1e6:.0f} us/frame)", flush=True)
     del hs, bufs
     torch.cuda.empty_cache()
