@@ -141,7 +141,58 @@ CVE_B200_API cve_status cve_nist_export(const char* key_hex, uint32_t workers,
                                         uint64_t byte_count,
                                         const char* out_path);
 
+/* ---- reference statistical analysis and image tools */
+
+/* Same layout as the reference (cve.h:117-125). */
+typedef struct cve_analyze_options {
+  const char* input;   /* P6 or CVE1 */
+  const char* second;  /* optional same-size image for NPCR/UACI */
+  uint32_t frame_index;  /* frame to take from a container */
+  uint32_t second_frame_index;
+  uint32_t samples;    /* adjacent-pair samples per direction, 0 -> 20000 */
+  uint64_t seed;       /* sampling seed */
+  int csv;             /* nonzero -> CSV, else key=value report */
+} cve_analyze_options;
+
+/* replaces cve.h:127-128.  Per-channel histogram variance, chi^2 (+ the
+ * 5 % uniformity verdict), entropy, local entropy over 30 disjoint 44x44
+ * blocks, horizontal / vertical / diagonal adjacent-pixel correlation over
+ * `samples` random pairs, and NPCR/UACI against `second` -- the same text,
+ * byte for byte, as the reference.  The histograms and NPCR/UACI counts are
+ * taken on the GPU.  *text_out is malloc'd: free with cve_string_free. */
+CVE_B200_API cve_status cve_analyze(const cve_analyze_options* options, char** text_out);
+
+/* replaces cve.h:132-134.  Salt-and-pepper noise over round(rate * side^2)
+ * distinct pixels of every frame (seed + frame index); P6 or CVE1 in, same
+ * format out, byte-identical to the reference. */
+CVE_B200_API cve_status cve_add_noise_file(const char* in_path, const char* out_path,
+                                           double rate, uint64_t seed);
+
+/* Same layout as the reference (cve.h:136-141). */
+typedef struct cve_crop_block {
+  uint32_t x;     /* column of the upper-left corner */
+  uint32_t y;     /* row of the upper-left corner */
+  uint32_t side;
+  uint8_t fill;   /* 0x00 or 0xFF */
+} cve_crop_block;
+
+/* replaces cve.h:143-145.  Square blocks filled with 0x00 / 0xFF in every
+ * frame; byte-identical to the reference. */
+CVE_B200_API cve_status cve_crop_file(const char* in_path, const char* out_path,
+                                      const cve_crop_block* blocks, size_t block_count);
+
 /* ---- additive: batched / device-resident / introspection ---------------- */
+
+/* Additive (row f4 on resident frames): the analysis reductions of a
+ * side x side RGB24 frame already in device memory, ordered on `stream`
+ * (a cudaStream_t; NULL = legacy default stream), without copying the frame.
+ * hist_out (device, 768 x u64): hist_out[c*256 + v] = pixels of channel c
+ * with value v.  With `second` (device frame of the same side) and diff_out
+ * (device, 6 x u64): diff_out[c] = positions where channel c differs,
+ * diff_out[3 + c] = sum of |a - b| over channel c (NPCR/UACI numerators). */
+CVE_B200_API cve_status cve_frame_stats_device(const uint8_t* frame, const uint8_t* second,
+                                               uint32_t side, uint64_t* hist_out,
+                                               uint64_t* diff_out, void* stream);
 
 /* The reference's padded_side (frame.cpp:19-26): smallest multiple of
  * `workers` covering max(width, height). */

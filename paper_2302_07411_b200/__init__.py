@@ -54,6 +54,18 @@ class IoOptions(C.Structure):
                 ("fps", C.c_uint16), ("raw_width", C.c_uint32), ("raw_height", C.c_uint32)]
 
 
+class AnalyzeOptions(C.Structure):
+    """cve_analyze_options (reference cve.h:117-125)."""
+    _fields_ = [("input", C.c_char_p), ("second", C.c_char_p), ("frame_index", C.c_uint32),
+                ("second_frame_index", C.c_uint32), ("samples", C.c_uint32),
+                ("seed", C.c_uint64), ("csv", C.c_int)]
+
+
+class CropBlock(C.Structure):
+    """cve_crop_block (reference cve.h:136-141)."""
+    _fields_ = [("x", C.c_uint32), ("y", C.c_uint32), ("side", C.c_uint32), ("fill", C.c_uint8)]
+
+
 class Stats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("keystream_iters", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("prbg_launches", C.c_uint64),
@@ -96,6 +108,10 @@ def _load() -> C.CDLL:
         "cve_decrypt_file": (C.c_int, [C.c_char_p, C.POINTER(IoOptions), C.c_int, C.c_char_p,
                                        C.c_char_p]),
         "cve_nist_export": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint64, C.c_char_p]),
+        "cve_analyze": (C.c_int, [C.POINTER(AnalyzeOptions), C.POINTER(vp)]),
+        "cve_add_noise_file": (C.c_int, [C.c_char_p, C.c_char_p, C.c_double, C.c_uint64]),
+        "cve_crop_file": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(CropBlock), C.c_size_t]),
+        "cve_frame_stats_device": (C.c_int, [vp, vp, C.c_uint32, vp, vp, vp]),
         "cve_padded_side": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]),
         "cve_cipher_encrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]),
         "cve_cipher_decrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -192,6 +208,42 @@ def nist_export(key_hex, workers: int, byte_count: int, out_path: str) -> None:
 
 
 # ---- frame model (reference frame.cpp:19-51) --------------------------------
+
+def analyze(input_path: str, second: str = None, frame_index: int = 0,
+            second_frame_index: int = 0, samples: int = 0, seed: int = 0,
+            csv: bool = False) -> str:
+    """Reference cve_analyze: histogram variance, chi^2, entropy, local
+    entropy, adjacent-pixel correlations, NPCR/UACI -- the same text.  The
+    histograms and NPCR/UACI counts run on the GPU."""
+    o = AnalyzeOptions(input_path.encode(), second.encode() if second else None, frame_index,
+                       second_frame_index, samples, seed, 1 if csv else 0)
+    out = C.c_void_p()
+    _check(lib.cve_analyze(C.byref(o), C.byref(out)))
+    try:
+        return C.string_at(out).decode()
+    finally:
+        lib.cve_string_free(out)
+
+
+def add_noise_file(in_path: str, out_path: str, rate: float, seed: int) -> None:
+    """Reference cve_add_noise_file (salt-and-pepper, every frame)."""
+    _check(lib.cve_add_noise_file(in_path.encode(), out_path.encode(), rate, seed))
+
+
+def crop_file(in_path: str, out_path: str, blocks) -> None:
+    """Reference cve_crop_file; blocks = [(x, y, side, fill), ...]."""
+    arr = (CropBlock * max(1, len(blocks)))(*[CropBlock(*b) for b in blocks])
+    _check(lib.cve_crop_file(in_path.encode(), out_path.encode(), arr if blocks else None,
+                             len(blocks)))
+
+
+def frame_stats_device(frame_ptr: int, side: int, hist_ptr: int, second_ptr: int = 0,
+                       diff_ptr: int = 0, stream: int = 0) -> None:
+    """Histograms (768 x u64 at hist_ptr) and NPCR/UACI counts (6 x u64 at
+    diff_ptr) of a device-resident frame, ordered on `stream`."""
+    _check(lib.cve_frame_stats_device(frame_ptr, second_ptr or None, side, hist_ptr or None,
+                                      diff_ptr or None, stream or None))
+
 
 def padded_side(width: int, height: int, workers: int) -> int:
     out = C.c_uint32()

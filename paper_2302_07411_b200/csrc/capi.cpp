@@ -11,8 +11,10 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/cve_b200.h"
+#include "analysis.hpp"
 #include "engine.hpp"
 #include "fileio.hpp"
 #include "files.hpp"
@@ -246,6 +248,66 @@ cve_status cve_nist_export(const char* key_hex, uint32_t workers,
     const int dev = current_device();
     DeviceScope scope(dev);
     cveb::keystream_export(key_hex, workers, byte_count, out_path, dev);
+  });
+}
+
+// capi.cpp:335-358: argument checks, then the frame(s), then the size match.
+cve_status cve_analyze(const cve_analyze_options* options, char** text_out) {
+  return guarded([&] {
+    require(options != nullptr, "options is null");
+    require(text_out != nullptr, "text_out is null");
+    require(options->input != nullptr, "input is null");
+    const uint32_t samples = options->samples != 0 ? options->samples : 20000;
+    const cveb::HostFrame frame = cveb::load_frame_any(options->input, options->frame_index);
+    cveb::HostFrame second;
+    if (options->second != nullptr) {
+      second = cveb::load_frame_any(options->second, options->second_frame_index);
+      if (second.side != frame.side) cveb::raise(cveb::Errc::mismatch, "images differ in size");
+    }
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    const std::string text = cveb::analyze(frame, options->second ? &second : nullptr, samples,
+                                           options->seed, options->csv != 0, dev);
+    char* out = static_cast<char*>(std::malloc(text.size() + 1));
+    if (out == nullptr) throw std::bad_alloc();
+    std::memcpy(out, text.c_str(), text.size() + 1);
+    *text_out = out;
+  });
+}
+
+cve_status cve_add_noise_file(const char* in_path, const char* out_path, double rate,
+                              uint64_t seed) {
+  return guarded([&] {
+    require(in_path != nullptr && out_path != nullptr, "path is null");
+    cveb::add_noise_file(in_path, out_path, rate, seed);
+  });
+}
+
+cve_status cve_crop_file(const char* in_path, const char* out_path, const cve_crop_block* blocks,
+                         size_t block_count) {
+  return guarded([&] {
+    require(in_path != nullptr && out_path != nullptr, "path is null");
+    require(block_count == 0 || blocks != nullptr, "blocks is null");
+    std::vector<cveb::CropBlock> list(block_count);
+    for (size_t i = 0; i < block_count; ++i)
+      list[i] = {blocks[i].x, blocks[i].y, blocks[i].side, blocks[i].fill};
+    cveb::crop_file(in_path, out_path, list);
+  });
+}
+
+cve_status cve_frame_stats_device(const uint8_t* frame, const uint8_t* second, uint32_t side,
+                                  uint64_t* hist_out, uint64_t* diff_out, void* stream) {
+  return guarded([&] {
+    require(frame != nullptr, "frame is null");
+    require(side != 0, "side must be >= 1");
+    require(hist_out != nullptr || (second != nullptr && diff_out != nullptr),
+            "nothing to compute");
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    cveb::launch_frame_stats(frame, second, uint64_t(side) * side * 3,
+                             reinterpret_cast<unsigned long long*>(hist_out),
+                             second ? reinterpret_cast<unsigned long long*>(diff_out) : nullptr,
+                             static_cast<cudaStream_t>(stream));
   });
 }
 

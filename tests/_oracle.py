@@ -163,3 +163,47 @@ def ref_encrypt_file(key_hex, in_path, out_path, workers=0, rounds=0, fps=0, raw
 def ref_decrypt_file(key_hex, in_path, out_path, fmt=0):
     return Reference.load().cve_decrypt_file(key_hex.encode(), None, fmt, in_path.encode(),
                                              out_path.encode())
+
+
+# ---- row f4: the reference's analysis and image tools ----------------------
+
+class RefAnalyzeOptions(C.Structure):
+    _fields_ = [("input", C.c_char_p), ("second", C.c_char_p), ("frame_index", C.c_uint32),
+                ("second_frame_index", C.c_uint32), ("samples", C.c_uint32),
+                ("seed", C.c_uint64), ("csv", C.c_int)]
+
+
+class RefCropBlock(C.Structure):
+    _fields_ = [("x", C.c_uint32), ("y", C.c_uint32), ("side", C.c_uint32), ("fill", C.c_uint8)]
+
+
+def ref_analyze(input_path, second=None, frame_index=0, second_frame_index=0, samples=0,
+                seed=0, csv=False):
+    """(status, text) from the reference's cve_analyze."""
+    L = Reference.load()
+    L.cve_analyze.argtypes = [C.POINTER(RefAnalyzeOptions), C.POINTER(C.c_void_p)]
+    L.cve_string_free.argtypes = [C.c_void_p]
+    o = RefAnalyzeOptions(input_path.encode() if input_path else None,
+                          second.encode() if second else None, frame_index,
+                          second_frame_index, samples, seed, 1 if csv else 0)
+    out = C.c_void_p()
+    st = L.cve_analyze(C.byref(o), C.byref(out))
+    if st:
+        return st, None
+    text = C.string_at(out).decode()
+    L.cve_string_free(out)
+    return 0, text
+
+
+def ref_add_noise_file(in_path, out_path, rate, seed):
+    L = Reference.load()
+    L.cve_add_noise_file.argtypes = [C.c_char_p, C.c_char_p, C.c_double, C.c_uint64]
+    return L.cve_add_noise_file(in_path.encode(), out_path.encode(), rate, seed)
+
+
+def ref_crop_file(in_path, out_path, blocks):
+    L = Reference.load()
+    L.cve_crop_file.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefCropBlock), C.c_size_t]
+    arr = (RefCropBlock * max(1, len(blocks)))(*[RefCropBlock(*b) for b in blocks])
+    return L.cve_crop_file(in_path.encode(), out_path.encode(), arr if blocks else None,
+                           len(blocks))
