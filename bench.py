@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines")
+    ap.add_argument("--no-rows", action="store_true",
+                    help="skip the row f1/f3/f4 measurements")
     ap.add_argument("--clips", type=int, default=16,
                     help="independent clips for the labelled multi-clip line (0: skip)")
     return ap.parse_args()
@@ -192,6 +194,132 @@ def cpu_baseline(name: str, seconds: float) -> dict:
             "sample": f"{frames} consecutive {name} frames ({synth.config_side(name)}^2, "
                       f"n={c['workers']}, r=5) in {el:.2f} s via cve_cipher_encrypt_frame, "
                       f"parallel=1 ({c['workers']} threads on {os.cpu_count()} host cpus)"}
+
+
+def rows_measure(stream) -> dict:
+    """SURVEY §8(f) rows next to the headline, each on the C4 geometry, this
+    engine vs the reference library (oracle/_ref, the CPU baseline legs of
+    these rows) on the same inputs:
+      f1  cve_encrypt_file / cve_decrypt_file, raw 1920x1080 clip <-> CVE1
+      f3  cve_nist_export, 64 workers
+      f4  cve_analyze of a 1920^2 frame with NPCR/UACI, and the device
+          reductions alone (cve_frame_stats_device) against HBM."""
+    import tempfile
+    import torch
+    import paper_2302_07411_b200 as cve
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import (Reference, ref_analyze, ref_decrypt_file,  # CPU baseline legs only
+                         ref_encrypt_file)
+    have_ref = Reference.available()
+    c = synth.CONFIGS["C4"]
+    W, H, n = c["width"], c["height"], c["workers"]
+    key = synth.config_key("C4")
+    nf = 24
+    rows = {}
+
+    def blob(p):
+        with open(p, "rb") as fh:
+            return fh.read()
+
+    with tempfile.TemporaryDirectory() as d:
+        raw = os.path.join(d, "clip.rgb")
+        pool = [synth.correlated_frame(W, H, t, 7000 + c["key_seed"]) for t in range(4)]
+        with open(raw, "wb") as fh:
+            for t in range(nf):
+                fh.write(pool[t % 4].tobytes())
+        ours, back = os.path.join(d, "ours.cve"), os.path.join(d, "ours.rgb")
+        t0 = time.perf_counter()
+        cve.encrypt_file(key, raw, ours, workers=n, rounds=synth.ROUNDS, raw=(W, H))
+        t_enc = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        cve.decrypt_file(key, ours, back, fmt=cve.CVE_OUT_RAW)
+        t_dec = time.perf_counter() - t0
+        f1 = {"workload": f"{nf}-frame raw {W}x{H} RGB24 file -> CVE1 (n={n}, r=5) and back, "
+                          "wall clock incl. file I/O (page cache)",
+              "encrypt_file": {"value": nf / t_enc, "unit": "frames/s"},
+              "decrypt_file": {"value": nf / t_dec, "unit": "frames/s"},
+              "round_trip": blob(back) == blob(raw)}
+        if have_ref:
+            refc, refb = os.path.join(d, "ref.cve"), os.path.join(d, "ref.rgb")
+            t0 = time.perf_counter()
+            assert ref_encrypt_file(key, raw, refc, workers=n, rounds=synth.ROUNDS,
+                                    raw=(W, H)) == 0
+            r_enc = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            assert ref_decrypt_file(key, refc, refb, fmt=2) == 0
+            r_dec = time.perf_counter() - t0
+            f1["reference"] = {"encrypt_file": nf / r_enc, "decrypt_file": nf / r_dec,
+                               "unit": "frames/s", "cores": os.cpu_count()}
+            f1["container_identical"] = blob(refc) == blob(ours)
+        rows["f1"] = f1
+
+        nbytes = 64 << 20
+        o3 = os.path.join(d, "ours.nist")
+        t0 = time.perf_counter()
+        cve.nist_export(key, n, nbytes, o3)
+        t3 = time.perf_counter() - t0
+        f3 = {"workload": f"{nbytes >> 20} MiB of generator bytes, {n} workers",
+              "value": nbytes / t3 / 1e6, "unit": "MB/s"}
+        if have_ref:
+            r3 = os.path.join(d, "ref.nist")
+            L = Reference.load()
+            t0 = time.perf_counter()
+            assert L.cve_nist_export(key.encode(), n, nbytes, r3.encode()) == 0
+            f3["reference"] = {"value": nbytes / (time.perf_counter() - t0) / 1e6,
+                               "unit": "MB/s", "cores": 1}
+            f3["identical"] = blob(r3) == blob(o3)
+        rows["f3"] = f3
+
+        side = synth.config_side("C4")
+        a_img, b_img = synth.config_frame("C4", 2), synth.config_frame("C4", 3)
+        pa, pb = os.path.join(d, "a.ppm"), os.path.join(d, "b.ppm")
+        for p_, img in ((pa, a_img), (pb, b_img)):
+            with open(p_, "wb") as fh:
+                fh.write(f"P6\n{side} {side}\n255\n".encode() + img.tobytes())
+        t0 = time.perf_counter()
+        txt = cve.analyze(pa, second=pb, seed=1)
+        t4 = time.perf_counter() - t0
+        f4 = {"workload": f"cve_analyze of a {side}^2 C4 frame with NPCR/UACI vs a second frame "
+                          "(P6 files), wall clock",
+              "analyze_ms": t4 * 1e3}
+        if have_ref:
+            t0 = time.perf_counter()
+            st, rtxt = ref_analyze(pa, second=pb, seed=1)
+            f4["reference_analyze_ms"] = (time.perf_counter() - t0) * 1e3
+            f4["identical_text"] = st == 0 and rtxt == txt
+        # device reductions alone: histograms (reads F) + NPCR/UACI (reads 2F),
+        # cycling over 8 frame pairs (177 MB, larger than L2)
+        pairs = 8
+        da = torch.from_numpy(np.stack([synth.config_frame("C4", 2 + t) for t in range(4)]))
+        da = da.repeat(pairs // 4, 1, 1, 1).contiguous().cuda()
+        db = torch.roll(da, 1, dims=0).contiguous()
+        fb = side * side * 3
+        hist = torch.zeros(768, dtype=torch.int64, device="cuda")
+        diff = torch.zeros(6, dtype=torch.int64, device="cuda")
+
+        def stats(i):
+            cve.frame_stats_device(da.data_ptr() + (i % pairs) * fb, side, hist.data_ptr(),
+                                   db.data_ptr() + (i % pairs) * fb, diff.data_ptr(),
+                                   stream.cuda_stream)
+        for i in range(pairs):
+            stats(i)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 48
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(reps):
+            stats(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        gbs = 2 * fb / (us * 1e-6) / 1e9
+        hbm, _ = peaks()
+        f4["device_stats"] = {"us_per_frame_pair": us, "achieved_gbs": gbs,
+                              "frac_of_hbm": gbs / hbm,
+                              "bytes": "2F per pair (one fused pass reads both frames once); "
+                                       "8 pairs cycled, 177 MB > L2"}
+        rows["f4"] = f4
+    return rows
 
 
 def config_dict(name: str, frames: int, world: int) -> dict:
@@ -453,6 +581,8 @@ def run_b200(args) -> None:
         "configs": per_config,
         "clocks": clk.summary(),
     }
+    if dist.rank == 0 and dist.world == 1 and not args.no_rows:
+        line["rows"] = rows_measure(stream)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, args.cpu_seconds)
     if dist.rank == 0:
