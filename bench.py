@@ -214,7 +214,7 @@ def rows_measure(stream) -> dict:
     c = synth.CONFIGS["C4"]
     W, H, n = c["width"], c["height"], c["workers"]
     key = synth.config_key("C4")
-    nf = 24
+    nf = 48
     rows = {}
 
     def blob(p):
@@ -228,14 +228,15 @@ def rows_measure(stream) -> dict:
             for t in range(nf):
                 fh.write(pool[t % 4].tobytes())
         ours, back = os.path.join(d, "ours.cve"), os.path.join(d, "ours.rgb")
-        t0 = time.perf_counter()
-        cve.encrypt_file(key, raw, ours, workers=n, rounds=synth.ROUNDS, raw=(W, H))
-        t_enc = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        cve.decrypt_file(key, ours, back, fmt=cve.CVE_OUT_RAW)
-        t_dec = time.perf_counter() - t0
+        for _ in range(2):  # the second call is timed: the first pays one-time
+            t0 = time.perf_counter()  # pinned-staging and engine setup
+            cve.encrypt_file(key, raw, ours, workers=n, rounds=synth.ROUNDS, raw=(W, H))
+            t_enc = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            cve.decrypt_file(key, ours, back, fmt=cve.CVE_OUT_RAW)
+            t_dec = time.perf_counter() - t0
         f1 = {"workload": f"{nf}-frame raw {W}x{H} RGB24 file -> CVE1 (n={n}, r=5) and back, "
-                          "wall clock incl. file I/O (page cache)",
+                          "wall clock incl. file I/O, second call of each",
               "encrypt_file": {"value": nf / t_enc, "unit": "frames/s"},
               "decrypt_file": {"value": nf / t_dec, "unit": "frames/s"},
               "round_trip": blob(back) == blob(raw)}

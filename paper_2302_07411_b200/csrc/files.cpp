@@ -4,13 +4,17 @@
 // reference's cve_encrypt_file / cve_decrypt_file (capi.cpp:143-164,
 // 262-333).  Differences: frames travel to the GPU unpadded and are padded
 // (and, on decrypt, cropped) on the device; the next batch is read from disk
-// while the GPU works on the current one.
+// and the previous one written while the GPU works on the current one.
 #include "files.hpp"
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <future>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "engine.hpp"
 #include "fileio.hpp"
@@ -20,14 +24,60 @@ namespace {
 
 constexpr uint64_t kBatchBytes = 64ull << 20;  // host staging per batch
 
+// Pinned staging buffers are cached process-wide: pinning ~100 MB per call
+// costs 0.1-1 s and varies, more than the GPU work of a short clip.
+class PinnedCache {
+ public:
+  static PinnedCache& get() {
+    static PinnedCache* c = new PinnedCache();  // never destroyed: the CUDA
+    return *c;                                  // runtime may be gone at exit
+  }
+  uint8_t* take(size_t n) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      size_t best = free_.size();
+      for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i].second >= n && (best == free_.size() || free_[i].second < free_[best].second))
+          best = i;
+      if (best != free_.size()) {
+        uint8_t* p = free_[best].first;
+        cached_ -= free_[best].second;
+        sizes_[p] = free_[best].second;
+        free_.erase(free_.begin() + long(best));
+        return p;
+      }
+    }
+    uint8_t* p = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p), n, cudaHostAllocDefault) != cudaSuccess)
+      raise(Errc::internal, "cudaHostAlloc failed");
+    std::lock_guard<std::mutex> lock(mu_);
+    sizes_[p] = n;
+    return p;
+  }
+  void give(uint8_t* p) {
+    std::lock_guard<std::mutex> lock(mu_);
+    const size_t n = sizes_[p];
+    sizes_.erase(p);
+    if (cached_ + n > kCacheCap) {
+      cudaFreeHost(p);
+      return;
+    }
+    free_.emplace_back(p, n);
+    cached_ += n;
+  }
+
+ private:
+  static constexpr size_t kCacheCap = size_t(512) << 20;
+  std::mutex mu_;
+  std::vector<std::pair<uint8_t*, size_t>> free_;
+  std::map<uint8_t*, size_t> sizes_;
+  size_t cached_ = 0;
+};
+
 struct Pinned {
   uint8_t* p = nullptr;
-  explicit Pinned(size_t n) {
-    if (cudaHostAlloc(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1),
-                      cudaHostAllocDefault) != cudaSuccess)
-      raise(Errc::internal, "cudaHostAlloc failed");
-  }
-  ~Pinned() { cudaFreeHost(p); }
+  explicit Pinned(size_t n) : p(PinnedCache::get().take(std::max<size_t>(n, 1))) {}
+  ~Pinned() { PinnedCache::get().give(p); }
   Pinned(const Pinned&) = delete;
   Pinned& operator=(const Pinned&) = delete;
 };
@@ -68,28 +118,32 @@ void encrypt_file(const char* key_hex, const FileOptions& opt, const char* in_pa
   const uint64_t sq_fb = uint64_t(h.side) * h.side * 3;
   const uint32_t B = batch_frames(sq_fb, h.frame_count);
   Pinned in_buf[2] = {Pinned(B * in_fb), Pinned(B * in_fb)};
-  Pinned out_buf(B * sq_fb);
+  Pinned out_buf[2] = {Pinned(B * sq_fb), Pinned(B * sq_fb)};
 
   auto read_batch = [&](uint8_t* dst, uint32_t nb) {
     for (uint32_t i = 0; i < nb; ++i) src.next(dst + i * in_fb);
   };
+  // batch k: read ahead (k+1) and write behind (k-1) overlap the GPU work
   uint32_t done = 0, cur = 0;
   uint32_t nb = std::min(B, h.frame_count);
   read_batch(in_buf[0].p, nb);
+  std::future<void> writing;
   while (done < h.frame_count) {
     const uint32_t next_nb = std::min(B, h.frame_count - done - nb);
     std::future<void> prefetch;
     if (next_nb)
       prefetch = std::async(std::launch::async, read_batch, in_buf[cur ^ 1].p, next_nb);
     engine.run_host_io(Engine::HostIo{in_buf[cur].p, h.orig_width, h.orig_height,
-                                      out_buf.p, h.side, h.side},
+                                      out_buf[cur].p, h.side, h.side},
                        h.side, nb, /*decrypt=*/false);
-    out.put(out_buf.p, nb);
+    if (writing.valid()) writing.get();  // batch k-1 written: its buffer is free
+    writing = std::async(std::launch::async, [&out, p = out_buf[cur].p, nb] { out.put(p, nb); });
     if (prefetch.valid()) prefetch.get();
     done += nb;
     nb = next_nb;
     cur ^= 1;
   }
+  if (writing.valid()) writing.get();
   out.finish();
 }
 
@@ -116,27 +170,31 @@ void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
   const uint64_t sq_fb = uint64_t(h.side) * h.side * 3;
   const uint32_t B = batch_frames(sq_fb, h.frame_count);
   Pinned in_buf[2] = {Pinned(B * sq_fb), Pinned(B * sq_fb)};
-  Pinned out_buf(B * out_fb);
+  Pinned out_buf[2] = {Pinned(B * out_fb), Pinned(B * out_fb)};
 
   uint32_t done = 0, cur = 0;
   uint32_t nb = std::min(B, h.frame_count);
   in.next(in_buf[0].p, nb);
+  std::future<void> writing;
   while (done < h.frame_count) {
     const uint32_t next_nb = std::min(B, h.frame_count - done - nb);
     std::future<void> prefetch;
     if (next_nb)
       prefetch = std::async(std::launch::async,
                             [&, dst = in_buf[cur ^ 1].p, k = next_nb] { in.next(dst, k); });
-    engine.run_host_io(Engine::HostIo{in_buf[cur].p, h.side, h.side, out_buf.p,
+    engine.run_host_io(Engine::HostIo{in_buf[cur].p, h.side, h.side, out_buf[cur].p,
                                       h.orig_width, h.orig_height},
                        h.side, nb, /*decrypt=*/true);
-    for (uint32_t i = 0; i < nb; ++i)
-      sink.put(out_buf.p + i * out_fb, h.orig_width, h.orig_height);
+    if (writing.valid()) writing.get();
+    writing = std::async(std::launch::async, [&sink, &h, out_fb, p = out_buf[cur].p, nb] {
+      for (uint32_t i = 0; i < nb; ++i) sink.put(p + i * out_fb, h.orig_width, h.orig_height);
+    });
     if (prefetch.valid()) prefetch.get();
     done += nb;
     nb = next_nb;
     cur ^= 1;
   }
+  if (writing.valid()) writing.get();
   sink.finish();
 }
 
