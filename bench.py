@@ -214,7 +214,7 @@ def rows_measure(stream) -> dict:
     c = synth.CONFIGS["C4"]
     W, H, n = c["width"], c["height"], c["workers"]
     key = synth.config_key("C4")
-    nf = 48
+    nf = 24
     rows = {}
 
     def blob(p):
@@ -228,13 +228,16 @@ def rows_measure(stream) -> dict:
             for t in range(nf):
                 fh.write(pool[t % 4].tobytes())
         ours, back = os.path.join(d, "ours.cve"), os.path.join(d, "ours.rgb")
-        for _ in range(2):  # the second call is timed: the first pays one-time
+        for rep in range(2):  # the second call is timed: the first pays one-time
             t0 = time.perf_counter()  # pinned-staging and engine setup
             cve.encrypt_file(key, raw, ours, workers=n, rounds=synth.ROUNDS, raw=(W, H))
             t_enc = time.perf_counter() - t0
             t0 = time.perf_counter()
             cve.decrypt_file(key, ours, back, fmt=cve.CVE_OUT_RAW)
             t_dec = time.perf_counter() - t0
+            if rep == 0:  # unlinked: their dirty pages are dropped, not written back
+                os.remove(ours)
+                os.remove(back)
         f1 = {"workload": f"{nf}-frame raw {W}x{H} RGB24 file -> CVE1 (n={n}, r=5) and back, "
                           "wall clock incl. file I/O, second call of each",
               "encrypt_file": {"value": nf / t_enc, "unit": "frames/s"},
@@ -249,6 +252,7 @@ def rows_measure(stream) -> dict:
             t0 = time.perf_counter()
             assert ref_decrypt_file(key, refc, refb, fmt=2) == 0
             r_dec = time.perf_counter() - t0
+            os.remove(refb)
             f1["reference"] = {"encrypt_file": nf / r_enc, "decrypt_file": nf / r_dec,
                                "unit": "frames/s", "cores": os.cpu_count()}
             f1["container_identical"] = blob(refc) == blob(ours)
@@ -446,6 +450,18 @@ def run_b200(args) -> None:
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e_value = frames_all / e2e_s
 
+    # ---- labelled: the reference's own call pattern -- one synchronous,
+    # in-place cve_cipher_encrypt_frame per frame on pageable numpy memory ----
+    single = cve.Cipher(key, n, synth.ROUNDS)
+    pageable = [hnp[t].copy() for t in range(F)]
+    for t in range(min(3, F)):
+        single.encrypt_frame(pageable[t])
+    t0 = time.perf_counter()
+    for t in range(F):
+        single.encrypt_frame(pageable[t])
+    single_fps = F / (time.perf_counter() - t0)
+    del single, pageable
+
     # ---- labelled decrypt line: the same clip decrypted (fresh handle) ----
     dec = cve.Cipher(key, n, synth.ROUNDS)
     for _ in range(args.warmup):
@@ -548,7 +564,10 @@ def run_b200(args) -> None:
         "gbps": value * fb / 1e9,
         "gbps_payload": value * c["width"] * c["height"] * 3 / 1e9,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": F * fb,
-                "d2h_bytes_per_step": F * fb, "api": "cve_cipher_encrypt_frames (pinned)"},
+                "d2h_bytes_per_step": F * fb, "api": "cve_cipher_encrypt_frames (pinned)",
+                "per_frame_calls": {"value": single_fps, "unit": "frames/s",
+                                    "api": "cve_cipher_encrypt_frame per frame, pageable "
+                                           "(the reference's call pattern)"}},
         "gpu_launches": launches,
         "roofline": {
             "bound": "hbm", "kernel": "k_prbg_chain (dominant: %.0f%% of the step)"
