@@ -38,7 +38,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# Each cipher handle drives 2 CUDA streams (4 with the host API); with the
+# Each cipher handle drives 1-2 CUDA streams (+2 with the host API); with the
 # default 8 hardware work queues, independent handles would falsely serialise
 # (multi-clip line).
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines")
     ap.add_argument("--no-rows", action="store_true",
                     help="skip the row f1/f3/f4 measurements")
-    ap.add_argument("--clips", type=int, default=16,
+    ap.add_argument("--clips", type=int, default=32,
                     help="independent clips for the labelled multi-clip line (0: skip)")
     return ap.parse_args()
 
@@ -509,8 +509,12 @@ def run_b200(args) -> None:
         M, MF = args.clips, 8
         bufs = [dev[:MF].clone() for _ in range(M)]
         streams = [torch.cuda.Stream() for _ in range(M)]
+        # one hardware queue per handle: M <= CUDA_DEVICE_MAX_CONNECTIONS
+        # handles never share a queue (cve_set_streams_per_handle)
+        cve.set_streams_per_handle(1)
         hs = [cve.Cipher(synth.det_key(7000 + 100 * dist.rank + k), n, synth.ROUNDS)
               for k in range(M)]
+        cve.set_streams_per_handle(2)
         for h, b, s_ in zip(hs, bufs, streams):
             h.encrypt_frames_device(b.data_ptr(), side, MF, s_.cuda_stream)
         torch.cuda.synchronize()
@@ -524,8 +528,10 @@ def run_b200(args) -> None:
         el = dist.max(time.perf_counter() - t0)
         multi = {"clips_per_gpu": M, "value": M * MF * msteps * dist.world / el,
                  "unit": "frames/s", "frames_per_clip": MF * msteps,
+                 "streams_per_handle": 1,
                  "note": "labelled scenario, not the headline: independent clips/keys "
-                         "run concurrently per GPU through the device-resident API"}
+                         "run concurrently per GPU through the device-resident API; wall "
+                         "clock between device synchronisations"}
         del hs, bufs
         torch.cuda.empty_cache()
 

@@ -261,6 +261,14 @@ CVE_B200_API cve_status cve_cipher_synchronize(cve_cipher* cipher);
  * (default: the current device). */
 CVE_B200_API cve_status cve_set_device(int device);
 
+/* Streams used by each handle created afterwards (process-wide; 1 or 2,
+ * default 2 or $CVE_B200_STREAMS_PER_HANDLE).  2: the generator chain has its
+ * own stream, so one clip never waits for its own cipher rounds (best for a
+ * single clip).  1: one hardware queue per handle, so up to
+ * CUDA_DEVICE_MAX_CONNECTIONS concurrent handles never share a queue (best
+ * for many concurrent clips). */
+CVE_B200_API cve_status cve_set_streams_per_handle(uint32_t streams);
+
 /* Copies the next `len` keystream bytes of subframe generator `worker` to
  * host memory WITHOUT consuming them from the cipher's stream (diagnostics /
  * parity; the reference's per-worker Prbg output, chaos.cpp:143-153). */

@@ -99,6 +99,7 @@ def _load() -> C.CDLL:
         "cve_cipher_decrypt_frames_async": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, vp]),
         "cve_cipher_synchronize": (C.c_int, [vp]),
         "cve_set_device": (C.c_int, [C.c_int]),
+        "cve_set_streams_per_handle": (C.c_int, [C.c_uint32]),
         "cve_cipher_peek_keystream": (C.c_int, [vp, C.c_uint32, vp, C.c_size_t]),
         "cve_cipher_prefetch_keystream": (C.c_int, [vp, C.c_uint64]),
         "cve_cipher_get_stats": (C.c_int, [vp, C.POINTER(Stats)]),
@@ -399,4 +400,10 @@ class Cipher:
 
 def set_device(device: int) -> None:
     _check(lib.cve_set_device(device))
+
+
+def set_streams_per_handle(streams: int) -> None:
+    """1: one hardware queue per handle (many concurrent clips); 2 (default):
+    the generator chain on its own stream (best for one clip)."""
+    _check(lib.cve_set_streams_per_handle(streams))
 

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -75,6 +76,26 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
 }
 }  // namespace
 
+namespace {
+std::atomic<int> g_streams{0};  // 0: not yet read from the environment
+}
+
+void set_streams_per_handle(int n) {
+  if (n != 1 && n != 2) raise(Errc::invalid_argument, "streams per handle must be 1 or 2");
+  g_streams.store(n);
+}
+
+int streams_per_handle() {
+  int v = g_streams.load();
+  if (v == 0) {
+    const char* e = std::getenv("CVE_B200_STREAMS_PER_HANDLE");
+    v = (e && std::atoi(e) == 1) ? 1 : 2;
+    int expected = 0;
+    if (!g_streams.compare_exchange_strong(expected, v)) v = expected;
+  }
+  return v;
+}
+
 void configure_kernels_once(int device) {
   static std::mutex mu;
   static std::set<int> done;
@@ -109,6 +130,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     if (v) gen_chunk_cap_ = v;
   }
 
+  one_stream_ = streams_per_handle() == 1;
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -118,6 +140,10 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   // hardware queues, so 16 concurrent handles fit CUDA_DEVICE_MAX_CONNECTIONS
   // = 32 without sharing a queue with another handle's long chain launches.
   s_ver_ = s_work_;
+  if (one_stream_) {  // generator on the rounds stream too: one hardware queue per handle
+    ck(cudaStreamDestroy(s_gen_), "stream");
+    s_gen_ = s_work_;
+  }
 
   const uint32_t nl = 2 * n_;
   std::vector<LaneConst> lc(nl);
@@ -158,7 +184,7 @@ Engine::~Engine() {
   cudaFree(ring_);
   free_prbg(pb_);
   cudaFree(d_lc_);
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
 }
 

@@ -136,3 +136,27 @@ def test_frame_model():
     sq = cve.pad_to_square(img, 4)
     assert sq.shape == (8, 8, 3) and not sq[5:].any() and not sq[:, 7:].any()
     assert np.array_equal(cve.crop_to_original(sq, 7, 5), img)
+
+
+def test_streams_per_handle_setting():
+    L = cve.lib
+    for bad in (0, 3, 100):
+        assert L.cve_set_streams_per_handle(bad) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_set_streams_per_handle(1) == cve.CVE_OK
+    assert L.cve_set_streams_per_handle(2) == cve.CVE_OK
+
+
+def test_analysis_and_tool_argument_checks():
+    # reference capi.cpp:335-383: null options / paths / blocks
+    L = cve.lib
+    out = C.c_void_p()
+    assert L.cve_analyze(None, C.byref(out)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    o = cve.AnalyzeOptions(None, None, 0, 0, 0, 0, 0)
+    assert L.cve_analyze(C.byref(o), C.byref(out)) == cve.CVE_ERROR_INVALID_ARGUMENT
+    o = cve.AnalyzeOptions(b"x.ppm", None, 0, 0, 0, 0, 0)
+    assert L.cve_analyze(C.byref(o), None) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_add_noise_file(None, b"o", 0.1, 1) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_crop_file(b"i", None, None, 0) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_crop_file(b"i", b"o", None, 2) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_frame_stats_device(None, None, 8, None, None, None) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT

@@ -322,3 +322,23 @@ def test_concurrent_handles_stress():
                 a = f.copy()
                 assert o.encrypt(a) == 0
                 assert np.array_equal(a, g), (rep, k)
+
+
+def test_one_stream_handles_match_oracle():
+    # cve_set_streams_per_handle(1): generator, verify and rounds on one
+    # stream per handle -- same bytes, several handles interleaved
+    cve.set_streams_per_handle(1)
+    try:
+        shapes = [(96, 8, 5), (64, 16, 3), (90, 3, 2)]
+        hs = [cve.Cipher(synth.det_key(4000 + k), n, r) for k, (s, n, r) in enumerate(shapes)]
+    finally:
+        cve.set_streams_per_handle(2)
+    for t in range(3):
+        for k, ((side, n, r), h) in enumerate(zip(shapes, hs)):
+            f = rand_frames(side, 1, 100 * k + t)[0]
+            a, b = f.copy(), f.copy()
+            h.encrypt_frame(b)
+            if t == 0:
+                hs[k].oracle = Oracle(synth.det_key(4000 + k), n, r)
+            assert hs[k].oracle.encrypt(a) == 0
+            assert np.array_equal(a, b), (k, t)
