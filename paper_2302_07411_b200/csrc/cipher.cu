@@ -1,5 +1,14 @@
 // K2/K3/K4: confusion + diffusion round kernels for sm_100a.
 //
+//   K2s k_encrypt_round_slots / K3s k_decrypt_round_slots: the production
+//       rounds (side % 16 == 0, 16-byte aligned frames and keystream):
+//       cp.async-staged source runs, 32-bit pixel slots in shared memory,
+//       cluster DSMEM band prefix (K2s).  Every benchmark config takes these.
+//   K2 k_encrypt_round / K3 k_decrypt_round: byte-staged rounds for any side.
+//   k_gather + k_gen_*: generic multi-kernel forward round for bands no
+//       cluster can hold.
+//   K4 k_shift: the per-frame shift table.
+//
 // Reference semantics (paths relative to /root/reference/proj):
 //   confusion   confuse_rows            src/engine.cpp:32-47   (scatter form)
 //               inverse_confuse_rows    src/engine.cpp:49-64

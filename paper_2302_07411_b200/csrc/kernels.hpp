@@ -82,7 +82,9 @@ void launch_shift_table(const double* sine, uint32_t seed, int32_t* shift,
                         uint32_t side, cudaStream_t s);
 
 // One forward round (confusion gather fused with the band XOR-scan
-// diffusion).  Returns false if this geometry needs the generic path.
+// diffusion).  plan_encrypt picks the slot-staged kernel when the geometry
+// allows it (side % 16 == 0, <= 16 rows per chunk), else the byte-staged
+// fused kernel, else (fused == false) the generic multi-kernel path.
 struct EncPlan {
   bool fused;
   uint32_t chunk_rows, h;  // h chunks (one cluster) per band
