@@ -47,6 +47,27 @@ namespace cg = cooperative_groups;
 namespace cveb {
 namespace {
 
+// Device-side bounds checks (make BOUNDS=1): every global address the round
+// kernels form is checked against its buffer before use; a failure prints
+// and traps.  Compiled out otherwise.
+#ifdef CVE_B200_BOUNDS
+#define CVE_CHECK(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("cve bounds check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__); \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define CVE_CHECK(cond) ((void)0)
+#endif
+__device__ __forceinline__ bool within(const void* p, uint64_t n, const void* base,
+                                       uint64_t bytes) {
+  const uint8_t* q = static_cast<const uint8_t*>(p);
+  const uint8_t* b = static_cast<const uint8_t*>(base);
+  return q >= b && q + n <= b + bytes;
+}
+
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kEncThreads = 512;
 constexpr int kSeg = 4;  // granules per thread per super-tile
@@ -156,6 +177,7 @@ struct EncArgs {
   uint32_t side, n, rows, chunk_rows, h;
   uint64_t region;
   FastDiv div_cr;
+  uint64_t frame_bytes;  // bounds checks only
 };
 
 __device__ __forceinline__ uint8_t seed_byte(const EncArgs& a, uint32_t band) {
@@ -446,6 +468,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
     uint64_t kp = kbase + 48ull * g;
     if (kp >= a.ring_bytes) kp -= a.ring_bytes;
     const uint8_t* p = ks + kp;
+    if (g < G) CVE_CHECK(within(p, 48, ks, a.ring_bytes));
 #pragma unroll
     for (int i = 0; i < 3; ++i) kv[i] = g < G ? ld_stream(p + 16 * i) : make_uint4(0, 0, 0, 0);
   };
@@ -466,8 +489,13 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t sr = st * kStageRows + cpr + 128u * i;
-      const uint32_t b0 = 3u * (sr * (side - 1) + al0) + (sr > al0 ? 3u * side : 0u);
-      const bool need = sr < side && 16u * cpc < (b0 & 15u) + 3u * cr;
+      const bool wraps = sr > al0;  // o0 = al0 - sr (+ side)
+      const uint32_t b0 = 3u * (sr * (side - 1) + al0) + (wraps ? 3u * side : 0u);
+      const uint32_t o0 = al0 - sr + (wraps ? side : 0u);
+      // runs that wrap past the row end are read by the deferred pass; their
+      // window could run past the end of the frame (last chunk, row side-1)
+      const bool need = sr < side && o0 + cr <= side && 16u * cpc < (b0 & 15u) + 3u * cr;
+      if (need) CVE_CHECK(within(a.src + (b0 & ~15u) + 16u * cpc, 16, a.src, a.frame_bytes));
       cp_async16(dst0 + 128u * kWinBytes * i, a.src + (b0 & ~15u) + 16u * cpc, need);
     }
     cp_async_commit();
@@ -552,6 +580,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
       uint32_t o = o0 + k;
       o -= o >= side ? side : 0u;
       const uint8_t* sp = a.src + (uint64_t(sr) * side + o) * 3;
+      CVE_CHECK(within(sp, 3, a.src, a.frame_bytes));
       const uint32_t pix = uint32_t(__ldg(sp)) | (uint32_t(__ldg(sp + 1)) << 8) |
                            (uint32_t(__ldg(sp + 2)) << 16);
       uint32_t be = o0 + cks[k];
@@ -641,6 +670,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
                                          uint64_t(chunk) * cb);
   if (ntiles == 1) {
     if (tid < G) {
+      CVE_CHECK(within(out4 + 3 * tid, 48, a.dst, a.frame_bytes));
       const uint32_t m = (prefix_share ^ excl_last) * 0x01010101u;
       out4[3 * tid] = make_uint4(res[0] ^ m, res[1] ^ m, res[2] ^ m, res[3] ^ m);
       out4[3 * tid + 1] = make_uint4(res[4] ^ m, res[5] ^ m, res[6] ^ m, res[7] ^ m);
@@ -651,6 +681,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
     for (uint32_t q = tid; q < 3 * G; q += kSlotThreads) {
       const uint32_t g = q / 3, c = q - 3 * g;
       const uint4 v = smem[4 * g + (c ^ ((g >> 1) & 3u))];
+      CVE_CHECK(within(out4 + q, 16, a.dst, a.frame_bytes));
       out4[q] = make_uint4(v.x ^ m, v.y ^ m, v.z ^ m, v.w ^ m);
     }
   }
@@ -671,6 +702,7 @@ struct DecArgs {
   uint32_t side, n, rows, T;
   uint64_t region;
   FastDiv div_T, div_rows;
+  uint64_t frame_bytes;  // bounds checks only
 };
 
 __device__ __forceinline__ uint8_t ks_byte(const DecArgs& a, uint32_t band,
@@ -856,6 +888,10 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
           if (need) src = a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes + kp;
         }
       }
+      if (need && cps < 4) CVE_CHECK(within(src, 16, a.src, a.frame_bytes));
+      if (need && cps >= 4)
+        CVE_CHECK(within(src, 16, a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes,
+                         a.ring_bytes));
       cp_async16(dst, src, need);
     }
     cp_async_commit();
@@ -877,6 +913,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
   auto ks_at = [&](uint32_t band, uint32_t j) {  // keystream byte j of the round
     uint64_t kp = a.pos + j;
     if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    CVE_CHECK(band < a.n && kp < a.ring_bytes);
     return uint32_t(__ldg(a.ring + uint64_t(band) * a.ring_bytes + kp));
   };
   // pixel m of source row al's run, byte by byte from global
@@ -898,6 +935,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
       } else {
         prev = __ldg(a.src + P + ch - 1);
       }
+      CVE_CHECK(P + ch < a.frame_bytes && (j == 0 || P + ch >= 1));
       pix |= (((b ^ __ldg(a.src + P + ch) ^ prev) - b) & 0xFFu) << (8 * ch);
     }
     return pix;
@@ -990,6 +1028,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
       y[3 * c + 1] = __byte_perm(v.y, v.z, 0x5421);
       y[3 * c + 2] = __byte_perm(v.z, v.w, 0x6542);
     }
+    CVE_CHECK(within(out4 + 3 * g, 48, a.dst, a.frame_bytes));
     out4[3 * g] = make_uint4(y[0], y[1], y[2], y[3]);
     out4[3 * g + 1] = make_uint4(y[4], y[5], y[6], y[7]);
     out4[3 * g + 2] = make_uint4(y[8], y[9], y[10], y[11]);
@@ -1193,7 +1232,7 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
                          reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
   if (plan.slots && aligned && ks.pos % 48 == 0 && ks.ring_bytes % 48 == 0) {
     EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
-              g.rows, plan.s_rows, plan.s_h, g.region, make_div(plan.s_rows)};
+              g.rows, plan.s_rows, plan.s_h, g.region, make_div(plan.s_rows), g.frame_bytes};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.n * plan.s_h);
     cfg.blockDim = dim3(kSlotThreads);
@@ -1213,7 +1252,8 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
   }
   if (plan.fused) {
     EncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n,
-              g.rows, plan.chunk_rows, plan.h, g.region, make_div(plan.chunk_rows)};
+              g.rows, plan.chunk_rows, plan.h, g.region, make_div(plan.chunk_rows),
+              g.frame_bytes};
     const bool vec = aligned;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.n * plan.h);
@@ -1286,7 +1326,7 @@ void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
   const uint32_t Ts = aligned ? plan_decrypt_slots(g, smem) : 0;
   if (Ts) {
     DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
-              Ts, g.region, make_div(Ts), make_div(g.rows)};
+              Ts, g.region, make_div(Ts), make_div(g.rows), g.frame_bytes};
     k_decrypt_round_slots<<<(g.side + Ts - 1) / Ts, kSlotThreads, smem, s>>>(a);
     check_launch("decrypt_round_slots");
     ++*launches;
@@ -1300,7 +1340,7 @@ void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
   smem = ((uint64_t(T) * row_bytes + 15) & ~uint64_t(15));
   if (smem > kSmemBudget) throw Error(Errc::invalid_argument, "frame side too large");
   DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
-            T, g.region, make_div(T), make_div(g.rows)};
+            T, g.region, make_div(T), make_div(g.rows), g.frame_bytes};
   const uint32_t grid = (g.side + T - 1) / T;
   if (aligned)
     k_decrypt_round<true><<<grid, kDecThreads, smem, s>>>(a);
