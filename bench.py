@@ -171,6 +171,17 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
 def cpu_baseline(name: str, seconds: float) -> dict:
     """The reference library (oracle/_ref) on host cores, bounded sample."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -193,7 +204,8 @@ def cpu_baseline(name: str, seconds: float) -> dict:
     return {"value": frames / el, "unit": "frames/s", "cores": cores, "kind": "reference",
             "sample": f"{frames} consecutive {name} frames ({synth.config_side(name)}^2, "
                       f"n={c['workers']}, r=5) in {el:.2f} s via cve_cipher_encrypt_frame, "
-                      f"parallel=1 ({c['workers']} threads on {os.cpu_count()} host cpus)"}
+                      f"parallel=1 ({c['workers']} threads on {os.cpu_count()} host cpus, "
+                      f"{cpu_model()})"}
 
 
 def rows_measure(stream) -> dict:
@@ -387,7 +399,8 @@ def run_reference(args) -> None:
                                   "kind": "reference",
                                   "sample": f"{per_step} frames per step of the {name} clip, "
                                             f"reference libcve (oracle/_ref) with parallel=1 "
-                                            f"({c['workers']} threads, {os.cpu_count()} host cpus)"},
+                                            f"({c['workers']} threads, {os.cpu_count()} host cpus, "
+                                            f"{cpu_model()})"},
                  "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0}})
     print(json.dumps(line))

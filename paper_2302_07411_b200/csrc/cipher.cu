@@ -1290,9 +1290,12 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
 }
 
 // Slot-staged inverse round: tile rows T in [6, 15] (<= side) minimising the
-// destination rows per SM, ceil(ceil(side / T) / SMs) * T (ties: larger T),
+// destination rows per SM, ceil(ceil(side / T) / SMs') * T (ties: larger T),
 // with T*side*4 (slots) + side*4 (shift table) + 2 window stages of shared
-// memory.
+// memory.  SMs' = SMs - 8: while its clip runs, each generator chain holds
+// one SM (K1 reserves it), and a CTA count equal to the SM count would then
+// need a second wave (measured at 1920^2: T = 13 -> 148 CTAs ran at 2x the
+// single-wave time next to a chain).
 uint32_t plan_decrypt_slots(const Geom& g, size_t& smem) {
   if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32) || std::getenv("CVE_B200_NO_SLOTS"))
     return 0;
@@ -1306,7 +1309,8 @@ uint32_t plan_decrypt_slots(const Geom& g, size_t& smem) {
                         3 * kDecStageRows * 16 + 2 * kDecStageBytes;
     if (need > kSlotSmemMax) continue;
     const uint64_t ctas = (g.side + T - 1) / T;
-    const uint64_t load = (ctas + uint64_t(sms) - 1) / uint64_t(sms) * T;
+    const uint64_t free_sms = uint64_t(std::max(1, sms - 8));
+    const uint64_t load = (ctas + free_sms - 1) / free_sms * T;
     if (load <= best_load) {
       best_load = load;
       best = T;

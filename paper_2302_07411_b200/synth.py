@@ -168,6 +168,12 @@ def config_frame(name: str, t: int) -> np.ndarray:
     return out
 
 
+def config_frame_job(arg) -> np.ndarray:
+    """config_frame((name, t)): a picklable entry point for process pools."""
+    name, t = arg
+    return config_frame(name, t)
+
+
 def config_side(name: str) -> int:
     c = CONFIGS[name]
     return (max(c["width"], c["height"]) + c["workers"] - 1) // c["workers"] * c["workers"]

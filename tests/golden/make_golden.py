@@ -11,8 +11,11 @@ paper_2302_07411_b200.synth and records:
   all-zero and all-255 edge frames); C3 adds the one-bit key-flip variant.
 * small.json -- full plaintext/ciphertext hex for small shapes (fast exact
   checks incl. decrypt), and full worker keystream prefixes.
+* clips.json (--full-clips) -- SHA-256 of the plaintext and of the reference
+  ciphertext of EVERY frame of the C3 (240), C4 (1000) and C5 (500) clips
+  (SURVEY 8(d) parity gate: per-frame digest equality for every frame).
 
-Usage:  python tests/golden/make_golden.py   (needs oracle/_ref built)
+Usage:  python tests/golden/make_golden.py [--full-clips]   (needs oracle/_ref)
 """
 from __future__ import annotations
 
@@ -134,5 +137,41 @@ def main() -> None:
     print("wrote", HERE)
 
 
+def full_clips() -> None:
+    """Every frame of C3/C4/C5 through the reference, frames synthesised in a
+    process pool (the reference clip itself is sequential)."""
+    import multiprocessing as mp
+    out = {}
+    with mp.Pool(max(1, (os.cpu_count() or 2) - 1)) as pool:
+        for name in ("C3", "C4", "C5"):
+            c = synth.CONFIGS[name]
+            ref = Reference(synth.config_key(name), c["workers"], synth.ROUNDS, 1)
+            plain_sha, cipher_sha = [], []
+            jobs = ((name, t) for t in range(c["frames"]))
+            for t, f in enumerate(pool.imap(_frame_job, jobs, chunksize=2)):
+                plain_sha.append(sha(f))
+                assert ref.encrypt(f) == 0
+                cipher_sha.append(sha(f))
+                if t % 100 == 0:
+                    print(name, t, flush=True)
+            out[name] = {"key": synth.config_key(name), "side": int(f.shape[0]),
+                         "workers": c["workers"], "rounds": synth.ROUNDS,
+                         "frames": c["frames"], "plain_sha256": plain_sha,
+                         "cipher_sha256": cipher_sha}
+            ref.close()
+            print(name, "done", flush=True)
+    with open(os.path.join(HERE, "clips.json"), "w") as fh:
+        json.dump(out, fh)
+    print("wrote clips.json")
+
+
+def _frame_job(arg):
+    name, t = arg
+    return synth.config_frame(name, t)
+
+
 if __name__ == "__main__":
-    main()
+    if "--full-clips" in sys.argv:
+        full_clips()
+    else:
+        main()

@@ -342,3 +342,32 @@ def test_one_stream_handles_match_oracle():
                 hs[k].oracle = Oracle(synth.det_key(4000 + k), n, r)
             assert hs[k].oracle.encrypt(a) == 0
             assert np.array_equal(a, b), (k, t)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_every_frame_of_config_clips_vs_reference(name):
+    # SURVEY 8(d) parity gate: per-frame digest equality with the reference
+    # for EVERY frame of the clip (C3 240, C4 1000, C5 500 frames; digests of
+    # the reference's own ciphertext, tests/golden/clips.json).  Plaintext
+    # digests are checked too, so a drift in the synthetic frames would show
+    # as such rather than as a cipher mismatch.
+    import multiprocessing as mp
+    path = os.path.join(GOLD, "clips.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/clips.json not generated")
+    g = load("clips.json")[name]
+    c = cve.Cipher(g["key"], g["workers"], g["rounds"])
+    batch = {"C3": 48, "C4": 25, "C5": 10}[name]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(max(1, min(16, (os.cpu_count() or 2) - 1))) as pool:
+        frames = pool.imap(synth.config_frame_job, ((name, t) for t in range(g["frames"])),
+                           chunksize=2)
+        t = 0
+        while t < g["frames"]:
+            buf = np.stack([next(frames) for _ in range(min(batch, g["frames"] - t))])
+            for i in range(len(buf)):
+                assert sha(buf[i]) == g["plain_sha256"][t + i], (name, t + i, "plaintext")
+            c.encrypt_frames(buf)
+            for i in range(len(buf)):
+                assert sha(buf[i]) == g["cipher_sha256"][t + i], (name, t + i)
+            t += len(buf)

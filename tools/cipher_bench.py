@@ -18,7 +18,10 @@ for name in sys.argv[1:] or ["C1", "C3", "C4", "C5"]:
         best = None
         for rep in range(3):  # best of 3: the keystream is generated first, so
             h = cve.Cipher(synth.config_key(name), n, 5)  # only cipher time counts
-            h.prefetch_keystream(NF * need); h.synchronize()
+            # normal ring (4 frames) unless CB_BIG_RING: the keystream of later
+            # frames is generated on the fly, outside the timed cipher events
+            h.prefetch_keystream((NF if os.environ.get("CB_BIG_RING") else 1) * need)
+            h.synchronize()
             s0 = h.stats()
             fn = h.encrypt_frames_device if mode == "enc" else h.decrypt_frames_device
             fn(frames.data_ptr(), side, NF, torch.cuda.current_stream().cuda_stream)

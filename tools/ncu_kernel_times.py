@@ -13,7 +13,8 @@ for r in rows[start + 1:]:
         continue
     name = re.sub(r"\(.*", "", r[ik]).replace("cveb::", "").replace("<unnamed>::", "")
     v = float(r[iv].replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[iu], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+             "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[iu], 1.0)
     agg[name].append(v * scale)
 for k, v in sorted(agg.items(), key=lambda t: -sum(t[1])):
     print(f"{k:45s} n={len(v):5d} mean={sum(v)/len(v):10.2f} us  min={min(v):10.2f} us  total={sum(v)/1e3:9.3f} ms")
