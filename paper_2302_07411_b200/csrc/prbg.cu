@@ -29,6 +29,8 @@
 // explicit _rn intrinsic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cmath>
 #include <cstring>
 
@@ -176,69 +178,81 @@ __global__ void __launch_bounds__(256)
                        const double* __restrict__ verified_end,
                        const LaneConst* __restrict__ lcs,
                        const double* __restrict__ orbit, uint32_t iters,
-                       uint32_t nlanes, uint8_t* __restrict__ ring,
+                       uint32_t nlanes, uint32_t gs, uint8_t* __restrict__ ring,
                        uint64_t ring_bytes, uint64_t it0,
                        unsigned* __restrict__ bad) {
+  // Persistent threads: thread = (lane l, first group g0), then groups
+  // g0 + gs, g0 + 2 gs, ...; the lane constants are loaded once.  Every warp
+  // runs the same number of trips (shuffle partners stay paired); trips past
+  // the last group, and threads past gs * nlanes, shadow a real group and
+  // store nothing.
   const uint64_t gid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint32_t groups = iters / 8;
-  const bool live = gid < uint64_t(groups) * nlanes;
-  // idle threads of the last warp shadow a real (lane, group) so that the
-  // shuffles see full warps; they store nothing
-  const uint64_t me = live ? gid : gid % nlanes;
+  const bool live_thread = gid < uint64_t(gs) * nlanes;
+  const uint64_t me = live_thread ? gid : gid % nlanes;
   const uint32_t l = uint32_t(me % nlanes);
-  const uint32_t g = uint32_t(me / nlanes);
+  const uint32_t g0 = uint32_t(me / nlanes);
   const LaneConst c = lcs[l];
-  const size_t i0 = size_t(g) * 8;
-  double x;
-  bool cont = true;  // continuity with the previous launch (group 0 only)
-  if (g) {
-    x = orbit[(i0 - 1) * nlanes + l];
-  } else {
-    x = ckpt[l];
-    cont = x == verified_end[l];
-  }
-  double y[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) y[t] = __ldg(orbit + (i0 + t) * nlanes + l);  // all in flight
-  bool suspect = false;
-  bool ok = plcm_verify_fast(x, y[0], c, suspect);
-#pragma unroll
-  for (int t = 1; t < 8; ++t) ok &= plcm_verify_fast(y[t - 1], y[t], c, suspect);
-  if (suspect) {  // rare: decide this group exactly
-    ok = true;
-    for (int t = 0; t < 8; ++t) ok &= plcm_verify_exact(t ? y[t - 1] : x, y[t], c);
-  }
-  if (!(ok && cont) && live) atomicOr(bad + (l >> 1), 1u);
-  uint32_t lo[8], hi[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    lo[t] = unsigned(__double2loint(y[t]));
-    hi[t] = unsigned(__double2hiint(y[t]));
-  }
   const uint32_t odd = l & 1u;
-  uint32_t mlo[4], mhi[4];
+  const uint32_t trips = (groups + gs - 1) / gs;
+  bool flagged = false;
+  for (uint32_t k = 0; k < trips; ++k) {
+    const uint32_t gr = g0 + k * gs;
+    const bool live = live_thread && gr < groups;
+    const uint32_t g = live ? gr : groups - 1;
+    const size_t i0 = size_t(g) * 8;
+    double x;
+    bool cont = true;  // continuity with the previous launch (group 0 only)
+    if (g) {
+      x = orbit[(i0 - 1) * nlanes + l];
+    } else {
+      x = ckpt[l];
+      cont = x == verified_end[l];
+    }
+    double y[8];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const uint32_t slo = odd ? lo[t] : lo[t + 4];
-    const uint32_t shi = odd ? hi[t] : hi[t + 4];
-    const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
-    const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
-    mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
-    mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
+    for (int t = 0; t < 8; ++t) y[t] = __ldg(orbit + (i0 + t) * nlanes + l);  // all in flight
+    bool suspect = false;
+    bool ok = plcm_verify_fast(x, y[0], c, suspect);
+#pragma unroll
+    for (int t = 1; t < 8; ++t) ok &= plcm_verify_fast(y[t - 1], y[t], c, suspect);
+    if (suspect) {  // rare: decide this group exactly
+      ok = true;
+      for (int t = 0; t < 8; ++t) ok &= plcm_verify_exact(t ? y[t - 1] : x, y[t], c);
+    }
+    flagged |= live && !(ok && cont);
+    uint32_t lo[8], hi[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      lo[t] = unsigned(__double2loint(y[t]));
+      hi[t] = unsigned(__double2hiint(y[t]));
+    }
+    uint32_t mlo[4], mhi[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t slo = odd ? lo[t] : lo[t + 4];
+      const uint32_t shi = odd ? hi[t] : hi[t + 4];
+      const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
+      const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
+      mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
+      mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
+    }
+    const uint32_t w0 = mlo[0], w1 = mhi[0] | (mlo[1] << 16),
+                   w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
+                   w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
+    if (live) {
+      const uint64_t off = ((it0 + i0) * 6u) % ring_bytes;  // 48-byte aligned
+      uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
+      if (!odd) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+        *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w4, w5);
+      } else {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+        *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w2, w3, w4, w5);
+      }
+    }
   }
-  const uint32_t w0 = mlo[0], w1 = mhi[0] | (mlo[1] << 16),
-                 w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
-                 w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
-  if (!live) return;
-  const uint64_t off = ((it0 + i0) * 6u) % ring_bytes;  // 48-byte aligned
-  uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
-  if (!odd) {
-    *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-    *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w4, w5);
-  } else {
-    *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
-    *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w2, w3, w4, w5);
-  }
+  if (flagged) atomicOr(bad + (l >> 1), 1u);
 }
 
 // (3) One thread per worker.  Verified: advance the verified end point to
@@ -310,9 +324,22 @@ void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
                         uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
                         uint32_t iters, uint32_t nlanes, cudaStream_t s) {
   const uint32_t nw = nlanes / 2;
-  const uint64_t threads = uint64_t(iters / 8) * nlanes;
+  // group streams gs: enough threads to fill the GPU (2048 per SM), each
+  // thread walking ceil(groups / gs) groups of its lane
+  static int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    return v;
+  }();
+  const uint32_t groups = iters / 8;
+  const uint64_t target = uint64_t(sms) * 2048;
+  const uint32_t gs = uint32_t(std::max<uint64_t>(
+      1, std::min<uint64_t>(groups, (target + nlanes - 1) / nlanes)));
+  const uint64_t threads = uint64_t(gs) * nlanes;
   k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
-      b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nlanes, ring, ring_bytes,
+      b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nlanes, gs, ring, ring_bytes,
       it0, b.bad);
   k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.orbit[slot], b.verified_end, lc,
                                                 iters, nw, ring, ring_bytes, it0,
