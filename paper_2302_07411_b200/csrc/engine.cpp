@@ -135,11 +135,10 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   ck(cudaStreamCreateWithFlags(&s_work_, cudaStreamNonBlocking), "stream");
-  // Verification shares s_work: every frame's rounds wait for their
+  // Verification runs on s_work: every frame's rounds wait for their
   // keystream's verify anyway, and a device-API handle then occupies two
   // hardware queues, so 16 concurrent handles fit CUDA_DEVICE_MAX_CONNECTIONS
   // = 32 without sharing a queue with another handle's long chain launches.
-  s_ver_ = s_work_;
   if (one_stream_) {  // generator on the rounds stream too: one hardware queue per handle
     ck(cudaStreamDestroy(s_gen_), "stream");
     s_gen_ = s_work_;
@@ -373,15 +372,15 @@ void Engine::gen_until(uint64_t end_byte) {
     ck(cudaGetLastError(), "prbg_chain launch");
     timed_end(s_gen_);
     ck(cudaEventRecord(chain_done_[slot], s_gen_), "cudaEventRecord");
-    // (2)+(3) verify, emit, fix up on s_ver while the next chain runs.
+    // (2)+(3) verify, emit, fix up on s_work while the next chain runs.
     // Ring bytes below write_end - R get overwritten: their readers must be
     // done.
-    ck(cudaStreamWaitEvent(s_ver_, chain_done_[slot], 0), "wait chain");
+    ck(cudaStreamWaitEvent(s_work_, chain_done_[slot], 0), "wait chain");
     const uint64_t write_end = (gen_iters_ + chunk) * 6;
     if (write_end > ring_bytes_) {
       const uint64_t dead = write_end - ring_bytes_;
       while (!consumers_.empty() && consumers_.front().lo < dead) {
-        ck(cudaStreamWaitEvent(s_ver_, consumers_.front().done, 0), "wait");
+        ck(cudaStreamWaitEvent(s_work_, consumers_.front().done, 0), "wait");
         if (consumers_.front().hi <= dead) {
           ev_put(consumers_.front().done);
           consumers_.pop_front();
@@ -390,19 +389,19 @@ void Engine::gen_until(uint64_t end_byte) {
         }
       }
     }
-    timed_begin(s_ver_, false, true);
+    timed_begin(s_work_, false, true);
     launch_prbg_verify(pb_, slot, d_lc_, ring_, ring_bytes_, gen_iters_,
-                       uint32_t(chunk), 2 * n_, s_ver_);
+                       uint32_t(chunk), 2 * n_, s_work_);
     ck(cudaGetLastError(), "prbg_verify launch");
-    timed_end(s_ver_);
-    ck(cudaEventRecord(ver_done_[slot], s_ver_), "cudaEventRecord");
+    timed_end(s_work_);
+    ck(cudaEventRecord(ver_done_[slot], s_work_), "cudaEventRecord");
     st_.kernel_launches += 3;
     ++st_.prbg_launches;
     ++launches_;
     gen_iters_ += chunk;
     st_.keystream_iters += chunk;
     GenMark m{gen_iters_ * 6, ev_get()};
-    ck(cudaEventRecord(m.ev, s_ver_), "cudaEventRecord");
+    ck(cudaEventRecord(m.ev, s_work_), "cudaEventRecord");
     gens_.push_back(m);
   }
 }

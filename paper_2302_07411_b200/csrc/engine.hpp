@@ -8,10 +8,12 @@
 // synchronous frame loop becomes a pipeline:
 //
 //   s_gen : K1 chain kernels, back to back, ahead of the frames that need them
-//   s_ver : K1 verification + keystream emission (+ exact fix-up)
-//   s_h2d : host->device frame copies
-//   s_work: K4 shift table, K2/K3 rounds (waits on s_h2d and s_ver events)
-//   s_d2h : device->host copies (waits on s_work)
+//           (the same stream as s_work with cve_set_streams_per_handle(1))
+//   s_work: K1 verification + keystream emission (+ exact fix-up) of each
+//           chain launch, then K4 shift table and K2/K3 rounds of the frames
+//           whose keystream it verified (waits on s_gen and s_h2d events)
+//   s_h2d : host->device frame copies  } created on the first host-API call
+//   s_d2h : device->host copies        } (waits on s_work)
 //
 // The keystream lives in one ring per worker (ring_bytes each).  Stream byte
 // s of worker i sits at ring[i*ring_bytes + s % ring_bytes]; the generator
@@ -121,9 +123,8 @@ class Engine {
   int dev_;
   Coordinator coord_;
 
-  // s_ver_ aliases s_work_; s_h2d_/s_d2h_ are created on first host-API use.
-  cudaStream_t s_gen_ = nullptr, s_ver_ = nullptr, s_h2d_ = nullptr,
-               s_work_ = nullptr, s_d2h_ = nullptr;
+  // s_h2d_/s_d2h_ are created on first host-API use.
+  cudaStream_t s_gen_ = nullptr, s_h2d_ = nullptr, s_work_ = nullptr, s_d2h_ = nullptr;
   cudaEvent_t chain_done_[2] = {nullptr, nullptr};
   cudaEvent_t ver_done_[2] = {nullptr, nullptr};
   uint64_t launches_ = 0;  // generator launches (slot = launches_ & 1)
