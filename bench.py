@@ -233,25 +233,38 @@ def rows_measure(stream) -> dict:
         with open(p, "rb") as fh:
             return fh.read()
 
-    with tempfile.TemporaryDirectory() as d:
+    # RAM-backed scratch when there is room: disk writeback from one leg
+    # otherwise shows up as noise in the next (host I/O, not the engine)
+    tmp_root = None
+    try:
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize > (4 << 30):
+            tmp_root = "/dev/shm"
+    except OSError:
+        pass
+    with tempfile.TemporaryDirectory(dir=tmp_root) as d:
         raw = os.path.join(d, "clip.rgb")
         pool = [synth.correlated_frame(W, H, t, 7000 + c["key_seed"]) for t in range(4)]
         with open(raw, "wb") as fh:
             for t in range(nf):
                 fh.write(pool[t % 4].tobytes())
         ours, back = os.path.join(d, "ours.cve"), os.path.join(d, "ours.rgb")
-        for rep in range(2):  # the second call is timed: the first pays one-time
+        t_enc = t_dec = float("inf")
+        for rep in range(3):  # best of the 2nd/3rd calls: the first pays one-time
             t0 = time.perf_counter()  # pinned-staging and engine setup
             cve.encrypt_file(key, raw, ours, workers=n, rounds=synth.ROUNDS, raw=(W, H))
-            t_enc = time.perf_counter() - t0
+            te = time.perf_counter() - t0
             t0 = time.perf_counter()
             cve.decrypt_file(key, ours, back, fmt=cve.CVE_OUT_RAW)
-            t_dec = time.perf_counter() - t0
-            if rep == 0:  # unlinked: their dirty pages are dropped, not written back
+            td = time.perf_counter() - t0
+            if rep:
+                t_enc, t_dec = min(t_enc, te), min(t_dec, td)
+            if rep < 2:  # unlinked: their dirty pages are dropped, not written back
                 os.remove(ours)
                 os.remove(back)
         f1 = {"workload": f"{nf}-frame raw {W}x{H} RGB24 file -> CVE1 (n={n}, r=5) and back, "
-                          "wall clock incl. file I/O, second call of each",
+                          "wall clock incl. file I/O, best of the 2nd/3rd calls; "
+                          f"scratch {'RAM (/dev/shm)' if tmp_root else 'disk'}",
               "encrypt_file": {"value": nf / t_enc, "unit": "frames/s"},
               "decrypt_file": {"value": nf / t_dec, "unit": "frames/s"},
               "round_trip": blob(back) == blob(raw)}
@@ -272,9 +285,11 @@ def rows_measure(stream) -> dict:
 
         nbytes = 64 << 20
         o3 = os.path.join(d, "ours.nist")
-        t0 = time.perf_counter()
-        cve.nist_export(key, n, nbytes, o3)
-        t3 = time.perf_counter() - t0
+        t3 = float("inf")
+        for _ in range(2):
+            t0 = time.perf_counter()
+            cve.nist_export(key, n, nbytes, o3)
+            t3 = min(t3, time.perf_counter() - t0)
         f3 = {"workload": f"{nbytes >> 20} MiB of generator bytes, {n} workers",
               "value": nbytes / t3 / 1e6, "unit": "MB/s"}
         if have_ref:
@@ -293,16 +308,21 @@ def rows_measure(stream) -> dict:
         for p_, img in ((pa, a_img), (pb, b_img)):
             with open(p_, "wb") as fh:
                 fh.write(f"P6\n{side} {side}\n255\n".encode() + img.tobytes())
-        t0 = time.perf_counter()
-        txt = cve.analyze(pa, second=pb, seed=1)
-        t4 = time.perf_counter() - t0
+        t4 = float("inf")
+        for _ in range(3):
+            t0 = time.perf_counter()
+            txt = cve.analyze(pa, second=pb, seed=1)
+            t4 = min(t4, time.perf_counter() - t0)
         f4 = {"workload": f"cve_analyze of a {side}^2 C4 frame with NPCR/UACI vs a second frame "
-                          "(P6 files), wall clock",
+                          "(P6 files), wall clock, best of 3",
               "analyze_ms": t4 * 1e3}
         if have_ref:
-            t0 = time.perf_counter()
-            st, rtxt = ref_analyze(pa, second=pb, seed=1)
-            f4["reference_analyze_ms"] = (time.perf_counter() - t0) * 1e3
+            tr = float("inf")
+            for _ in range(3):
+                t0 = time.perf_counter()
+                st, rtxt = ref_analyze(pa, second=pb, seed=1)
+                tr = min(tr, time.perf_counter() - t0)
+            f4["reference_analyze_ms"] = tr * 1e3
             f4["identical_text"] = st == 0 and rtxt == txt
         # device reductions alone: histograms (reads F) + NPCR/UACI (reads 2F),
         # cycling over 8 frame pairs (177 MB, larger than L2)

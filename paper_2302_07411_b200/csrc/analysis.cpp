@@ -189,20 +189,27 @@ void gpu_counts(const HostFrame& a, const HostFrame* b, int device, uint64_t his
   cudaStream_t s = nullptr;
   uint8_t *da = nullptr, *db = nullptr;
   unsigned long long* dout = nullptr;
+  // stream-ordered allocations: cudaFree would synchronise the whole device
+  // (and wait for any other handle's work); cudaFreeAsync does not
   auto cleanup = [&] {
-    if (s) cudaStreamSynchronize(s);
-    cudaFree(da);
-    cudaFree(db);
-    cudaFree(dout);
-    if (s) cudaStreamDestroy(s);
+    if (s) {
+      if (da) cudaFreeAsync(da, s);
+      if (db) cudaFreeAsync(db, s);
+      if (dout) cudaFreeAsync(dout, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
   };
   try {
     check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    check_cuda(cudaMalloc(&da, std::max<uint64_t>(nbytes, 16)), "cudaMalloc");
-    check_cuda(cudaMalloc(&dout, 774 * sizeof(unsigned long long)), "cudaMalloc");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&da), std::max<uint64_t>(nbytes, 16), s),
+               "cudaMallocAsync");
+    check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dout), 774 * sizeof(unsigned long long), s),
+               "cudaMallocAsync");
     check_cuda(cudaMemcpyAsync(da, a.px.data(), nbytes, cudaMemcpyHostToDevice, s), "H2D");
     if (b) {
-      check_cuda(cudaMalloc(&db, std::max<uint64_t>(nbytes, 16)), "cudaMalloc");
+      check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&db), std::max<uint64_t>(nbytes, 16), s),
+                 "cudaMallocAsync");
       check_cuda(cudaMemcpyAsync(db, b->px.data(), nbytes, cudaMemcpyHostToDevice, s), "H2D");
     }
     launch_frame_stats(da, db, nbytes, dout, b ? dout + 768 : nullptr, s);
