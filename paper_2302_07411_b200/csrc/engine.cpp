@@ -28,23 +28,43 @@ constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
 // synchronous cudaMemcpy / cudaMemset run on the legacy default stream, which
 // does not order against our non-blocking streams (a pageable H2D cudaMemcpy
 // may even return before its DMA lands).
-PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s) {
+// Largest launch (iterations, multiple of 8) the orbit budget allows.
+uint32_t orbit_cap_iters(uint32_t nlanes) {
+  const uint64_t iters = std::min<uint64_t>(kOrbitBytes / (8ull * nlanes), 1u << 20) / 8 * 8;
+  return uint32_t(std::max<uint64_t>(iters, 8));
+}
+
+// orbit_iters = 0: no orbit buffers yet (an Engine sizes them from its ring,
+// resize_orbit); otherwise capacity for launches of orbit_iters iterations.
+PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
   PrbgBuffers b{};
-  uint64_t iters = kOrbitBytes / (8ull * nlanes);
-  iters = std::min<uint64_t>(iters, 1u << 20) / 8 * 8;
-  b.max_iters = uint32_t(std::max<uint64_t>(iters, 8));
+  b.max_iters = orbit_iters;
   const size_t lanes_bytes = nlanes * sizeof(double);
   ck(cudaMalloc(&b.state, lanes_bytes), "cudaMalloc state");
   ck(cudaMalloc(&b.verified_end, lanes_bytes), "cudaMalloc state");
   for (int k = 0; k < 2; ++k) {
     ck(cudaMalloc(&b.ckpt[k], lanes_bytes), "cudaMalloc ckpt");
-    ck(cudaMalloc(&b.orbit[k], uint64_t(b.max_iters) * lanes_bytes), "cudaMalloc orbit");
+    if (b.max_iters)
+      ck(cudaMalloc(&b.orbit[k], uint64_t(b.max_iters) * lanes_bytes), "cudaMalloc orbit");
   }
   ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
   ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
   ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
   ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
   return b;
+}
+
+// Grows both orbit buffers to launches of `iters` iterations (caller has
+// synchronised: no kernel may be using them).
+void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(b.orbit[k]);
+    b.orbit[k] = nullptr;
+  }
+  b.max_iters = 0;
+  for (int k = 0; k < 2; ++k)
+    ck(cudaMalloc(&b.orbit[k], uint64_t(iters) * nlanes * sizeof(double)), "cudaMalloc orbit");
+  b.max_iters = iters;
 }
 
 void free_prbg(PrbgBuffers& b) {
@@ -153,7 +173,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
     x0[2 * i] = lanes[i].a.x0;
     x0[2 * i + 1] = lanes[i].b.x0;
   }
-  pb_ = alloc_prbg(nl, s_gen_);
+  pb_ = alloc_prbg(nl, s_gen_, 0);  // orbit buffers sized by ensure_ring
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
   ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice,
                      s_gen_), "upload lanes");
@@ -296,6 +316,12 @@ void Engine::ensure_ring(uint64_t need) {
   cudaFree(ring_);
   ring_ = fresh;
   ring_bytes_ = want;
+  // orbit buffers for the longest launch gen_until will issue (a quarter of
+  // the ring), within the orbit budget: a small clip holds MBs, not 256 MB
+  const uint32_t cap = orbit_cap_iters(2 * n_);
+  const uint64_t launch = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+  const uint32_t iters = uint32_t(std::min<uint64_t>(launch, cap));
+  if (iters > pb_.max_iters) resize_orbit(pb_, 2 * n_, iters);
   for (auto& c : consumers_) ev_put(c.done);
   consumers_.clear();
   for (auto& g : gens_) ev_put(g.ev);
@@ -364,6 +390,7 @@ void Engine::gen_until(uint64_t end_byte) {
     uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
     if (gen_chunk_cap_) max_chunk = std::min(max_chunk, gen_chunk_cap_);
     chunk = std::min<uint64_t>({chunk, max_chunk, pb_.max_iters});
+    if (chunk == 0) raise(Errc::internal, "generator launch without orbit buffers");
     const int slot = int(launches_ & 1);
     // (1) chain on s_gen, once the verifier is done with this slot's buffers
     if (launches_ >= 2) ck(cudaStreamWaitEvent(s_gen_, ver_done_[slot], 0), "wait slot");
@@ -597,7 +624,7 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     configure_kernels_once(dev);
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    pb = alloc_prbg(2, s);
+    pb = alloc_prbg(2, s, orbit_cap_iters(2));
     ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
     ck(cudaMalloc(&d_out, ring), "cudaMalloc");
     ck(cudaMemcpyAsync(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice, s), "upload");
@@ -632,7 +659,7 @@ KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, int devi
     x0[2 * i + 1] = lanes[i].b.x0;
   }
   ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
-  pb_ = alloc_prbg(nl, s_);
+  pb_ = alloc_prbg(nl, s_, orbit_cap_iters(nl));
   ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
   ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice, s_),
      "upload");
