@@ -371,3 +371,31 @@ def test_every_frame_of_config_clips_vs_reference(name):
             for i in range(len(buf)):
                 assert sha(buf[i]) == g["cipher_sha256"][t + i], (name, t + i)
             t += len(buf)
+
+
+@pytest.mark.parametrize("side", [8, 16, 64, 512])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("r", [1, 5])
+def test_acceptance_grid_vs_oracle(side, n, r):
+    # the reference acceptance suite's round-trip grid (acceptance.cpp:97-384:
+    # sides {8,16,64,512} x workers {1,2,4,8} x rounds {1,5}), here also
+    # byte-compared with the oracle
+    key = synth.det_key(77 + side + n + r)
+    f = rand_frames(side, 1, side * 100 + n * 10 + r)[0]
+    a, b = f.copy(), f.copy()
+    assert Oracle(key, n, r).encrypt(a) == 0
+    cve.Cipher(key, n, r).encrypt_frame(b)
+    assert np.array_equal(a, b)
+    cve.Cipher(key, n, r).decrypt_frame(b)
+    assert np.array_equal(b, f)
+
+
+def test_workers_change_ciphertext():
+    # test_engine.cpp:189-195: n is a cipher parameter
+    key, f = synth.det_key(5), rand_frames(64, 1, 5)[0]
+    outs = []
+    for n in (1, 2, 4, 8):
+        x = f.copy()
+        cve.Cipher(key, n, 5).encrypt_frame(x)
+        outs.append(x.tobytes())
+    assert len(set(outs)) == 4
