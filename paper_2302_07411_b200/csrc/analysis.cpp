@@ -24,6 +24,7 @@
 #include <random>
 #include <unordered_set>
 
+#include "engine.hpp"
 #include "fileio.hpp"
 #include "keying.hpp"
 
@@ -323,6 +324,7 @@ HostFrame load_frame_any(const char* path, uint32_t frame_index) {
 
 std::string analyze(const HostFrame& frame, const HostFrame* second, uint32_t samples,
                     uint64_t seed, bool csv, int device) {
+  NvtxRange nvtx("cve: analyze");
   static const char* names[3] = {"R", "G", "B"};
   const std::vector<ChannelStats> st = all_stats(frame, second, samples, seed, device);
   std::string out;

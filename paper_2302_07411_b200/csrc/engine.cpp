@@ -1,5 +1,7 @@
 #include "engine.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <atomic>
@@ -99,6 +101,9 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
 namespace {
 std::atomic<int> g_streams{0};  // 0: not yet read from the environment
 }
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 void set_streams_per_handle(int n) {
   if (n != 1 && n != 2) raise(Errc::invalid_argument, "streams per handle must be 1 or 2");
@@ -302,6 +307,7 @@ void Engine::fold_timings(bool wait) {
 // Ring of >= 4 frames of keystream per worker, so the generator can run one
 // frame ahead while up to two frames are still being ciphered.
 void Engine::ensure_ring(uint64_t need) {
+  NvtxRange nvtx("cve: keystream ring grow");
   if (ring_bytes_ >= 4 * need) return;
   const uint64_t want = round_up(4 * need + 48 * 1024, 48 * 1024);
   synchronize();
@@ -381,6 +387,7 @@ const double* Engine::sine_for(uint32_t side) {
 // Enqueue generator launches on s_gen until stream byte `end_byte` (per
 // worker) is produced.  Launches cover whole 8-iteration (48-byte) blocks.
 void Engine::gen_until(uint64_t end_byte) {
+  NvtxRange nvtx("cve: generator launches");
   uint64_t target = round_up((end_byte + 5) / 6, 8);
   // never produce beyond what the ring can hold ahead of unassigned bytes
   const uint64_t cap = (cons_ + ring_bytes_) / 6 / 8 * 8;
@@ -443,6 +450,7 @@ cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
 
 void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
                            bool decrypt) {
+  NvtxRange nvtx("cve: frame");
   const uint64_t need = uint64_t(r_) * g.region;
   const uint64_t lo = cons_;
   cons_ += need;
@@ -489,6 +497,7 @@ void Engine::run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt) 
 }
 
 void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool decrypt) {
+  NvtxRange nvtx("cve: frames (host buffers)");
   draw_and_check(side, count);
   if (io.in_w > side || io.in_h > side || io.out_w > side || io.out_h > side ||
       !io.in_w || !io.in_h || !io.out_w || !io.out_h)
@@ -542,6 +551,7 @@ void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool d
 
 void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
                         bool decrypt, cudaStream_t user) {
+  NvtxRange nvtx("cve: frames (device-resident)");
   draw_and_check(side, count);
   const Geom g = geometry(side);
   ensure_ring(uint64_t(r_) * g.region);

@@ -33,6 +33,16 @@
 
 namespace cveb {
 
+// NVTX range for the host-side phases (enqueue of frames, generator
+// launches, ring growth, file pipelines).  NVTX v3 is header-only and a
+// no-op unless a profiler (Nsight Systems) injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct EngineStats {
   uint64_t frames = 0;
   uint64_t keystream_iters = 0;

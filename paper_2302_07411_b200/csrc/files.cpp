@@ -91,6 +91,7 @@ uint32_t batch_frames(uint64_t frame_bytes, uint32_t total) {
 
 void encrypt_file(const char* key_hex, const FileOptions& opt, const char* in_path,
                   const char* out_path, int device) {
+  NvtxRange nvtx("cve: encrypt_file");
   if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
   if (!in_path || !out_path) raise(Errc::invalid_argument, "path is null");
   if (opt.raw_width || opt.raw_height) {
@@ -149,6 +150,7 @@ void encrypt_file(const char* key_hex, const FileOptions& opt, const char* in_pa
 
 void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
                   const char* in_path, const char* out_path, int device) {
+  NvtxRange nvtx("cve: decrypt_file");
   if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
   if (!in_path || !out_path) raise(Errc::invalid_argument, "path is null");
   if (format < 0 || format > 2) raise(Errc::invalid_argument, "unknown output format");
@@ -205,6 +207,7 @@ void decrypt_file(const char* key_hex, const FileOptions* opt, int format,
 // copied back and written at each worker's file offset.
 void keystream_export(const char* key_hex, uint32_t workers, uint64_t byte_count,
                       const char* out_path, int device) {
+  NvtxRange nvtx("cve: nist_export");
   if (!key_hex) raise(Errc::invalid_argument, "key_hex is null");
   if (!out_path) raise(Errc::invalid_argument, "path is null");
   if (byte_count == 0) raise(Errc::invalid_argument, "byte_count must be >= 1");
