@@ -26,33 +26,50 @@ uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
 constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
 
-// Every upload / memset below is ordered on the stream that consumes it: the
-// synchronous cudaMemcpy / cudaMemset run on the legacy default stream, which
-// does not order against our non-blocking streams (a pageable H2D cudaMemcpy
-// may even return before its DMA lands).
 // Largest launch (iterations, multiple of 8) the orbit budget allows.
 uint32_t orbit_cap_iters(uint32_t nlanes) {
   const uint64_t iters = std::min<uint64_t>(kOrbitBytes / (8ull * nlanes), 1u << 20) / 8 * 8;
   return uint32_t(std::max<uint64_t>(iters, 8));
 }
 
+void free_prbg(PrbgBuffers& b) {
+  cudaFree(b.state);
+  cudaFree(b.verified_end);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(b.ckpt[k]);
+    cudaFree(b.orbit[k]);
+  }
+  cudaFree(b.bad);
+  cudaFree(b.replays);
+  b = PrbgBuffers{};
+}
+
+// Every upload / memset below is ordered on the stream that consumes it: the
+// synchronous cudaMemcpy / cudaMemset run on the legacy default stream, which
+// does not order against our non-blocking streams (a pageable H2D cudaMemcpy
+// may even return before its DMA lands).
 // orbit_iters = 0: no orbit buffers yet (an Engine sizes them from its ring,
 // resize_orbit); otherwise capacity for launches of orbit_iters iterations.
 PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
   PrbgBuffers b{};
-  b.max_iters = orbit_iters;
-  const size_t lanes_bytes = nlanes * sizeof(double);
-  ck(cudaMalloc(&b.state, lanes_bytes), "cudaMalloc state");
-  ck(cudaMalloc(&b.verified_end, lanes_bytes), "cudaMalloc state");
-  for (int k = 0; k < 2; ++k) {
-    ck(cudaMalloc(&b.ckpt[k], lanes_bytes), "cudaMalloc ckpt");
-    if (b.max_iters)
-      ck(cudaMalloc(&b.orbit[k], uint64_t(b.max_iters) * lanes_bytes), "cudaMalloc orbit");
+  try {
+    const size_t lanes_bytes = nlanes * sizeof(double);
+    ck(cudaMalloc(&b.state, lanes_bytes), "cudaMalloc state");
+    ck(cudaMalloc(&b.verified_end, lanes_bytes), "cudaMalloc state");
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaMalloc(&b.ckpt[k], lanes_bytes), "cudaMalloc ckpt");
+      if (orbit_iters)
+        ck(cudaMalloc(&b.orbit[k], uint64_t(orbit_iters) * lanes_bytes), "cudaMalloc orbit");
+    }
+    b.max_iters = orbit_iters;
+    ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
+    ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
+    ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
+    ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
+  } catch (...) {
+    free_prbg(b);
+    throw;
   }
-  ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
-  ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
-  ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
-  ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
   return b;
 }
 
@@ -69,32 +86,22 @@ void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
   b.max_iters = iters;
 }
 
-void free_prbg(PrbgBuffers& b) {
-  cudaFree(b.state);
-  cudaFree(b.verified_end);
-  for (int k = 0; k < 2; ++k) {
-    cudaFree(b.ckpt[k]);
-    cudaFree(b.orbit[k]);
-  }
-  cudaFree(b.bad);
-  cudaFree(b.replays);
-  b = PrbgBuffers{};
-}
-
 // x <- guard(x0) + 256 warm-up steps; the warm state is the first verified
 // end point.
 void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
                uint32_t nlanes, cudaStream_t s) {
-  double* d_x0 = nullptr;
-  ck(cudaMalloc(&d_x0, nlanes * sizeof(double)), "cudaMalloc x0");
-  ck(cudaMemcpyAsync(d_x0, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice, s),
+  struct Staging {  // freed on every path (cudaFree waits for the device)
+    double* p = nullptr;
+    ~Staging() { cudaFree(p); }
+  } x0d;
+  ck(cudaMalloc(&x0d.p, nlanes * sizeof(double)), "cudaMalloc x0");
+  ck(cudaMemcpyAsync(x0d.p, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice, s),
      "upload x0");
-  launch_prbg_init(b.state, d_lc, d_x0, nlanes, s);
+  launch_prbg_init(b.state, d_lc, x0d.p, nlanes, s);
   ck(cudaGetLastError(), "prbg_init launch");
   ck(cudaMemcpyAsync(b.verified_end, b.state, nlanes * sizeof(double),
                      cudaMemcpyDeviceToDevice, s), "copy state");
   ck(cudaStreamSynchronize(s), "prbg_init");
-  cudaFree(d_x0);
 }
 }  // namespace
 
@@ -156,6 +163,15 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   }
 
   one_stream_ = streams_per_handle() == 1;
+  try {
+    acquire(lanes);
+  } catch (...) {
+    release();  // the destructor does not run for a throwing constructor
+    throw;
+  }
+}
+
+void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
   ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -186,30 +202,55 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   ++st_.kernel_launches;
 }
 
-Engine::~Engine() {
+Engine::~Engine() { release(); }
+
+// Frees everything the engine holds; safe on a partially constructed engine
+// and idempotent.
+void Engine::release() noexcept {
   cudaSetDevice(dev_);
   for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamSynchronize(s);
   for (auto& c : consumers_) ev_put(c.done);
-  for (auto e : ver_done_) if (e) cudaEventDestroy(e);
-  for (auto e : chain_done_) if (e) cudaEventDestroy(e);
+  consumers_.clear();
+  for (auto& e : ver_done_) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+  for (auto& e : chain_done_) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
   for (auto& g : gens_) ev_put(g.ev);
+  gens_.clear();
   for (auto& t : timed_) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
+  timed_.clear();
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  ev_pool_.clear();
   for (cudaEvent_t e : tev_pool_) cudaEventDestroy(e);
+  tev_pool_.clear();
   for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
+  slot_free_.clear();
   for (uint8_t* p : slots_) cudaFree(p);
+  slots_.clear();
   for (auto& kv : sines_) cudaFree(kv.second);
-  for (uint8_t* p : scratch_) cudaFree(p);
+  sines_.clear();
+  for (uint8_t*& p : scratch_) {
+    cudaFree(p);
+    p = nullptr;
+  }
   cudaFree(d_shift_);
+  d_shift_ = nullptr;
   cudaFree(ring_);
+  ring_ = nullptr;
   free_prbg(pb_);
   cudaFree(d_lc_);
+  d_lc_ = nullptr;
   for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
+  s_gen_ = s_h2d_ = s_work_ = s_d2h_ = nullptr;
 }
 
 Geom Engine::geometry(uint32_t side) const {
@@ -668,21 +709,31 @@ KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, int devi
     x0[2 * i] = lanes[i].a.x0;
     x0[2 * i + 1] = lanes[i].b.x0;
   }
-  ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
-  pb_ = alloc_prbg(nl, s_, orbit_cap_iters(nl));
-  ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-  ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice, s_),
-     "upload");
-  init_prbg(pb_, d_lc_, x0.data(), nl, s_);
-  ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
+  try {
+    ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+    pb_ = alloc_prbg(nl, s_, orbit_cap_iters(nl));
+    ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
+    ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice, s_),
+       "upload");
+    init_prbg(pb_, d_lc_, x0.data(), nl, s_);
+    ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
+  } catch (...) {
+    release();
+    throw;
+  }
 }
 
-KeystreamSource::~KeystreamSource() {
+KeystreamSource::~KeystreamSource() { release(); }
+
+void KeystreamSource::release() noexcept {
   if (s_) cudaStreamSynchronize(s_);
   free_prbg(pb_);
   cudaFree(d_lc_);
+  d_lc_ = nullptr;
   cudaFree(d_buf_);
+  d_buf_ = nullptr;
   if (s_) cudaStreamDestroy(s_);
+  s_ = nullptr;
 }
 
 // Generates whole chunks of max_iters iterations; a request that does not

@@ -127,6 +127,8 @@ class Engine {
   void timed_begin(cudaStream_t s, bool chain, bool verify = false);
   void timed_end(cudaStream_t s);
   void fold_timings(bool wait);
+  void acquire(const std::vector<WorkerLanes>& lanes);  // constructor's CUDA resources
+  void release() noexcept;
 
   Key key_;
   uint32_t n_, r_;
@@ -184,6 +186,7 @@ class KeystreamSource {
   void next(uint8_t* host, uint64_t bytes);
 
  private:
+  void release() noexcept;
   uint32_t n_;
   PrbgBuffers pb_{};
   LaneConst* d_lc_ = nullptr;
