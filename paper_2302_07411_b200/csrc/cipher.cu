@@ -501,13 +501,18 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
     cp_async_commit();
   };
 
+  // Programmatic dependent launch: the next round may be scheduled as soon
+  // as SMs free up; it runs its independent prologue (first keystream tile,
+  // cluster arrive) and waits for this grid before touching the frame.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // cluster phase 1 (arrive now, wait before the DSMEM stores): every CTA of
   // the cluster has started before any remote store lands in it
   if (a.h > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  uint4 kv[3];
+  load_ks(tid, kv);  // first super-tile's keystream (independent of the frame)
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
   issue_stage(0);
   if (nstages > 1) issue_stage(1);
-  uint4 kv[3];
-  load_ks(tid, kv);  // first super-tile's keystream
   for (uint32_t t = tid; t < cr; t += kSlotThreads) {
     uint32_t c = t + uint32_t(a.shift[al0 + t]);
     cks[t] = c >= side ? c - side : c;
@@ -828,6 +833,10 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
 
   __shared__ uint32_t dlist[kDecDefer];  // rows deferred to the per-pixel pass
   __shared__ uint32_t dcount;
+  // programmatic dependent launch: hides the launch gap between rounds; the
+  // shift table and the frame are read only after the previous grid is done
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (uint32_t i = tid; i < side; i += kSlotThreads) sht[i] = a.shift[i];
   if (tid == 0) dcount = 0;
   __syncthreads();
@@ -1245,6 +1254,13 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    cudaLaunchAttribute attr2[2] = {attr[0], {}};
+    if (!std::getenv("CVE_B200_NO_PDL")) {  // experiments only
+      attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr2[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr2;
+      cfg.numAttrs = 2;
+    }
     cudaLaunchKernelEx(&cfg, k_encrypt_round_slots, a);
     check_launch("encrypt_round_slots");
     ++*launches;
@@ -1331,7 +1347,17 @@ void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
   if (Ts) {
     DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
               Ts, g.region, make_div(Ts), make_div(g.rows), g.frame_bytes};
-    k_decrypt_round_slots<<<(g.side + Ts - 1) / Ts, kSlotThreads, smem, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((g.side + Ts - 1) / Ts);
+    cfg.blockDim = dim3(kSlotThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 0 : 1;  // experiments only
+    cudaLaunchKernelEx(&cfg, k_decrypt_round_slots, a);
     check_launch("decrypt_round_slots");
     ++*launches;
     return;
