@@ -160,3 +160,31 @@ def test_analysis_and_tool_argument_checks():
     assert L.cve_crop_file(b"i", b"o", None, 2) == cve.CVE_ERROR_INVALID_ARGUMENT
     assert L.cve_frame_stats_device(None, None, 8, None, None, None) == \
         cve.CVE_ERROR_INVALID_ARGUMENT
+
+
+def _build_c_demo(tmp_path):
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    exe = str(tmp_path / "c_abi_demo")
+    libdir = os.path.dirname(cve.lib_path)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror",
+                    "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c_abi_demo.c"), "-o", exe,
+                    "-L", libdir, "-lcve_b200", "-Wl,-rpath," + libdir],
+                   check=True, capture_output=True)
+    return exe
+
+
+def test_c_caller_compiles_links_and_runs(tmp_path):
+    # the header is plain C99 and a C program links the library the way a
+    # reference caller links libcve.so; without a GPU it fails cleanly
+    import subprocess
+    exe = _build_c_demo(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    if gpu_present():
+        assert out.stdout.startswith("ok "), out.stdout
+    else:
+        assert out.stdout.strip() == f"nogpu {cve.CVE_ERROR_INTERNAL}", out.stdout

@@ -399,3 +399,28 @@ def test_workers_change_ciphertext():
         cve.Cipher(key, n, 5).encrypt_frame(x)
         outs.append(x.tobytes())
     assert len(set(outs)) == 4
+
+
+def test_c_caller_matches_oracle(tmp_path):
+    # tests/c_abi_demo.c: a C99 program linked against the library the way a
+    # reference caller links libcve.so; its ciphertext digest against the oracle
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe, libdir = str(tmp_path / "c_abi_demo"), os.path.dirname(cve.lib_path)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "c_abi_demo.c"), "-o", exe, "-L", libdir,
+                    "-lcve_b200", "-Wl,-rpath," + libdir], check=True, capture_output=True)
+    out = subprocess.run([exe, PLCM], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    side, n = 96, 96 * 96 * 3
+    f = np.array([((i * 2654435761) >> 24) & 0xFF for i in range(n)], np.uint8)
+    f = f.reshape(side, side, 3)
+    assert Oracle(PLCM, 8, 5).encrypt(f) == 0
+    x = 0
+    for i, b in enumerate(f.ravel().tolist()):
+        x ^= b << (8 * (i & 3))
+    assert out.stdout.split()[:2] == ["ok", f"{x:08x}"], out.stdout
+    assert "seeds=1" in out.stdout
