@@ -188,3 +188,28 @@ def test_c_caller_compiles_links_and_runs(tmp_path):
         assert out.stdout.startswith("ok "), out.stdout
     else:
         assert out.stdout.strip() == f"nogpu {cve.CVE_ERROR_INTERNAL}", out.stdout
+
+
+REF_HEADER = "/root/reference/proj/include/cve.h"
+
+
+@pytest.mark.skipif(not os.path.exists(REF_HEADER), reason="reference headers not present")
+def test_c_caller_built_against_the_reference_header(tmp_path):
+    # drop-in at the source level: the same C program compiled against the
+    # REFERENCE's own cve.h (a shim named cve_b200.h includes it) links and
+    # runs against libcve_b200.so -- names, types and struct layouts agree
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    shim = tmp_path / "inc"
+    shim.mkdir()
+    (shim / "cve_b200.h").write_text(f'#include "{REF_HEADER}"\n')
+    exe, libdir = str(tmp_path / "demo_ref_hdr"), os.path.dirname(cve.lib_path)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", str(shim),
+                    os.path.join(ROOT, "tests", "c_abi_demo.c"), "-o", exe, "-L", libdir,
+                    "-lcve_b200", "-Wl,-rpath," + libdir], check=True, capture_output=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("ok ") if gpu_present() else \
+        out.stdout.strip() == f"nogpu {cve.CVE_ERROR_INTERNAL}"
