@@ -171,6 +171,25 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def baseline_roofline(side: int, hbm_gbs: float) -> dict:
+    """BASELINE.json's roofline per frame: the slower of the frame's HBM
+    bytes (2F) at peak and the PRBG's FP64 ops at the measured FP64 peak
+    (3 ops per lane-iteration in the reference formulation, r * side^2
+    lane-iterations per frame)."""
+    F = side * side * 3
+    hbm_us = 2 * F / (hbm_gbs * 1e9) * 1e6
+    out = {"hbm_us": hbm_us}
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            tf = float(json.load(fh)["fp64_tflops"])
+        fp64_us = 3 * synth.ROUNDS * side * side / (tf * 1e12) * 1e6
+        out.update({"fp64_us": fp64_us, "fp64_tflops_measured": tf,
+                    "bound_us": max(hbm_us, fp64_us)})
+    except (OSError, KeyError, ValueError):
+        out["bound_us"] = hbm_us
+    return out
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -615,6 +634,7 @@ def run_b200(args) -> None:
             "frac": chain_gbs / hbm if chain_gbs else None, "peak_source": hbm_src,
             "traffic": traffic_per_launch,
             "algorithmic_bytes_per_launch": alg_per_launch,
+            "baseline_roofline_us_per_frame": baseline_roofline(side, hbm),
             "note": "BASELINE.json roofline: 2*side^2*3 B per frame (SURVEY 8(d)) at peak "
                     "HBM; the kernel is bound by the FP64 dependency latency of 2n "
                     "sequential orbits instead (see 'chain')"},
