@@ -642,10 +642,10 @@ def run_b200(args) -> None:
             "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
             "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
             "cycles_per_iteration": ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3,
-            # ptxas stall counts of the unrolled loop (tools/iter_cycles.py on
-            # build/csrc/prbg.o): 7 x 42 + 47 (back-edge) per 8 iterations
-            "static_schedule_cycles": 42.625,
-            "frac_of_static_schedule": 42.625 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
+            # ptxas stall counts of the unrolled loop body (SASS control
+            # bits, tools/iter_cycles.py): 326 cycles per 8 iterations
+            "static_schedule_cycles": 40.75,
+            "frac_of_static_schedule": 40.75 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
             "launches": int(len(chain_times)),
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,

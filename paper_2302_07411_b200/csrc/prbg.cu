@@ -30,8 +30,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -87,8 +87,19 @@ __device__ __forceinline__ double plcm_exact(double x, double p, double q) {
 // DADD -> DADD -> DFMA -> FSEL (case D).  Static schedule: 42 cycles per
 // iteration (tools/iter_cycles.py; other formulations tried scored 44-57,
 // tools/chain_search.py).
+// The predicates are integer compares of the bit patterns (x >= 0, so the
+// signed 64-bit order is the double order), which keeps 3 of the 14 FP64
+// instructions off the FP64 pipe: 26.2 -> 25.4 ns/iteration
+// (tools/chain_ops.cu, variant C).  fold tests x >= 0.5 on the high word:
+// it differs from x > 0.5 only at x == 0.5, a guard value whose step the
+// verifier always re-decides exactly.
+__device__ __forceinline__ bool bits_gt(double u, double v) {
+  return __double_as_longlong(u) > __double_as_longlong(v);
+}
+
 __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
-  const bool a = x < c.p, cc = x > c.cthr, fold = x > 0.5;
+  const bool a = bits_gt(c.p, x), cc = bits_gt(x, c.cthr);
+  const bool fold = __double2hiint(x) >= 0x3FE00000;
   const double t1 = __dsub_rn(1.0, x);  // exact when x > 0.5
   const double nb = __dsub_rn(x, c.p);
   const double nd = __dsub_rn(t1, c.p);
@@ -304,19 +315,29 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
                                                                     x0, nlanes);
 }
 
-constexpr int kChainReserve = 160 * 1024;
+// The chain CTA reserves all of an SM's shared memory, so no other CTA (not
+// even the shared-memory-free verifier) is co-resident and steals issue slots
+// from the 4 chain warps: 160 -> 227 KB gave 268 -> 270 frames/s at C4 and
+// 5.66k -> 5.71k frames/s for 32 clips.
+int chain_reserve() {
+  static const int v = [] {
+    int kb = 227;
+    if (const char* e = std::getenv("CVE_B200_CHAIN_RESERVE_KB")) kb = std::atoi(e);  // experiments only
+    return std::min(std::max(kb, 1), 227) * 1024;
+  }();
+  return v;
+}
 
 void configure_prbg_kernels() {
   cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kChainReserve);
+                       chain_reserve());
 }
 
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
                        uint32_t iters, uint32_t nlanes, cudaStream_t s) {
-  // 128 threads/CTA, one CTA per SM (the dynamic shared memory request only
-  // enforces SM exclusivity, which also keeps smem-heavy cipher CTAs off the
-  // chain's SMs).
-  k_prbg_chain<<<(nlanes + 127) / 128, 128, kChainReserve, s>>>(
+  // 128 threads/CTA, one CTA per SM; the dynamic shared memory request only
+  // enforces SM exclusivity (chain_reserve).
+  k_prbg_chain<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
       b.state, b.ckpt[slot], lc, b.orbit[slot], iters, nlanes);
 }
 
