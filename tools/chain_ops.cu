@@ -17,11 +17,18 @@
 //   J  C as predicated assignments: y = yb; if (a) y = ya; if (fold) y = yd;
 //      if (cc) y = yc
 //   N  C unrolled by 16
+//   K  C with each orbit store as `asm volatile` st.global.f64 (not sunk)
+//   L  C with __stcg stores
+//   U4, U2  C unrolled by 4 / 2
 // Prints ns/iteration and checks every variant's orbit against A's.
-// Measured (B200, 1965 MHz, 128 lanes x 2^18 iterations): A 26.22, B 25.65,
-// C 25.45, D 31.89, E 31.95, F 28.83, G 28.77 ns/iteration.  C is the product
-// step since r01h; selecting case D last (F, G) or sharing corrections (D, E)
-// lengthens the path the hardware actually sees.
+// Measured (B200, 1965 MHz, 128 lanes x 2^18 iterations), ns/iteration:
+//   A 26.18  B 25.61  C 25.36  D 31.85  E 31.91  F 28.79  G 28.67  H 28.72
+//   J 28.67  N 25.29  K 25.36  L 25.35  U4 28.02  U2 25.67
+// C is the product step since r01h (N's gain reverses inside the product).
+// Selecting case D last (F, G) or sharing corrections (D, E) lengthens the
+// path the hardware actually sees; the store form (K, L) does not matter;
+// the 2 IMAD.MOV per 8 steps come from the halves of a predicated select
+// landing in unpaired registers and survive every unroll factor.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false tools/chain_ops.cu -o tools/chain_ops
 #include <cmath>
 #include <cstdint>
@@ -93,8 +100,8 @@ __device__ __forceinline__ double step(double x, const LaneConst& c) {
 template <int V>
 __global__ void __launch_bounds__(128, 1)
     k(double* state, const LaneConst* lcs, double* orbit, uint32_t iters, uint32_t nl) {
-  constexpr int S = V == 9 ? 2 : V;  // N: the C step
-  constexpr int U = V == 9 ? 16 : 8;
+  constexpr int S = V >= 9 ? 2 : V;  // N, K, L: the C step
+  constexpr int U = V == 9 ? 16 : V == 12 ? 4 : V == 13 ? 2 : 8;
   const uint32_t l = threadIdx.x;
   const LaneConst c = lcs[l];
   double x = state[l];
@@ -103,7 +110,12 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int t = 0; t < U; ++t) {
       x = step<S>(x, c);
-      o[size_t(t) * nl] = x;
+      if (V == 10)
+        asm volatile("st.global.f64 [%0], %1;" ::"l"(o + size_t(t) * nl), "d"(x) : "memory");
+      else if (V == 11)
+        __stcg(o + size_t(t) * nl, x);
+      else
+        o[size_t(t) * nl] = x;
     }
     o += size_t(U) * nl;
   }
@@ -148,13 +160,15 @@ int main() {
   cudaEventCreate(&b);
   void (*ks[])(double*, const LaneConst*, double*, uint32_t, uint32_t) = {k<0>, k<1>, k<2>,
                                                                          k<3>, k<4>, k<5>, k<6>,
-                                                                         k<7>, k<8>, k<9>};
+                                                                         k<7>, k<8>, k<9>, k<10>, k<11>, k<12>, k<13>};
   const char* names[] = {"A product (14 FP64)", "B fold from hi word", "C integer predicates",
                          "D shared corrections", "E C + D",
                          "F C, case D selected last", "G F with LOP3 bit-select",
-                         "H C, cc-first select", "J C, predicated assigns", "N C, unroll 16"};
+                         "H C, cc-first select", "J C, predicated assigns", "N C, unroll 16",
+                         "K C, asm volatile stores", "L C, __stcg stores",
+                         "U4 C, unroll 4", "U2 C, unroll 2"};
   std::vector<double> ref(size_t(iters) * T), got(size_t(iters) * T);
-  for (int m = 0; m < 10; ++m) {
+  for (int m = 0; m < 14; ++m) {
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemcpy(dx, x0.data(), T * 8, cudaMemcpyHostToDevice);
