@@ -10,10 +10,10 @@
  * pipelined and device-resident variants the synchronous per-frame call
  * cannot express.
  *
- * Only PLCM keys (tag 0x00, 66 hex chars) drive the GPU engine.  LASM keys
- * validate (cve_key_validate) but cve_cipher_create rejects them with
- * CVE_ERROR_INVALID_ARGUMENT: the LASM map needs a glibc-exact device sin
- * and is out of this round's scope.
+ * Both key maps drive the GPU engine: PLCM keys (tag 0x00, 66 hex chars) and
+ * LASM keys (tag 0x01, 50 hex chars; the LASM generator evaluates glibc's
+ * own sin algorithm on the device, glibc_sin.cuh, so its keystream is the
+ * reference's bit for bit on a glibc 2.39 host).
  *
  * Threading matches the reference (cve.h:5-6): one handle is driven by one
  * thread at a time; distinct handles are independent.  All calls are
@@ -286,10 +286,10 @@ CVE_B200_API cve_status cve_cipher_prefetch_keystream(cve_cipher* cipher,
 /* Profiling counters of the handle (cumulative since create). */
 typedef struct cve_cipher_stats {
   uint64_t frames;           /* frames completed (encrypt + decrypt) */
-  uint64_t keystream_iters;  /* PLCM iterations generated per lane */
+  uint64_t keystream_iters;  /* generator iterations per lane (6 B PLCM, 12 B LASM) */
   uint64_t kernel_launches;  /* CUDA kernels launched by this handle */
   uint64_t prbg_launches;    /* of which keystream-generator launches */
-  uint64_t guard_replays;    /* 8-iteration blocks replayed exactly */
+  uint64_t guard_replays;    /* PLCM workers recomputed exactly (0 for LASM) */
   double prbg_ms;            /* device time of generator launches */
   double chain_ms;           /* of which the sequential chain kernel */
   double cipher_ms;          /* device time of cipher-round launches */
@@ -308,12 +308,25 @@ CVE_B200_API cve_status cve_cipher_get_stats(cve_cipher* cipher,
 CVE_B200_API cve_status cve_keystream_generate(const double lanes[4],
                                                uint8_t* out, size_t len);
 
+/* LASM counterpart (row f2): lanes {x0_a, y0_a, mu_a, x0_b, y0_b, mu_b}, the
+ * reference's Prbg(LasmParams, LasmParams).take(len) (chaos.cpp:93-107,
+ * 119-153: 12 bytes per iteration).  Out-of-domain lanes -> BAD_KEY. */
+CVE_B200_API cve_status cve_keystream_generate_lasm(const double lanes[6],
+                                                    uint8_t* out, size_t len);
+
+/* Diagnostics for row f2: y[i] = sin(x[i]) evaluated on the GPU by the
+ * restatement of the host glibc's libm sin the LASM generator uses
+ * (glibc_sin.cuh); bit-identical to the host's sin() for |x| < 105414350,
+ * NaN beyond. */
+CVE_B200_API cve_status cve_glibc_sin(const double* x, double* y, size_t count);
+
 /* Host-only keying (no GPU needed): the lane table the key's coordinator
- * derives for `workers` subframes -- lanes_out[4*i .. 4*i+3] = x0_a, p_a,
- * x0_b, p_b of subframe i (reference keying.cpp:180-207) -- followed by the
- * first `nseeds` per-frame confusion seeds (keying.cpp:209-218).  PLCM keys
- * only.  For key management and diagnostics; the cipher handle does the same
- * derivation internally. */
+ * derives for `workers` subframes (reference keying.cpp:180-207) -- for PLCM
+ * keys lanes_out[4*i .. 4*i+3] = x0_a, p_a, x0_b, p_b of subframe i, for LASM
+ * keys lanes_out[6*i .. 6*i+5] = x0_a, y0_a, mu_a, x0_b, y0_b, mu_b --
+ * followed by the first `nseeds` per-frame confusion seeds
+ * (keying.cpp:209-218).  For key management and diagnostics; the cipher
+ * handle does the same derivation internally. */
 CVE_B200_API cve_status cve_derive_worker_lanes(const char* key_hex,
                                                 uint32_t workers,
                                                 double* lanes_out,

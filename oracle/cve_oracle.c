@@ -9,14 +9,16 @@
  *
  * Parity pin: tests/test_oracle.py checks this file against (a) the golden
  * constants of the reference's own unit tests (test_chaos.cpp:96-109,
- * test_keying.cpp:160-179, test_engine.cpp:61-70/117-120) and (b) the
+ * test_keying.cpp:160-179, test_engine.cpp:61-70/117-120; LASM:
+ * test_chaos.cpp:36-45/111-123, test_keying.cpp:181-195) and (b) the
  * compiled reference itself (oracle/_ref/libcve_ref.so, built from the
  * reference sources in place by oracle/Makefile) on whole frames.
  *
  * Every function cites the reference file:line whose behaviour it restates
  * (paths relative to /root/reference/proj).  Arithmetic is IEEE binary64 with
  * FP contraction off (see Makefile: -ffp-contract=off), like the reference's
- * x86-64 Release build (no -march, so no FMA).
+ * x86-64 Release build (no -march, so no FMA).  The LASM map calls the host
+ * libm `sin`, exactly as the reference does (chaos.cpp:34-38).
  */
 #include <math.h>
 #include <stdint.h>
@@ -50,12 +52,30 @@ double orc_plcm_iterate(double x, double p) {
   return orc_plcm_guard(orc_plcm_step(x, p), p);
 }
 
-/* Two-lane byte generator, src/chaos.cpp:79-91 (ctor), 109-117 (step_lane),
- * 119-141 (refill), 143-153 (fill), 46-56 (extract_bytes). */
+/* src/chaos.cpp:34-38 (std::numbers::pi, evaluated left to right, glibc sin) */
+static void orc_lasm_step(double* x, double* y, double mu) {
+  const double pi = 3.14159265358979323846;
+  double xn = sin(pi * mu * (*y + 3.0) * *x * (1.0 - *x));
+  double yn = sin(pi * mu * (xn + 3.0) * *y * (1.0 - *y));
+  *x = xn;
+  *y = yn;
+}
+
+/* src/chaos.cpp:40-44 */
+static int orc_lasm_mu_valid(double mu) {
+  return (mu >= 0.37 && mu <= 0.38) || (mu >= 0.40 && mu <= 0.42) ||
+         (mu >= 0.44 && mu <= 0.93) || mu == 1.0;
+}
+
+/* Two-lane byte generator, src/chaos.cpp:79-107 (ctors), 109-117 (step_lane),
+ * 119-141 (refill: 6 bytes per PLCM iteration, 12 per LASM iteration, x bytes
+ * then y bytes), 143-153 (fill), 46-56 (extract_bytes).  Lane q = p (PLCM) or
+ * mu (LASM). */
 typedef struct {
-  double xa, pa, xb, pb;
-  uint8_t buf[6];
-  int pos; /* 6 == empty */
+  int lasm;
+  double xa, ya, qa, xb, yb, qb;
+  uint8_t buf[12];
+  int pos, len; /* pos == len: empty */
   uint64_t emitted;
 } orc_prbg;
 
@@ -65,29 +85,54 @@ static int orc_plcm_valid(double x0, double p) { /* src/chaos.cpp:58-65 */
   return 1;
 }
 
+static int orc_lasm_valid(double x0, double y0, double mu) { /* src/chaos.cpp:67-77 */
+  if (!(isfinite(x0) && x0 >= 0.0 && x0 <= 1.0)) return 0;
+  if (!(isfinite(y0) && y0 >= 0.0 && y0 <= 1.0)) return 0;
+  return isfinite(mu) && orc_lasm_mu_valid(mu);
+}
+
+static void orc_step_lanes(orc_prbg* g) { /* src/chaos.cpp:109-117 */
+  if (g->lasm) {
+    orc_lasm_step(&g->xa, &g->ya, g->qa);
+    orc_lasm_step(&g->xb, &g->yb, g->qb);
+  } else {
+    g->xa = orc_plcm_iterate(g->xa, g->qa);
+    g->xb = orc_plcm_iterate(g->xb, g->qb);
+  }
+}
+
 static void orc_prbg_init(orc_prbg* g, double xa, double pa, double xb,
                           double pb) {
-  g->pa = pa;
-  g->pb = pb;
+  memset(g, 0, sizeof *g);
+  g->qa = pa;
+  g->qb = pb;
   g->xa = orc_plcm_guard(xa, pa);
   g->xb = orc_plcm_guard(xb, pb);
-  for (int i = 0; i < 256; ++i) { /* kWarmupSteps, chaos.hpp:14 */
-    g->xa = orc_plcm_iterate(g->xa, g->pa);
-    g->xb = orc_plcm_iterate(g->xb, g->pb);
-  }
-  g->pos = 6;
-  g->emitted = 0;
+  for (int i = 0; i < 256; ++i) orc_step_lanes(g); /* kWarmupSteps, chaos.hpp:14 */
+}
+
+static void orc_lasm_init(orc_prbg* g, const double a[3], const double b[3]) {
+  memset(g, 0, sizeof *g); /* src/chaos.cpp:93-107: no guard */
+  g->lasm = 1;
+  g->xa = a[0], g->ya = a[1], g->qa = a[2];
+  g->xb = b[0], g->yb = b[1], g->qb = b[2];
+  for (int i = 0; i < 256; ++i) orc_step_lanes(g);
+}
+
+static void orc_xor48(uint8_t* out, double a, double b) {
+  uint64_t ua, ub;
+  memcpy(&ua, &a, 8);
+  memcpy(&ub, &b, 8);
+  for (int k = 0; k < 6; ++k) out[k] = (uint8_t)((ua ^ ub) >> (8 * k));
 }
 
 static void orc_prbg_fill(orc_prbg* g, uint8_t* out, size_t n) {
   for (size_t i = 0; i < n; ++i) {
-    if (g->pos == 6) {
-      uint64_t a, b;
-      g->xa = orc_plcm_iterate(g->xa, g->pa);
-      g->xb = orc_plcm_iterate(g->xb, g->pb);
-      memcpy(&a, &g->xa, 8);
-      memcpy(&b, &g->xb, 8);
-      for (int k = 0; k < 6; ++k) g->buf[k] = (uint8_t)((a ^ b) >> (8 * k));
+    if (g->pos == g->len) {
+      orc_step_lanes(g);
+      orc_xor48(g->buf, g->xa, g->xb);
+      if (g->lasm) orc_xor48(g->buf + 6, g->ya, g->yb);
+      g->len = g->lasm ? 12 : 6;
       g->pos = 0;
     }
     out[i] = g->buf[g->pos++];
@@ -105,6 +150,20 @@ int orc_plcm_stream(double xa, double pa, double xb, double pb, uint8_t* out,
   return ORC_OK;
 }
 
+/* lanes = {x0a, y0a, mua, x0b, y0b, mub} */
+int orc_lasm_stream(const double lanes[6], uint8_t* out, size_t n) {
+  orc_prbg g;
+  if (!orc_lasm_valid(lanes[0], lanes[1], lanes[2]) ||
+      !orc_lasm_valid(lanes[3], lanes[4], lanes[5]))
+    return ORC_BAD_KEY;
+  orc_lasm_init(&g, lanes, lanes + 3);
+  orc_prbg_fill(&g, out, n);
+  return ORC_OK;
+}
+
+/* One LASM iteration (x, y) -> (x', y'), for the frozen examples. */
+void orc_lasm_iterate(double* x, double* y, double mu) { orc_lasm_step(x, y, mu); }
+
 /* ---- L1: key + coordinator -------------------------------------------- */
 
 static int orc_nibble(char c) {
@@ -114,28 +173,49 @@ static int orc_nibble(char c) {
   return -1;
 }
 
-/* src/keying.cpp:77-107 (PLCM branch only; LASM is out of scope) */
-int orc_parse_plcm_key(const char* hex, double lanes[4]) {
+/* src/keying.cpp:77-107.  Returns the map kind in *lasm; PLCM keys fill
+ * k[0..3] = {x0a, pa, x0b, pb}, LASM keys k[0..2] = {x0, y0, mu}. */
+int orc_parse_key(const char* hex, double k[4], int* lasm) {
   size_t len = strlen(hex);
   uint8_t bytes[33];
   while (len > 0 && (hex[len - 1] == '\n' || hex[len - 1] == '\r' ||
                      hex[len - 1] == ' ' || hex[len - 1] == '\t'))
     --len;
-  if (len != 66) return ORC_BAD_KEY;
-  for (size_t i = 0; i < 33; ++i) {
+  if (len != 66 && len != 50) return ORC_BAD_KEY;
+  for (size_t i = 0; i < len / 2; ++i) {
     int hi = orc_nibble(hex[2 * i]), lo = orc_nibble(hex[2 * i + 1]);
     if (hi < 0 || lo < 0) return ORC_BAD_KEY;
     bytes[i] = (uint8_t)(hi << 4 | lo);
   }
-  if (bytes[0] != 0x00) return ORC_BAD_KEY;
-  for (int k = 0; k < 4; ++k) {
-    uint64_t bits = 0;
-    for (int i = 0; i < 8; ++i) bits |= (uint64_t)bytes[1 + 8 * k + i] << (8 * i);
-    memcpy(&lanes[k], &bits, 8);
+  if (bytes[0] == 0x00 && len == 66) {
+    *lasm = 0;
+  } else if (bytes[0] == 0x01 && len == 50) {
+    *lasm = 1;
+  } else {
+    return ORC_BAD_KEY; /* unknown tag, or a tag with the other map's length */
   }
-  if (!orc_plcm_valid(lanes[0], lanes[1]) || !orc_plcm_valid(lanes[2], lanes[3]))
+  for (int j = 0; j < (*lasm ? 3 : 4); ++j) {
+    uint64_t bits = 0;
+    for (int i = 0; i < 8; ++i) bits |= (uint64_t)bytes[1 + 8 * j + i] << (8 * i);
+    memcpy(&k[j], &bits, 8);
+  }
+  if (*lasm ? !orc_lasm_valid(k[0], k[1], k[2])
+            : (!orc_plcm_valid(k[0], k[1]) || !orc_plcm_valid(k[2], k[3])))
     return ORC_BAD_KEY;
   return ORC_OK;
+}
+
+int orc_parse_plcm_key(const char* hex, double lanes[4]) {
+  int lasm = 0;
+  int st = orc_parse_key(hex, lanes, &lasm);
+  return st ? st : (lasm ? ORC_BAD_KEY : ORC_OK);
+}
+
+/* src/keying.cpp:67-73 */
+static double orc_rotate_half(double v) {
+  v += 0.5;
+  if (v >= 1.0) v -= 1.0;
+  return v;
 }
 
 /* src/keying.cpp:61-65 */
@@ -180,9 +260,10 @@ int64_t orc_confusion_shift(uint32_t alpha, uint32_t side, uint32_t seed) {
 
 typedef struct {
   uint32_t n, r;
+  int lasm;
   orc_prbg coord;
   orc_prbg* workers;
-  double* params; /* n x (x0a, pa, x0b, pb) as derived */
+  double* params; /* PLCM: n x (x0a, pa, x0b, pb); LASM: n x (x0a, y0a, mua, x0b, y0b, mub) */
   uint64_t seeds;
 } orc_cipher;
 
@@ -190,28 +271,45 @@ typedef struct {
 int orc_cipher_create(const char* key_hex, uint32_t n, uint32_t r,
                       orc_cipher** out) {
   double k[4];
-  int st;
+  int st, lasm = 0;
   if (!key_hex || !out) return ORC_INVALID;
-  st = orc_parse_plcm_key(key_hex, k);
+  st = orc_parse_key(key_hex, k, &lasm);
   if (st) return st;
   if (n == 0 || r == 0 || r > 255) return ORC_INVALID;
   orc_cipher* c = (orc_cipher*)calloc(1, sizeof *c);
+  const size_t per = lasm ? 6 : 4;
   c->n = n;
   c->r = r;
-  orc_prbg_init(&c->coord, k[0], k[1], k[2], k[3]);
+  c->lasm = lasm;
+  if (lasm) { /* keying.cpp:164-170: lane b = key rotated by one half */
+    double b[3] = {orc_rotate_half(k[0]), orc_rotate_half(k[1]), k[2]};
+    orc_lasm_init(&c->coord, k, b);
+  } else {
+    orc_prbg_init(&c->coord, k[0], k[1], k[2], k[3]);
+  }
   c->workers = (orc_prbg*)calloc(n, sizeof(orc_prbg));
-  c->params = (double*)calloc((size_t)n * 4, sizeof(double));
-  for (uint32_t i = 0; i < n; ++i) {
-    double* q = c->params + 4 * (size_t)i;
+  c->params = (double*)calloc((size_t)n * per, sizeof(double));
+  for (uint32_t i = 0; i < n; ++i) { /* keying.cpp:180-207 */
+    double* q = c->params + per * (size_t)i;
     for (int lane = 0; lane < 2; ++lane) {
-      q[2 * lane + 0] = orc_clamp_inside(orc_next_unit(&c->coord), 0.0, 1.0);
-      q[2 * lane + 1] =
-          orc_clamp_inside(orc_next_unit(&c->coord) * 0.5, 0.0, 0.5);
+      if (lasm) {
+        q[3 * lane + 0] = orc_clamp_inside(orc_next_unit(&c->coord), 0.0, 1.0);
+        q[3 * lane + 1] = orc_clamp_inside(orc_next_unit(&c->coord), 0.0, 1.0);
+        q[3 * lane + 2] = orc_clamp_inside(
+            0.44 + orc_next_unit(&c->coord) * (0.93 - 0.44), 0.44, 0.93);
+      } else {
+        q[2 * lane + 0] = orc_clamp_inside(orc_next_unit(&c->coord), 0.0, 1.0);
+        q[2 * lane + 1] =
+            orc_clamp_inside(orc_next_unit(&c->coord) * 0.5, 0.0, 0.5);
+      }
     }
   }
   for (uint32_t i = 0; i < n; ++i) {
-    double* q = c->params + 4 * (size_t)i;
-    orc_prbg_init(&c->workers[i], q[0], q[1], q[2], q[3]);
+    double* q = c->params + per * (size_t)i;
+    if (lasm)
+      orc_lasm_init(&c->workers[i], q, q + 3);
+    else
+      orc_prbg_init(&c->workers[i], q[0], q[1], q[2], q[3]);
   }
   *out = c;
   return ORC_OK;
@@ -227,6 +325,8 @@ void orc_cipher_destroy(orc_cipher* c) {
 uint64_t orc_cipher_seeds_drawn(const orc_cipher* c) { return c->seeds; }
 
 const double* orc_cipher_params(const orc_cipher* c) { return c->params; }
+
+int orc_cipher_is_lasm(const orc_cipher* c) { return c->lasm; }
 
 /* Draw `len` more keystream bytes of worker i (for PRBG kernel parity). */
 void orc_cipher_worker_stream(orc_cipher* c, uint32_t i, uint8_t* out,

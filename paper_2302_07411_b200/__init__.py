@@ -118,6 +118,8 @@ def _load() -> C.CDLL:
         "cve_cipher_decrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32,
                                                    C.c_uint32, vp]),
         "cve_keystream_generate": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
+        "cve_keystream_generate_lasm": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
+        "cve_glibc_sin": (C.c_int, [vp, vp, C.c_size_t]),
         "cve_derive_worker_lanes": (C.c_int, [C.c_char_p, C.c_uint32,
                                               C.POINTER(C.c_double),
                                               C.POINTER(C.c_uint32), C.c_size_t]),
@@ -157,10 +159,12 @@ def key_generate(kind: int = CVE_MAP_PLCM) -> str:
 
 def derive_worker_lanes(key_hex, workers: int, seeds: int = 0
                         ) -> Tuple[np.ndarray, np.ndarray]:
-    """Host keying only (no GPU): the (workers, 4) lane table
-    (x0_a, p_a, x0_b, p_b) the coordinator derives, then `seeds` confusion
-    seeds (reference keying.cpp:164-218)."""
-    lanes = np.zeros((workers, 4), dtype=np.float64)
+    """Host keying only (no GPU): the lane table the coordinator derives --
+    (workers, 4) = (x0_a, p_a, x0_b, p_b) for PLCM keys, (workers, 6) =
+    (x0_a, y0_a, mu_a, x0_b, y0_b, mu_b) for LASM keys -- then `seeds`
+    confusion seeds (reference keying.cpp:164-218)."""
+    per = 6 if key_validate(key_hex) == CVE_MAP_LASM else 4
+    lanes = np.zeros((workers, per), dtype=np.float64)
     out = np.zeros(max(seeds, 1), dtype=np.uint32)
     _check(lib.cve_derive_worker_lanes(
         _as_key(key_hex), workers, lanes.ctypes.data_as(C.POINTER(C.c_double)),
@@ -174,6 +178,24 @@ def keystream_generate(lanes, length: int) -> np.ndarray:
     out = np.zeros(length, dtype=np.uint8)
     _check(lib.cve_keystream_generate(lan, out.ctypes.data, length))
     return out
+
+
+def keystream_generate_lasm(lanes, length: int) -> np.ndarray:
+    """GPU keystream of one LASM generator with explicit lanes
+    (x0_a, y0_a, mu_a, x0_b, y0_b, mu_b): 12 bytes per iteration."""
+    lan = (C.c_double * 6)(*[float(v) for v in lanes])
+    out = np.zeros(length, dtype=np.uint8)
+    _check(lib.cve_keystream_generate_lasm(lan, out.ctypes.data, length))
+    return out
+
+
+def glibc_sin(x: np.ndarray) -> np.ndarray:
+    """sin of every element, evaluated on the GPU by the glibc restatement the
+    LASM generator uses (diagnostics / parity)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    _check(lib.cve_glibc_sin(x.ctypes.data, y.ctypes.data, x.size))
+    return y
 
 
 # ---- file pipelines (reference cve.h:84-113) ----------------------------------

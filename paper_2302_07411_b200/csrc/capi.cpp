@@ -415,6 +415,36 @@ cve_status cve_keystream_generate(const double lanes[4], uint8_t* out,
   });
 }
 
+cve_status cve_keystream_generate_lasm(const double lanes[6], uint8_t* out,
+                                       size_t len) {
+  return guarded([&] {
+    require(lanes != nullptr, "lanes is null");
+    require(out != nullptr || len == 0, "out is null");
+    cveb::standalone_stream(cveb::LasmLane{lanes[0], lanes[1], lanes[2]},
+                            cveb::LasmLane{lanes[3], lanes[4], lanes[5]}, out, len);
+  });
+}
+
+cve_status cve_glibc_sin(const double* x, double* y, size_t count) {
+  return guarded([&] {
+    require((x != nullptr && y != nullptr) || count == 0, "null buffer");
+    if (count == 0) return;
+    struct Buf {
+      double* p = nullptr;
+      ~Buf() { cudaFree(p); }
+    } dx, dy;
+    if (cudaMalloc(&dx.p, count * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&dy.p, count * sizeof(double)) != cudaSuccess)
+      cveb::raise(cveb::Errc::internal, "cudaMalloc failed (no usable CUDA device?)");
+    if (cudaMemcpy(dx.p, x, count * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      cveb::raise(cveb::Errc::internal, "upload failed");
+    cveb::launch_glibc_sin(dx.p, dy.p, count, nullptr);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpy(y, dy.p, count * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      cveb::raise(cveb::Errc::internal, "glibc_sin kernel failed");
+  });
+}
+
 cve_status cve_derive_worker_lanes(const char* key_hex, uint32_t workers,
                                    double* lanes_out, uint32_t* seeds_out,
                                    size_t nseeds) {
@@ -426,10 +456,19 @@ cve_status cve_derive_worker_lanes(const char* key_hex, uint32_t workers,
     cveb::Coordinator coord(cveb::parse_key(key_hex));
     const std::vector<cveb::WorkerLanes> w = coord.derive_workers(workers);
     for (uint32_t i = 0; i < workers; ++i) {
-      lanes_out[4 * i + 0] = w[i].a.x0;
-      lanes_out[4 * i + 1] = w[i].a.p;
-      lanes_out[4 * i + 2] = w[i].b.x0;
-      lanes_out[4 * i + 3] = w[i].b.p;
+      if (coord.kind() == cveb::MapKind::Plcm) {
+        lanes_out[4 * i + 0] = w[i].a.x0;
+        lanes_out[4 * i + 1] = w[i].a.p;
+        lanes_out[4 * i + 2] = w[i].b.x0;
+        lanes_out[4 * i + 3] = w[i].b.p;
+      } else {
+        const cveb::LasmLane* l[2] = {&w[i].la, &w[i].lb};
+        for (int k = 0; k < 2; ++k) {
+          lanes_out[6 * i + 3 * k + 0] = l[k]->x0;
+          lanes_out[6 * i + 3 * k + 1] = l[k]->y0;
+          lanes_out[6 * i + 3 * k + 2] = l[k]->mu;
+        }
+      }
     }
     for (size_t k = 0; k < nseeds; ++k) seeds_out[k] = coord.next_seed();
   });

@@ -26,12 +26,6 @@ uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
 constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
 
-// Largest launch (iterations, multiple of 8) the orbit budget allows.
-uint32_t orbit_cap_iters(uint32_t nlanes) {
-  const uint64_t iters = std::min<uint64_t>(kOrbitBytes / (8ull * nlanes), 1u << 20) / 8 * 8;
-  return uint32_t(std::max<uint64_t>(iters, 8));
-}
-
 void free_prbg(PrbgBuffers& b) {
   cudaFree(b.state);
   cudaFree(b.verified_end);
@@ -103,7 +97,112 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
                      cudaMemcpyDeviceToDevice, s), "copy state");
   ck(cudaStreamSynchronize(s), "prbg_init");
 }
+
+void free_lasm(LasmBuffers& b) {
+  cudaFree(b.state);
+  cudaFree(b.mu);
+  for (auto& o : b.orbit) cudaFree(o);
+  b = LasmBuffers{};
+}
 }  // namespace
+
+void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaStream_t s,
+                     uint32_t orbit_iters) {
+  release();
+  kind_ = kind;
+  nl_ = uint32_t(2 * lanes.size());
+  if (kind_ == MapKind::Plcm) {
+    std::vector<LaneConst> lc(nl_);
+    std::vector<double> x0(nl_);
+    for (size_t i = 0; i < lanes.size(); ++i) {
+      lc[2 * i] = make_lane_const(lanes[i].a.p);
+      lc[2 * i + 1] = make_lane_const(lanes[i].b.p);
+      x0[2 * i] = lanes[i].a.x0;
+      x0[2 * i + 1] = lanes[i].b.x0;
+    }
+    pb_ = alloc_prbg(nl_, s, orbit_iters);
+    ck(cudaMalloc(&d_lc_, nl_ * sizeof(LaneConst)), "cudaMalloc lanes");
+    ck(cudaMemcpyAsync(d_lc_, lc.data(), nl_ * sizeof(LaneConst), cudaMemcpyHostToDevice, s),
+       "upload lanes");
+    init_prbg(pb_, d_lc_, x0.data(), nl_, s);
+    return;
+  }
+  std::vector<double> mu(nl_);
+  std::vector<double2> xy0(nl_);
+  for (size_t i = 0; i < lanes.size(); ++i) {
+    mu[2 * i] = lanes[i].la.mu;
+    mu[2 * i + 1] = lanes[i].lb.mu;
+    xy0[2 * i] = make_double2(lanes[i].la.x0, lanes[i].la.y0);
+    xy0[2 * i + 1] = make_double2(lanes[i].lb.x0, lanes[i].lb.y0);
+  }
+  struct Staging {  // freed on every path (cudaFree waits for the device)
+    double2* p = nullptr;
+    ~Staging() { cudaFree(p); }
+  } d_xy0;
+  ck(cudaMalloc(&lb_.state, nl_ * sizeof(double2)), "cudaMalloc lasm state");
+  ck(cudaMalloc(&lb_.mu, nl_ * sizeof(double)), "cudaMalloc lasm mu");
+  ck(cudaMalloc(&d_xy0.p, nl_ * sizeof(double2)), "cudaMalloc lasm x0");
+  ck(cudaMemcpyAsync(lb_.mu, mu.data(), nl_ * sizeof(double), cudaMemcpyHostToDevice, s),
+     "upload mu");
+  ck(cudaMemcpyAsync(d_xy0.p, xy0.data(), nl_ * sizeof(double2), cudaMemcpyHostToDevice, s),
+     "upload x0");
+  launch_lasm_init(lb_.state, lb_.mu, d_xy0.p, nl_, s);
+  ck(cudaGetLastError(), "lasm_init launch");
+  if (orbit_iters) resize(orbit_iters);
+  ck(cudaStreamSynchronize(s), "lasm_init");
+}
+
+void Generator::release() noexcept {
+  free_prbg(pb_);
+  cudaFree(d_lc_);
+  d_lc_ = nullptr;
+  free_lasm(lb_);
+}
+
+uint32_t Generator::orbit_cap_iters() const {
+  const uint64_t per = (kind_ == MapKind::Lasm ? 16ull : 8ull) * nl_;
+  const uint64_t iters = std::min<uint64_t>(kOrbitBytes / per, 1u << 20) / 8 * 8;
+  return uint32_t(std::max<uint64_t>(iters, 8));
+}
+
+void Generator::resize(uint32_t iters) {
+  if (kind_ == MapKind::Plcm) {
+    resize_orbit(pb_, nl_, iters);
+    return;
+  }
+  for (auto& o : lb_.orbit) {
+    cudaFree(o);
+    o = nullptr;
+  }
+  lb_.max_iters = 0;
+  for (auto& o : lb_.orbit)
+    ck(cudaMalloc(&o, uint64_t(iters) * nl_ * sizeof(double2)), "cudaMalloc lasm orbit");
+  lb_.max_iters = iters;
+}
+
+void Generator::chain(int slot, uint32_t iters, cudaStream_t s) {
+  if (kind_ == MapKind::Plcm)
+    launch_prbg_chain(pb_, slot, d_lc_, iters, nl_, s);
+  else
+    launch_lasm_chain(lb_, slot, iters, nl_, s);
+  ck(cudaGetLastError(), "generator chain launch");
+}
+
+void Generator::emit(int slot, uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
+                     uint32_t iters, cudaStream_t s) {
+  if (kind_ == MapKind::Plcm)
+    launch_prbg_verify(pb_, slot, d_lc_, ring, ring_bytes, it0, iters, nl_, s);
+  else
+    launch_lasm_emit(lb_, slot, ring, ring_bytes, it0, iters, nl_, s);
+  ck(cudaGetLastError(), "generator emit launch");
+}
+
+uint64_t Generator::replays() {
+  if (kind_ != MapKind::Plcm || !pb_.replays) return 0;
+  unsigned long long rep = 0;
+  ck(cudaMemcpy(&rep, pb_.replays, sizeof rep, cudaMemcpyDeviceToHost), "stats");
+  return rep;
+}
 
 namespace {
 std::atomic<int> g_streams{0};  // 0: not yet read from the environment
@@ -185,20 +284,8 @@ void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
     s_gen_ = s_work_;
   }
 
-  const uint32_t nl = 2 * n_;
-  std::vector<LaneConst> lc(nl);
-  std::vector<double> x0(nl);
-  for (uint32_t i = 0; i < n_; ++i) {
-    lc[2 * i] = make_lane_const(lanes[i].a.p);
-    lc[2 * i + 1] = make_lane_const(lanes[i].b.p);
-    x0[2 * i] = lanes[i].a.x0;
-    x0[2 * i + 1] = lanes[i].b.x0;
-  }
-  pb_ = alloc_prbg(nl, s_gen_, 0);  // orbit buffers sized by ensure_ring
-  ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-  ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice,
-                     s_gen_), "upload lanes");
-  init_prbg(pb_, d_lc_, x0.data(), nl, s_gen_);
+  gen_.init(lanes, key_.kind, s_gen_, 0);  // orbit buffers sized by ensure_ring
+  bpi_ = gen_.bytes_per_iter();
   ++st_.kernel_launches;
 }
 
@@ -245,9 +332,7 @@ void Engine::release() noexcept {
   d_shift_ = nullptr;
   cudaFree(ring_);
   ring_ = nullptr;
-  free_prbg(pb_);
-  cudaFree(d_lc_);
-  d_lc_ = nullptr;
+  gen_.release();
   for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_h2d_, s_work_, s_d2h_})
     if (s) cudaStreamDestroy(s);
   s_gen_ = s_h2d_ = s_work_ = s_d2h_ = nullptr;
@@ -354,7 +439,7 @@ void Engine::ensure_ring(uint64_t need) {
   synchronize();
   uint8_t* fresh = nullptr;
   ck(cudaMalloc(&fresh, want * n_), "cudaMalloc keystream ring");
-  const uint64_t gen_bytes = gen_iters_ * 6;
+  const uint64_t gen_bytes = gen_iters_ * bpi_;
   if (ring_ && gen_bytes > cons_) {
     launch_ring_move(ring_, ring_bytes_, fresh, want, cons_, gen_bytes, n_, s_gen_);
     ++st_.kernel_launches;
@@ -365,10 +450,10 @@ void Engine::ensure_ring(uint64_t need) {
   ring_bytes_ = want;
   // orbit buffers for the longest launch gen_until will issue (a quarter of
   // the ring), within the orbit budget: a small clip holds MBs, not 256 MB
-  const uint32_t cap = orbit_cap_iters(2 * n_);
-  const uint64_t launch = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+  const uint32_t cap = gen_.orbit_cap_iters();
+  const uint64_t launch = std::max<uint64_t>(8, ring_bytes_ / 4 / bpi_ / 8 * 8);
   const uint32_t iters = uint32_t(std::min<uint64_t>(launch, cap));
-  if (iters > pb_.max_iters) resize_orbit(pb_, 2 * n_, iters);
+  if (iters > gen_.max_iters()) gen_.resize(iters);
   for (auto& c : consumers_) ev_put(c.done);
   consumers_.clear();
   for (auto& g : gens_) ev_put(g.ev);
@@ -429,29 +514,28 @@ const double* Engine::sine_for(uint32_t side) {
 // worker) is produced.  Launches cover whole 8-iteration (48-byte) blocks.
 void Engine::gen_until(uint64_t end_byte) {
   NvtxRange nvtx("cve: generator launches");
-  uint64_t target = round_up((end_byte + 5) / 6, 8);
+  uint64_t target = round_up((end_byte + bpi_ - 1) / bpi_, 8);
   // never produce beyond what the ring can hold ahead of unassigned bytes
-  const uint64_t cap = (cons_ + ring_bytes_) / 6 / 8 * 8;
+  const uint64_t cap = (cons_ + ring_bytes_) / bpi_ / 8 * 8;
   target = std::min(target, cap);
   while (gen_iters_ < target) {
     uint64_t chunk = target - gen_iters_;
-    uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / 6 / 8 * 8);
+    uint64_t max_chunk = std::max<uint64_t>(8, ring_bytes_ / 4 / bpi_ / 8 * 8);
     if (gen_chunk_cap_) max_chunk = std::min(max_chunk, gen_chunk_cap_);
-    chunk = std::min<uint64_t>({chunk, max_chunk, pb_.max_iters});
+    chunk = std::min<uint64_t>({chunk, max_chunk, uint64_t(gen_.max_iters())});
     if (chunk == 0) raise(Errc::internal, "generator launch without orbit buffers");
     const int slot = int(launches_ & 1);
     // (1) chain on s_gen, once the verifier is done with this slot's buffers
     if (launches_ >= 2) ck(cudaStreamWaitEvent(s_gen_, ver_done_[slot], 0), "wait slot");
     timed_begin(s_gen_, true);
-    launch_prbg_chain(pb_, slot, d_lc_, uint32_t(chunk), 2 * n_, s_gen_);
-    ck(cudaGetLastError(), "prbg_chain launch");
+    gen_.chain(slot, uint32_t(chunk), s_gen_);
     timed_end(s_gen_);
     ck(cudaEventRecord(chain_done_[slot], s_gen_), "cudaEventRecord");
     // (2)+(3) verify, emit, fix up on s_work while the next chain runs.
     // Ring bytes below write_end - R get overwritten: their readers must be
     // done.
     ck(cudaStreamWaitEvent(s_work_, chain_done_[slot], 0), "wait chain");
-    const uint64_t write_end = (gen_iters_ + chunk) * 6;
+    const uint64_t write_end = (gen_iters_ + chunk) * bpi_;
     if (write_end > ring_bytes_) {
       const uint64_t dead = write_end - ring_bytes_;
       while (!consumers_.empty() && consumers_.front().lo < dead) {
@@ -465,17 +549,15 @@ void Engine::gen_until(uint64_t end_byte) {
       }
     }
     timed_begin(s_work_, false, true);
-    launch_prbg_verify(pb_, slot, d_lc_, ring_, ring_bytes_, gen_iters_,
-                       uint32_t(chunk), 2 * n_, s_work_);
-    ck(cudaGetLastError(), "prbg_verify launch");
+    gen_.emit(slot, ring_, ring_bytes_, gen_iters_, uint32_t(chunk), s_work_);
     timed_end(s_work_);
     ck(cudaEventRecord(ver_done_[slot], s_work_), "cudaEventRecord");
-    st_.kernel_launches += 3;
+    st_.kernel_launches += gen_.kind() == MapKind::Plcm ? 3 : 2;
     ++st_.prbg_launches;
     ++launches_;
     gen_iters_ += chunk;
     st_.keystream_iters += chunk;
-    GenMark m{gen_iters_ * 6, ev_get()};
+    GenMark m{gen_iters_ * bpi_, ev_get()};
     ck(cudaEventRecord(m.ev, s_work_), "cudaEventRecord");
     gens_.push_back(m);
   }
@@ -636,9 +718,7 @@ void Engine::prefetch(uint64_t bytes) {
 EngineStats Engine::stats() {
   synchronize();
   fold_timings(true);
-  unsigned long long rep = 0;
-  ck(cudaMemcpy(&rep, pb_.replays, sizeof rep, cudaMemcpyDeviceToHost), "stats");
-  st_.guard_replays = rep;
+  st_.guard_replays = gen_.replays();
   return st_;
 }
 
@@ -650,23 +730,16 @@ std::vector<float> Engine::take_prbg_times() {
   return out;
 }
 
-// The reference's Prbg{lane_a, lane_b}.take(len) (chaos.cpp:79-91, 143-153,
-// 174-180) on the GPU: explicit lanes, one worker, K1 kernels.
-void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
-  if (len == 0) return;
-  HostPrbg validate(a, b);  // domain checks (bad_key), cheap
-  (void)validate;
-  const uint64_t iters = round_up((len + 5) / 6, 8);
-  const uint64_t ring = iters * 6;  // multiple of 48
-  LaneConst lc[2] = {make_lane_const(a.p), make_lane_const(b.p)};
-  const double x0[2] = {a.x0, b.x0};
-  PrbgBuffers pb{};
-  LaneConst* d_lc = nullptr;
-  uint8_t* d_out = nullptr;
+namespace {
+// The reference's Prbg{lane_a, lane_b}.take(len) (chaos.cpp:79-107, 143-153)
+// on the GPU: explicit lanes, one worker.
+void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len) {
   cudaStream_t s = nullptr;
+  uint8_t* d_out = nullptr;
+  Generator gen;
   auto cleanup = [&] {
-    free_prbg(pb);
-    cudaFree(d_lc);
+    if (s) cudaStreamSynchronize(s);
+    gen.release();
     cudaFree(d_out);
     if (s) cudaStreamDestroy(s);
   };
@@ -675,17 +748,17 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     configure_kernels_once(dev);
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    pb = alloc_prbg(2, s, orbit_cap_iters(2));
-    ck(cudaMalloc(&d_lc, sizeof lc), "cudaMalloc");
+    gen.init({w}, kind, s, 0);
+    gen.resize(gen.orbit_cap_iters());
+    const uint32_t bpi = gen.bytes_per_iter();
+    const uint64_t iters = round_up((len + bpi - 1) / bpi, 8);
+    const uint64_t ring = iters * bpi;  // multiple of 48
     ck(cudaMalloc(&d_out, ring), "cudaMalloc");
-    ck(cudaMemcpyAsync(d_lc, lc, sizeof lc, cudaMemcpyHostToDevice, s), "upload");
-    init_prbg(pb, d_lc, x0, 2, s);
     int slot = 0;
-    for (uint64_t it = 0; it < iters; it += pb.max_iters, slot ^= 1) {
-      const uint32_t n = uint32_t(std::min<uint64_t>(pb.max_iters, iters - it));
-      launch_prbg_chain(pb, slot, d_lc, n, 2, s);
-      launch_prbg_verify(pb, slot, d_lc, d_out, ring, it, n, 2, s);
-      ck(cudaGetLastError(), "prbg_generate");
+    for (uint64_t it = 0; it < iters; it += gen.max_iters(), slot ^= 1) {
+      const uint32_t n = uint32_t(std::min<uint64_t>(gen.max_iters(), iters - it));
+      gen.chain(slot, n, s);
+      gen.emit(slot, d_out, ring, it, n, s);
     }
     ck(cudaStreamSynchronize(s), "keystream");
     ck(cudaMemcpy(out, d_out, len, cudaMemcpyDeviceToHost), "download");
@@ -695,27 +768,37 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
   }
   cleanup();
 }
+}  // namespace
 
-KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, int device)
+void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
+  if (len == 0) return;
+  HostPrbg validate(a, b);  // domain checks (bad_key), cheap
+  (void)validate;
+  WorkerLanes w;
+  w.a = a;
+  w.b = b;
+  standalone(w, MapKind::Plcm, out, len);
+}
+
+void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len) {
+  if (len == 0) return;
+  check_lasm_lane(a);
+  check_lasm_lane(b);
+  WorkerLanes w;
+  w.la = a;
+  w.lb = b;
+  standalone(w, MapKind::Lasm, out, len);
+}
+
+KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind,
+                                 int device)
     : n_(uint32_t(lanes.size())) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   configure_kernels_once(device);
-  const uint32_t nl = 2 * n_;
-  std::vector<LaneConst> lc(nl);
-  std::vector<double> x0(nl);
-  for (uint32_t i = 0; i < n_; ++i) {
-    lc[2 * i] = make_lane_const(lanes[i].a.p);
-    lc[2 * i + 1] = make_lane_const(lanes[i].b.p);
-    x0[2 * i] = lanes[i].a.x0;
-    x0[2 * i + 1] = lanes[i].b.x0;
-  }
   try {
     ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
-    pb_ = alloc_prbg(nl, s_, orbit_cap_iters(nl));
-    ck(cudaMalloc(&d_lc_, nl * sizeof(LaneConst)), "cudaMalloc lanes");
-    ck(cudaMemcpyAsync(d_lc_, lc.data(), nl * sizeof(LaneConst), cudaMemcpyHostToDevice, s_),
-       "upload");
-    init_prbg(pb_, d_lc_, x0.data(), nl, s_);
+    gen_.init(lanes, kind, s_, 0);
+    gen_.resize(gen_.orbit_cap_iters());
     ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
   } catch (...) {
     release();
@@ -727,9 +810,7 @@ KeystreamSource::~KeystreamSource() { release(); }
 
 void KeystreamSource::release() noexcept {
   if (s_) cudaStreamSynchronize(s_);
-  free_prbg(pb_);
-  cudaFree(d_lc_);
-  d_lc_ = nullptr;
+  gen_.release();
   cudaFree(d_buf_);
   d_buf_ = nullptr;
   if (s_) cudaStreamDestroy(s_);
@@ -744,9 +825,8 @@ void KeystreamSource::next(uint8_t* host, uint64_t bytes) {
   uint64_t got = 0;
   while (got < bytes) {
     if (carry_ == have_) {
-      launch_prbg_chain(pb_, slot_, d_lc_, pb_.max_iters, 2 * n_, s_);
-      launch_prbg_verify(pb_, slot_, d_lc_, d_buf_, cb, 0, pb_.max_iters, 2 * n_, s_);
-      ck(cudaGetLastError(), "keystream launch");
+      gen_.chain(slot_, gen_.max_iters(), s_);
+      gen_.emit(slot_, d_buf_, cb, 0, gen_.max_iters(), s_);
       slot_ ^= 1;
       carry_ = 0;
       have_ = cb;

@@ -63,6 +63,45 @@ struct EngineStats {
 void set_streams_per_handle(int n);
 int streams_per_handle();
 
+// Keystream generator of 2n lanes of either map on one device: the PLCM
+// kernels (prbg.cu: speculative chain, verify/emit, fix-up) or the LASM
+// kernels (lasm.cu: chain, emit).  chain(slot) advances every lane and writes
+// orbit buffer `slot`; emit(slot) turns that orbit into keystream bytes.  The
+// two orbit buffers let emission of launch L overlap the chain of launch L+1.
+class Generator {
+ public:
+  Generator() = default;
+  ~Generator() { release(); }
+  Generator(const Generator&) = delete;
+  Generator& operator=(const Generator&) = delete;
+
+  // Uploads the lanes and runs the warm-up on `s` (synchronously).
+  // orbit_iters = 0: no orbit buffers yet (see resize).
+  void init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaStream_t s,
+            uint32_t orbit_iters);
+  void release() noexcept;
+  MapKind kind() const { return kind_; }
+  uint32_t bytes_per_iter() const { return kind_ == MapKind::Lasm ? 12 : 6; }
+  uint32_t max_iters() const { return kind_ == MapKind::Lasm ? lb_.max_iters : pb_.max_iters; }
+  // Largest launch (iterations, multiple of 8) the orbit memory budget allows.
+  uint32_t orbit_cap_iters() const;
+  // Regrows both orbit buffers to `iters` per launch (caller synchronised).
+  void resize(uint32_t iters);
+  void chain(int slot, uint32_t iters, cudaStream_t s);
+  // Iterations [it0, it0+iters) of launch `slot` into the ring at stream byte
+  // bytes_per_iter()*it (mod ring_bytes).
+  void emit(int slot, uint8_t* ring, uint64_t ring_bytes, uint64_t it0, uint32_t iters,
+            cudaStream_t s);
+  uint64_t replays();  // PLCM workers recomputed exactly (always 0 for LASM)
+
+ private:
+  MapKind kind_ = MapKind::Plcm;
+  uint32_t nl_ = 0;
+  PrbgBuffers pb_{};
+  LaneConst* d_lc_ = nullptr;
+  LasmBuffers lb_{};
+};
+
 class Engine {
  public:
   Engine(const Key& key, uint32_t workers, uint32_t rounds, int device);
@@ -142,8 +181,8 @@ class Engine {
   uint64_t launches_ = 0;  // generator launches (slot = launches_ & 1)
   uint64_t gen_chunk_cap_ = 0;  // optional cap on iterations per generator launch
   bool one_stream_ = false;     // generator shares the rounds stream
-  PrbgBuffers pb_{};
-  LaneConst* d_lc_ = nullptr;
+  Generator gen_;
+  uint32_t bpi_ = 6;  // keystream bytes per generator iteration (6 PLCM, 12 LASM)
 
   uint8_t* ring_ = nullptr;
   uint64_t ring_bytes_ = 0;
@@ -169,8 +208,9 @@ class Engine {
   EngineStats st_;
 };
 
-// Reference Prbg with explicit lanes, generated by K1 on the current device.
+// Reference Prbg with explicit lanes, generated on the current device.
 void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len);
+void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len);
 
 // Fresh generators for a set of workers (reference WorkerParams::make_prbg,
 // keying.cpp:154-162), advanced together on the GPU; next() copies the next
@@ -178,18 +218,17 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len);
 // with a stride of chunk_bytes().
 class KeystreamSource {
  public:
-  KeystreamSource(const std::vector<WorkerLanes>& lanes, int device);
+  KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind, int device);
   ~KeystreamSource();
   KeystreamSource(const KeystreamSource&) = delete;
   KeystreamSource& operator=(const KeystreamSource&) = delete;
-  uint64_t chunk_bytes() const { return uint64_t(pb_.max_iters) * 6; }
+  uint64_t chunk_bytes() const { return uint64_t(gen_.max_iters()) * gen_.bytes_per_iter(); }
   void next(uint8_t* host, uint64_t bytes);
 
  private:
   void release() noexcept;
   uint32_t n_;
-  PrbgBuffers pb_{};
-  LaneConst* d_lc_ = nullptr;
+  Generator gen_;
   uint8_t* d_buf_ = nullptr;
   cudaStream_t s_ = nullptr;
   int slot_ = 0;

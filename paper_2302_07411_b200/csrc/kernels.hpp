@@ -62,6 +62,29 @@ void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
                         uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
                         uint32_t iters, uint32_t nlanes, cudaStream_t s);
 
+// LASM generator (lasm.cu, row f2).  Lane layout as above; per lane the
+// chain position (x, y) and mu.  Orbit values are lane-major:
+// orbit[slot][lane * max_iters + i] = (x, y) after iteration i of the launch.
+struct LasmBuffers {
+  double2* state;
+  double* mu;
+  double2* orbit[2];
+  uint32_t max_iters;  // per launch, multiple of 8
+};
+// 256 warm-up iterations from the start points xy0 (chaos.cpp:93-107).
+void launch_lasm_init(double2* state, const double* mu, const double2* xy0, uint32_t nlanes,
+                      cudaStream_t s);
+// Advances every lane by `iters` (multiple of 8) iterations into orbit[slot].
+void launch_lasm_chain(const LasmBuffers& b, int slot, uint32_t iters, uint32_t nlanes,
+                       cudaStream_t s);
+// Emits the 12 bytes per iteration of launch `slot` (iterations
+// [it0, it0+iters), it0 % 8 == 0) into the ring at stream byte 12*it
+// (mod ring_bytes, ring_bytes % 48 == 0).
+void launch_lasm_emit(const LasmBuffers& b, int slot, uint8_t* ring, uint64_t ring_bytes,
+                      uint64_t it0, uint32_t iters, uint32_t nlanes, cudaStream_t s);
+// y[i] = glibc sin(x[i]) (glibc_sin.cuh), for parity tests.
+void launch_glibc_sin(const double* x, double* y, size_t n, cudaStream_t s);
+
 // Geometry of one square frame split into n row bands.
 struct Geom {
   uint32_t side, n, rows;  // rows = side / n

@@ -46,12 +46,12 @@ bool lasm_mu_ok(double mu) {  // chaos.cpp:41-44
          (mu >= 0.44 && mu <= 0.93) || mu == 1.0;
 }
 
-void check_lasm(const Key& k) {
-  auto unit = [](double v) { return std::isfinite(v) && v >= 0.0 && v <= 1.0; };
-  if (!unit(k.lx0)) raise(Errc::bad_key, "lasm x0 outside [0,1]");
-  if (!unit(k.ly0)) raise(Errc::bad_key, "lasm y0 outside [0,1]");
-  if (!(std::isfinite(k.lmu) && lasm_mu_ok(k.lmu)))
-    raise(Errc::bad_key, "lasm mu outside the chaotic bands");
+void check_lasm(const Key& k) { check_lasm_lane(LasmLane{k.lx0, k.ly0, k.lmu}); }
+
+double rotate_half(double v) {  // keying.cpp:67-73
+  v += 0.5;
+  if (v >= 1.0) v -= 1.0;
+  return v;
 }
 
 double inside(double v, double lo, double hi) {  // keying.cpp:61-65
@@ -69,6 +69,14 @@ double entropy_unit(std::random_device& rd) {  // keying.cpp:52-59
 }
 
 }  // namespace
+
+void check_lasm_lane(const LasmLane& l) {  // chaos.cpp:67-77
+  auto unit = [](double v) { return std::isfinite(v) && v >= 0.0 && v <= 1.0; };
+  if (!unit(l.x0)) raise(Errc::bad_key, "lasm x0 outside [0,1]");
+  if (!unit(l.y0)) raise(Errc::bad_key, "lasm y0 outside [0,1]");
+  if (!(std::isfinite(l.mu) && lasm_mu_ok(l.mu)))
+    raise(Errc::bad_key, "lasm mu outside the chaotic bands");
+}
 
 Key parse_key(const char* hex) {
   size_t len = std::strlen(hex);
@@ -154,38 +162,65 @@ double plcm_iterate(double x, double p) {
   return plcm_guard(y, p);
 }
 
+void lasm_iterate(double& x, double& y, double mu) {
+  const double pi = 3.14159265358979323846;  // std::numbers::pi
+  const double xn = std::sin(pi * mu * (y + 3.0) * x * (1.0 - x));
+  const double yn = std::sin(pi * mu * (xn + 3.0) * y * (1.0 - y));
+  x = xn;
+  y = yn;
+}
+
 HostPrbg::HostPrbg(Lane a, Lane b) : pa_(a.p), pb_(b.p) {
   check_plcm(a);
   check_plcm(b);
   xa_ = plcm_guard(a.x0, pa_);
   xb_ = plcm_guard(b.x0, pb_);
-  for (int i = 0; i < 256; ++i) {  // kWarmupSteps (chaos.hpp:14)
+  for (int i = 0; i < 256; ++i) step();  // kWarmupSteps (chaos.hpp:14)
+}
+
+HostPrbg::HostPrbg(LasmLane a, LasmLane b)
+    : lasm_(true), xa_(a.x0), pa_(a.mu), xb_(b.x0), pb_(b.mu), ya_(a.y0), yb_(b.y0) {
+  check_lasm_lane(a);  // chaos.cpp:93-107: no guard for LASM
+  check_lasm_lane(b);
+  for (int i = 0; i < 256; ++i) step();
+}
+
+void HostPrbg::step() {
+  if (lasm_) {
+    lasm_iterate(xa_, ya_, pa_);
+    lasm_iterate(xb_, yb_, pb_);
+  } else {
     xa_ = plcm_iterate(xa_, pa_);
     xb_ = plcm_iterate(xb_, pb_);
   }
 }
 
 void HostPrbg::fill(uint8_t* out, size_t n) {
+  auto put48 = [](uint8_t* dst, double a, double b) {
+    uint64_t ba, bb;
+    std::memcpy(&ba, &a, 8);
+    std::memcpy(&bb, &b, 8);
+    for (int k = 0; k < 6; ++k) dst[k] = uint8_t((ba ^ bb) >> (8 * k));
+  };
   for (size_t i = 0; i < n; ++i) {
-    if (pos_ == 6) {
-      xa_ = plcm_iterate(xa_, pa_);
-      xb_ = plcm_iterate(xb_, pb_);
-      uint64_t ba, bb;
-      std::memcpy(&ba, &xa_, 8);
-      std::memcpy(&bb, &xb_, 8);
-      const uint64_t v = ba ^ bb;
-      for (int k = 0; k < 6; ++k) buf_[k] = uint8_t(v >> (8 * k));
+    if (pos_ == len_) {
+      step();
+      put48(buf_, xa_, xb_);
+      if (lasm_) put48(buf_ + 6, ya_, yb_);
+      len_ = lasm_ ? 12 : 6;
       pos_ = 0;
     }
     out[i] = buf_[pos_++];
   }
 }
 
-Coordinator::Coordinator(const Key& key) {
-  if (key.kind != MapKind::Plcm)
-    raise(Errc::invalid_argument,
-          "LASM keys are not supported by the B200 engine (PLCM only)");
-  prbg_ = HostPrbg(key.a, key.b);
+Coordinator::Coordinator(const Key& key) : kind_(key.kind) {
+  if (key.kind == MapKind::Plcm) {
+    prbg_ = HostPrbg(key.a, key.b);
+  } else {  // keying.cpp:164-170: lane b is the key rotated by one half
+    prbg_ = HostPrbg(LasmLane{key.lx0, key.ly0, key.lmu},
+                     LasmLane{rotate_half(key.lx0), rotate_half(key.ly0), key.lmu});
+  }
 }
 
 double Coordinator::next_unit() {
@@ -196,12 +231,20 @@ double Coordinator::next_unit() {
   return double(v) / double((uint64_t(1) << 48) - 1);
 }
 
-std::vector<WorkerLanes> Coordinator::derive_workers(uint32_t n) {
+std::vector<WorkerLanes> Coordinator::derive_workers(uint32_t n) {  // keying.cpp:180-207
   std::vector<WorkerLanes> out(n);
   for (auto& w : out) {
-    for (Lane* l : {&w.a, &w.b}) {
-      l->x0 = inside(next_unit(), 0.0, 1.0);
-      l->p = inside(next_unit() * 0.5, 0.0, 0.5);
+    if (kind_ == MapKind::Plcm) {
+      for (Lane* l : {&w.a, &w.b}) {
+        l->x0 = inside(next_unit(), 0.0, 1.0);
+        l->p = inside(next_unit() * 0.5, 0.0, 0.5);
+      }
+    } else {
+      for (LasmLane* l : {&w.la, &w.lb}) {
+        l->x0 = inside(next_unit(), 0.0, 1.0);
+        l->y0 = inside(next_unit(), 0.0, 1.0);
+        l->mu = inside(0.44 + next_unit() * (0.93 - 0.44), 0.44, 0.93);
+      }
     }
   }
   return out;

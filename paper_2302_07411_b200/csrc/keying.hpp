@@ -41,10 +41,16 @@ struct Lane {  // one PLCM orbit: start point and control parameter
   double p = 0;
 };
 
+struct LasmLane {  // one LASM orbit (chaos.hpp LasmParams): start point, mu
+  double x0 = 0;
+  double y0 = 0;
+  double mu = 0;
+};
+
 struct Key {
   MapKind kind = MapKind::Plcm;
   Lane a, b;                          // PLCM
-  double lx0 = 0, ly0 = 0, lmu = 0;   // LASM (validated only)
+  double lx0 = 0, ly0 = 0, lmu = 0;   // LASM
 };
 
 // Reference parse_key_hex (keying.cpp:77-107): trailing whitespace trimmed,
@@ -59,23 +65,35 @@ Key fresh_key(MapKind kind);  // OS entropy, like generate_key (keying.cpp:131-1
 double plcm_iterate(double x, double p);
 double plcm_guard(double x, double p);
 
-// Two-lane, 6-byte-per-iteration byte generator with a chunk-invariant byte
-// cursor (chaos.cpp:79-91, 119-153).
+// LASM map, one iteration (chaos.cpp:34-38) with the host's libm sin -- the
+// coordinator's copy; the subframe generators run on the GPU (lasm.cu).
+void lasm_iterate(double& x, double& y, double mu);
+void check_lasm_lane(const LasmLane& l);  // chaos.cpp:67-77, throws bad_key
+
+// Two-lane byte generator with a chunk-invariant byte cursor: 6 bytes per
+// PLCM iteration, 12 per LASM iteration (x bytes, then y bytes)
+// (chaos.cpp:79-107, 119-153).
 class HostPrbg {
  public:
   HostPrbg() = default;
   HostPrbg(Lane a, Lane b);
+  HostPrbg(LasmLane a, LasmLane b);
   void fill(uint8_t* out, size_t n);
 
  private:
-  double xa_ = 0, pa_ = 0, xb_ = 0, pb_ = 0;
-  uint8_t buf_[6] = {};
-  int pos_ = 6;
+  void step();
+  bool lasm_ = false;
+  double xa_ = 0, pa_ = 0, xb_ = 0, pb_ = 0;  // LASM: pa_/pb_ hold mu
+  double ya_ = 0, yb_ = 0;
+  uint8_t buf_[12] = {};
+  int pos_ = 0, len_ = 0;  // pos_ == len_: empty
 };
 
-// Lane pair of subframe generator i, in reference derivation order.
+// Lane pair of subframe generator i, in reference derivation order; the
+// PLCM pair (a, b) or the LASM pair (la, lb), by the key's map.
 struct WorkerLanes {
   Lane a, b;
+  LasmLane la, lb;
 };
 
 // Coordinator (keying.cpp:164-218): seeded from the key lanes, derives the
@@ -84,12 +102,14 @@ struct WorkerLanes {
 class Coordinator {
  public:
   explicit Coordinator(const Key& key);
+  MapKind kind() const { return kind_; }
   std::vector<WorkerLanes> derive_workers(uint32_t n);
   uint32_t next_seed();
   uint64_t seeds_drawn() const { return seeds_; }
 
  private:
   double next_unit();
+  MapKind kind_ = MapKind::Plcm;
   HostPrbg prbg_;
   uint64_t seeds_ = 0;
 };

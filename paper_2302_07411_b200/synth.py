@@ -80,6 +80,23 @@ def det_key(seed: int) -> str:
     return "00" + "".join(_f64_hex_le(v) for v in (x0a, pa, x0b, pb))
 
 
+def det_key_lasm(seed: int) -> str:
+    """LASM key hex from a seed (acceptance.cpp:57-74, LASM branch:
+    {unit(), unit(), 0.44 + unit() * (0.93 - 0.44)})."""
+    rng = MT19937_64(seed)
+
+    def unit() -> float:
+        while True:
+            u = float(rng() >> 11) * 2.0 ** -53
+            if 0.0 < u < 1.0:
+                return u
+
+    x0 = unit()
+    y0 = unit()
+    mu = 0.44 + unit() * (0.93 - 0.44)
+    return "01" + "".join(_f64_hex_le(v) for v in (x0, y0, mu))
+
+
 def flip_key_lsb(key_hex: str) -> str:
     """Flip the mantissa LSB of x0_a (key stays in-domain)."""
     raw = bytearray(bytes.fromhex(key_hex))

@@ -52,6 +52,9 @@ class Oracle:
             L.orc_cipher_params.argtypes = [vp]
             L.orc_cipher_params.restype = C.POINTER(C.c_double)
             L.orc_plcm_stream.argtypes = [C.c_double] * 4 + [vp, C.c_size_t]
+            L.orc_lasm_stream.argtypes = [C.POINTER(C.c_double), vp, C.c_size_t]
+            L.orc_lasm_iterate.argtypes = [C.POINTER(C.c_double)] * 2 + [C.c_double]
+            L.orc_cipher_is_lasm.argtypes = [vp]
             L.orc_plcm_iterate.argtypes = [C.c_double, C.c_double]
             L.orc_plcm_iterate.restype = C.c_double
             L.orc_confusion_shift.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32]
@@ -84,8 +87,11 @@ class Oracle:
         return out
 
     def params(self) -> np.ndarray:
+        """(workers, 4) PLCM lanes, or (workers, 6) LASM lanes."""
+        per = 6 if Oracle.lib.orc_cipher_is_lasm(self.h) else 4
         p = Oracle.lib.orc_cipher_params(self.h)
-        return np.ctypeslib.as_array(p, shape=(self.workers * 4,)).reshape(self.workers, 4).copy()
+        return np.ctypeslib.as_array(p, shape=(self.workers * per,)).reshape(self.workers,
+                                                                             per).copy()
 
     @property
     def seeds_drawn(self) -> int:
@@ -97,6 +103,21 @@ def plcm_stream(xa, pa, xb, pb, n) -> np.ndarray:
     st = Oracle.load().orc_plcm_stream(xa, pa, xb, pb, _ptr(out), n)
     assert st == 0
     return out
+
+
+def lasm_stream(lanes, n) -> np.ndarray:
+    """Reference Prbg(LasmParams, LasmParams).take(n), lanes = 6 doubles."""
+    out = np.zeros(n, dtype=np.uint8)
+    arr = (C.c_double * 6)(*[float(v) for v in lanes])
+    st = Oracle.load().orc_lasm_stream(arr, _ptr(out), n)
+    assert st == 0
+    return out
+
+
+def lasm_iterate(x, y, mu):
+    xx, yy = C.c_double(x), C.c_double(y)
+    Oracle.load().orc_lasm_iterate(C.byref(xx), C.byref(yy), mu)
+    return xx.value, yy.value
 
 
 class RefIo(C.Structure):

@@ -14,8 +14,12 @@ paper_2302_07411_b200.synth and records:
 * clips.json (--full-clips) -- SHA-256 of the plaintext and of the reference
   ciphertext of EVERY frame of the C3 (240), C4 (1000) and C5 (500) clips
   (SURVEY 8(d) parity gate: per-frame digest equality for every frame).
+* lasm.json (--lasm) -- row f2, LASM keys (acceptance.cpp det_key recipe):
+  full ciphertexts of small shapes, the reference's per-frame digests of the
+  config geometries C1-C4 under a LASM key, and worker keystream digests.
+  Also refreshes reference_unit.json (which holds the LASM unit goldens).
 
-Usage:  python tests/golden/make_golden.py [--full-clips]   (needs oracle/_ref)
+Usage:  python tests/golden/make_golden.py [--full-clips | --lasm]   (needs oracle/_ref)
 """
 from __future__ import annotations
 
@@ -54,9 +58,11 @@ def ref_encrypt_clip(key: str, n: int, frames):
     return out
 
 
-def main() -> None:
-    assert Reference.available(), "build oracle/_ref first (make -C oracle ref)"
-    unit = {
+LASM_HEX = "01333333333333d33f666666666666e63f6f8104c58f31ed3f"
+
+
+def unit_goldens() -> dict:
+    return {
         "source": "literal constants from the reference's unit tests",
         "plcm_golden_48": {
             "cite": "proj/tests/test_chaos.cpp:96-109",
@@ -79,7 +85,32 @@ def main() -> None:
                             "v": 0xF0, "b": 0x10, "prev": 0x0F, "c": 0x1F},
         "extract_third": {"cite": "proj/tests/test_chaos.cpp:83-94",
                           "value": "1/3", "bytes": "555555555555"},
+        "lasm_golden_48": {
+            "cite": "proj/tests/test_chaos.cpp:111-123",
+            "lanes": [0.3, 0.7, 0.9123, 0.55, 0.21, 0.8321],
+            "bytes": "de82ae7020e9cd4a7258ad36d7d70ca19e2dcc691dba3c2a"
+                     "0c17f9d3b93ab32f735e22f35752c6bf1ac9d6ae5b42e897",
+        },
+        "lasm_step_examples": {
+            "cite": "proj/tests/test_chaos.cpp:36-45 (Approx, epsilon 1e-12; x=1 gives x'=0 exactly)",
+            "cases": [{"x": 0.5, "y": 0.5, "mu": 0.9,
+                       "approx": [0.6190939493098342, 0.5508696497734819]},
+                      {"x": 1.0, "y": 0.5, "mu": 0.9,
+                       "approx": [0.0, 0.8526401643540923]}],
+        },
+        "lasm_worker_params_n1": {
+            "cite": "proj/tests/test_keying.cpp:181-195",
+            "key": LASM_HEX,
+            "lanes": [[0.3531432805935934, 0.64474196869762912, 0.63942352257547352,
+                       0.91624103790716271, 0.46510262553097259, 0.90454267912309261]],
+            "seeds": [443065481, 4137672024],
+        },
     }
+
+
+def main() -> None:
+    assert Reference.available(), "build oracle/_ref first (make -C oracle ref)"
+    unit = unit_goldens()
     with open(os.path.join(HERE, "reference_unit.json"), "w") as fh:
         json.dump(unit, fh, indent=1)
 
@@ -165,6 +196,54 @@ def full_clips() -> None:
     print("wrote clips.json")
 
 
+# LASM geometries (row f2): (config geometry, frames recorded)
+LASM_CLIPS = {"C1": 2, "C2": 4, "C3": 3, "C4": 2}
+
+
+def lasm() -> None:
+    """Row f2 goldens from the reference itself, LASM keys."""
+    assert Reference.available(), "build oracle/_ref first (make -C oracle ref)"
+    with open(os.path.join(HERE, "reference_unit.json"), "w") as fh:
+        json.dump(unit_goldens(), fh, indent=1)
+    out = {"cases": [], "clips": {}}
+    rng = np.random.Generator(np.random.PCG64(2303))
+    for side, n, r, nframes in [(8, 2, 3, 3), (24, 4, 5, 2), (30, 3, 5, 2), (48, 1, 2, 2),
+                                (96, 8, 5, 2), (20, 5, 1, 2)]:
+        key = synth.det_key_lasm(2000 + side + n)
+        plain = [rng.integers(0, 256, (side, side, 3), dtype=np.uint8) for _ in range(nframes)]
+        rr = Reference(key, n, r, 1)
+        ct = []
+        for p in plain:
+            x = p.copy()
+            assert rr.encrypt(x) == 0
+            ct.append(x.tobytes().hex())
+        out["cases"].append({"key": key, "side": side, "workers": n, "rounds": r,
+                             "plain": [p.tobytes().hex() for p in plain], "cipher": ct})
+    for name, count in LASM_CLIPS.items():
+        c = synth.CONFIGS[name]
+        key = synth.det_key_lasm(4242 + c["workers"])
+        plain = synth.frame_list(name, count)
+        ct = ref_encrypt_clip(key, c["workers"], plain)
+        out["clips"][name] = {"key": key, "side": synth.config_side(name),
+                              "workers": c["workers"], "rounds": synth.ROUNDS,
+                              "plain_sha256": [sha(p) for p in plain],
+                              "cipher_sha256": [sha(x) for x in ct]}
+        print(name, "done", flush=True)
+    # worker keystream prefixes (oracle restatement, pinned to the reference
+    # through the frames above and tests/test_lasm.py)
+    ks = {}
+    for name in ("C1", "C4"):
+        c = synth.CONFIGS[name]
+        key = out["clips"][name]["key"]
+        o = Oracle(key, c["workers"])
+        ks[name] = [hashlib.sha256(o.worker_stream(i, 1 << 18).tobytes()).hexdigest()
+                    for i in range(c["workers"])]
+    out["worker_stream_sha256_256KiB"] = ks
+    with open(os.path.join(HERE, "lasm.json"), "w") as fh:
+        json.dump(out, fh)
+    print("wrote lasm.json")
+
+
 def _frame_job(arg):
     name, t = arg
     return synth.config_frame(name, t)
@@ -173,5 +252,7 @@ def _frame_job(arg):
 if __name__ == "__main__":
     if "--full-clips" in sys.argv:
         full_clips()
+    elif "--lasm" in sys.argv:
+        lasm()
     else:
         main()

@@ -123,10 +123,24 @@ def test_host_keying_matches_oracle(workers):
     assert seeds.tolist() == [Oracle.lib.orc_cipher_next_seed(o.h) for _ in range(5)]
 
 
-def test_lasm_key_rejected_by_engine():
-    with pytest.raises(cve.CveError) as e:
-        cve.derive_worker_lanes(LASM, 1, 0)
-    assert e.value.status == cve.CVE_ERROR_INVALID_ARGUMENT
+def test_host_keying_lasm_matches_reference_goldens():
+    # test_keying.cpp:181-195 (frozen worker derivation, lasm)
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_unit.json")))
+    w = g["lasm_worker_params_n1"]
+    lanes, seeds = cve.derive_worker_lanes(LASM, 1, 2)
+    assert lanes.tolist() == w["lanes"]
+    assert seeds.tolist() == w["seeds"]
+
+
+@pytest.mark.parametrize("workers", [1, 8, 64])
+def test_host_keying_lasm_matches_oracle(workers):
+    from _oracle import Oracle
+    from paper_2302_07411_b200 import synth
+    key = synth.det_key_lasm(workers + 5)
+    lanes, seeds = cve.derive_worker_lanes(key, workers, 5)
+    o = Oracle(key, workers)
+    assert np.array_equal(lanes, o.params())
+    assert seeds.tolist() == [Oracle.lib.orc_cipher_next_seed(o.h) for _ in range(5)]
 
 
 def test_frame_model():

@@ -122,17 +122,19 @@ def test_decrypt_enforces_geometry_and_key_kind(tmp_path):
 
 
 @pytest.mark.gpu
-def test_raw_video_round_trip_and_auto_directory(tmp_path):
-    # test_capi.cpp:247-284 (with a PLCM key: LASM is out of scope)
+@pytest.mark.parametrize("key", [LASM, PLCM])
+def test_raw_video_round_trip_and_auto_directory(tmp_path, key):
+    # test_capi.cpp:247-284 (the reference runs it with its LASM key)
     data = rgb(8, 8, 10).tobytes() + rgb(8, 8, 11).tobytes()
     put(tmp_path / "video.rgb", data)
     out = str(tmp_path / "video.cve")
-    cve.encrypt_file(PLCM, str(tmp_path / "video.rgb"), out, workers=2, rounds=2, raw=(8, 8))
+    cve.encrypt_file(key, str(tmp_path / "video.rgb"), out, workers=2, rounds=2, raw=(8, 8))
     c = blob(out)
     assert len(c) == 27 + 2 * 8 * 8 * 3 and c[23] == 2
-    cve.decrypt_file(PLCM, out, str(tmp_path / "back.rgb"), fmt=cve.CVE_OUT_RAW)
+    assert c[5] == (1 if key == LASM else 0)  # map kind byte
+    cve.decrypt_file(key, out, str(tmp_path / "back.rgb"), fmt=cve.CVE_OUT_RAW)
     assert blob(tmp_path / "back.rgb") == data
-    cve.decrypt_file(PLCM, out, str(tmp_path / "frames"), io=False)
+    cve.decrypt_file(key, out, str(tmp_path / "frames"), io=False)
     assert (tmp_path / "frames" / "frame_000000.ppm").exists()
     assert (tmp_path / "frames" / "frame_000001.ppm").exists()
 
@@ -149,6 +151,38 @@ def test_nist_export_matches_reference(tmp_path, workers, count):
     ours = blob(tmp_path / "ours.bin")
     assert len(ours) == count
     assert ours == blob(tmp_path / "ref.bin")
+
+
+@pytest.mark.gpu
+@need_ref
+@pytest.mark.parametrize("workers,count", [(2, 100001), (64, 5 << 18)])
+def test_nist_export_lasm_matches_reference(tmp_path, workers, count):
+    # row f3 with a LASM key (12 bytes per generator iteration)
+    key = synth.det_key_lasm(31)
+    cve.nist_export(key, workers, count, str(tmp_path / "ours.bin"))
+    assert Reference.load().cve_nist_export(key.encode(), workers, count,
+                                            str(tmp_path / "ref.bin").encode()) == 0
+    assert blob(tmp_path / "ours.bin") == blob(tmp_path / "ref.bin")
+
+
+@pytest.mark.gpu
+@need_ref
+def test_lasm_container_matches_reference(tmp_path):
+    # row f1 with a LASM key: the CVE1 container is byte-identical to the
+    # reference's, and each side decrypts the other's
+    frames = [rgb(50, 30, s) for s in (3, 4, 5)]
+    d = tmp_path / "seq"
+    d.mkdir()
+    for i, f in enumerate(frames):
+        put(d / f"frame_{i:06d}.ppm", p6(50, 30, f))
+    key = synth.det_key_lasm(77)
+    ours, ref = str(tmp_path / "ours.cve"), str(tmp_path / "ref.cve")
+    cve.encrypt_file(key, str(d), ours, workers=4, rounds=5)
+    assert ref_encrypt_file(key, str(d), ref, workers=4, rounds=5) == 0
+    assert blob(ours) == blob(ref)
+    cve.decrypt_file(key, ref, str(tmp_path / "back"))
+    for i, f in enumerate(frames):
+        assert blob(tmp_path / "back" / f"frame_{i:06d}.ppm") == p6(50, 30, f)
 
 
 # ---- CPU: argument and format checks (raised before any device work) --------
