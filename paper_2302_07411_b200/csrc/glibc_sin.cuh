@@ -13,7 +13,7 @@
 // below 105414350), in the operation order and FMA contractions of the
 // `sin` ifunc variant the dynamic linker selects on hosts with FMA + AVX2
 // (every B200 host).  The polynomial and reduction constants are the
-// algorithm's published coefficients; the 111-entry sin/cos table is read
+// algorithm's published coefficients; the 110-entry sin/cos table is read
 // from the installed libm at build time (gen_sincostab.py -> the generated
 // glibc_sincostab.inc), because its low parts are not reproducible by
 // recomputation.  Parity is pinned by tests/test_lasm.py against the host's
@@ -39,8 +39,8 @@
 
 namespace gsin {
 
-// Entries {sin hi, sin lo, cos hi, cos lo} of k/128, k = 0..110.
-constexpr int kTableDoubles = 444;
+// Entries {sin hi, sin lo, cos hi, cos lo} of k/128, k = 0..109.
+constexpr int kTableDoubles = 440;
 
 // Coefficients (hex-exact).
 constexpr double kBig = 0x1.8p45;              // rounds |x| to a multiple of 2^-7
@@ -131,7 +131,7 @@ GSIN_HD double cos_tab(double a, double da, const double* tab) {
   return cs + cor;
 }
 
-// glibc sin(x), |x| < 105414350; `tab` = the 444 table doubles.
+// glibc sin(x), |x| < 105414350; `tab` = the 440 table doubles.
 GSIN_HD double sin(double x, const double* tab) {
   const uint32_t k = (uint32_t)(bits(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e500000u) return x;  // |x| < 2^-26
@@ -140,7 +140,7 @@ GSIN_HD double sin(double x, const double* tab) {
     if (ax < kTaylorMax) return taylor(x, 0.0);
     return sin_tab(x, 0.0, tab);
   }
-  if (k < 0x400368fdu) {          // |x| < 2.426265: cos(pi/2 - |x|)
+  if (k < 0x400368fdu) {          // |x| < 0x1.368fdp+1 (2.4262638): cos(pi/2 - |x|)
     const double ax = from_bits(bits(x) & 0x7fffffffffffffffull);
     const double t = kHp0 - ax;
     return copysign_of(cos_tab(t, kHp1, tab), x);
@@ -165,6 +165,40 @@ GSIN_HD double sin(double x, const double* tab) {
     return (n & 2u) ? -r : r;
   }
   return from_bits(0x7ff8000000000000ull);  // outside the supported domain
+}
+
+// The same function, arranged for a latency-bound chain (the LASM map).
+// 98% of LASM arguments lie in [2^-26, 2.4262638): glibc's Taylor, sin-table
+// and cos(pi/2 - x)-table branches.  Here those three are evaluated without
+// branches -- one shared table walk whose four table operands are permuted
+// by index select (sin_tab and cos_tab are the same three-FMA correction with
+// the table entries in a different order), the Taylor series beside it, one
+// select at the end -- so no data-dependent branch sits on the chain.  The
+// remaining arguments (tiny, Cody-Waite reduction, negative, NaN) take the
+// general routine above.  Every operation is the one glibc performs for that
+// argument; selects only choose which result is kept.  For x > 0 the results
+// of the three branches are positive, so glibc's copysign is the identity.
+GSIN_HD double sin_fast(double x, const double* tab) {
+  if (!(x >= 0x1p-26 && x < 0x1.368fdp+1)) return sin(x, tab);
+  const bool is_cos = x >= 0x1.b6p-1;  // glibc's |x| >= 0.855469 branch
+  const double t = kHp0 - x;
+  const double at = from_bits(bits(t) & 0x7fffffffffffffffull);
+  const double a = is_cos ? at : x;
+  const double u = kBig + a;
+  const int k = (int)((uint32_t)bits(u) << 2);
+  const double dx = is_cos ? (t < 0.0 ? -kHp1 : kHp1) : 0.0;
+  const double xr = (a - (u - kBig)) + dx;  // + 0.0 is exact (a - (u - big) >= +0)
+  const double xx = xr * xr;
+  const double x3 = xr * xx;
+  const double ps = fmad(xx, kSn5, kSn3);
+  const double c = xx * fmad(xx, fmad(xx, kCs6, kCs4), kCs2);
+  // sin_tab: s = x + fma(x^3, ps, +0), cor = fma(s, cs, fma(-c, sn, fma(s, ccs, ssn)))
+  // cos_tab: s = fma(x^3, ps, x),      cor = fma(-s, sn, fma(-c, cs, fma(-s, ssn, ccs)))
+  const double sv = is_cos ? -fmad(x3, ps, xr) : xr + fmad(x3, ps, 0.0);
+  const double t1 = tab[k + (is_cos ? 1 : 3)], t2 = tab[k + (is_cos ? 3 : 1)];
+  const double t3 = tab[k + (is_cos ? 2 : 0)], t4 = tab[k + (is_cos ? 0 : 2)];
+  const double r = t3 + fmad(sv, t4, fmad(-c, t3, fmad(sv, t1, t2)));
+  return x < kTaylorMax ? taylor(x, 0.0) : r;
 }
 
 }  // namespace gsin

@@ -147,8 +147,8 @@ def test_gpu_sin_matches_libm():
     import paper_2302_07411_b200 as cve
     rng = np.random.Generator(np.random.PCG64(7))
     parts = [rng.uniform(lo, hi, 150_000) for lo, hi in
-             ((0, 2 ** -26), (2 ** -26, 0.126), (0.126, 0.85546875), (0.85546875, 2.4262695),
-              (2.4262650, 2.4262696), (2.4262695, math.pi), (math.pi, 26.0), (-26.0, 0.0))]
+             ((0, 2 ** -26), (2 ** -26, 0.126), (0.126, 0.85546875), (0.85546875, 2.4262639),
+              (2.4262600, 2.4262700), (2.4262638, math.pi), (math.pi, 26.0), (-26.0, 0.0))]
     x = np.concatenate(parts)
     got = cve.glibc_sin(x)
     want = np.array([math.sin(v) for v in x])  # CPython's math.sin is libm sin
