@@ -167,38 +167,4 @@ GSIN_HD double sin(double x, const double* tab) {
   return from_bits(0x7ff8000000000000ull);  // outside the supported domain
 }
 
-// The same function, arranged for a latency-bound chain (the LASM map).
-// 98% of LASM arguments lie in [2^-26, 2.4262638): glibc's Taylor, sin-table
-// and cos(pi/2 - x)-table branches.  Here those three are evaluated without
-// branches -- one shared table walk whose four table operands are permuted
-// by index select (sin_tab and cos_tab are the same three-FMA correction with
-// the table entries in a different order), the Taylor series beside it, one
-// select at the end -- so no data-dependent branch sits on the chain.  The
-// remaining arguments (tiny, Cody-Waite reduction, negative, NaN) take the
-// general routine above.  Every operation is the one glibc performs for that
-// argument; selects only choose which result is kept.  For x > 0 the results
-// of the three branches are positive, so glibc's copysign is the identity.
-GSIN_HD double sin_fast(double x, const double* tab) {
-  if (!(x >= 0x1p-26 && x < 0x1.368fdp+1)) return sin(x, tab);
-  const bool is_cos = x >= 0x1.b6p-1;  // glibc's |x| >= 0.855469 branch
-  const double t = kHp0 - x;
-  const double at = from_bits(bits(t) & 0x7fffffffffffffffull);
-  const double a = is_cos ? at : x;
-  const double u = kBig + a;
-  const int k = (int)((uint32_t)bits(u) << 2);
-  const double dx = is_cos ? (t < 0.0 ? -kHp1 : kHp1) : 0.0;
-  const double xr = (a - (u - kBig)) + dx;  // + 0.0 is exact (a - (u - big) >= +0)
-  const double xx = xr * xr;
-  const double x3 = xr * xx;
-  const double ps = fmad(xx, kSn5, kSn3);
-  const double c = xx * fmad(xx, fmad(xx, kCs6, kCs4), kCs2);
-  // sin_tab: s = x + fma(x^3, ps, +0), cor = fma(s, cs, fma(-c, sn, fma(s, ccs, ssn)))
-  // cos_tab: s = fma(x^3, ps, x),      cor = fma(-s, sn, fma(-c, cs, fma(-s, ssn, ccs)))
-  const double sv = is_cos ? -fmad(x3, ps, xr) : xr + fmad(x3, ps, 0.0);
-  const double t1 = tab[k + (is_cos ? 1 : 3)], t2 = tab[k + (is_cos ? 3 : 1)];
-  const double t3 = tab[k + (is_cos ? 2 : 0)], t4 = tab[k + (is_cos ? 0 : 2)];
-  const double r = t3 + fmad(sv, t4, fmad(-c, t3, fmad(sv, t1, t2)));
-  return x < kTaylorMax ? taylor(x, 0.0) : r;
-}
-
 }  // namespace gsin

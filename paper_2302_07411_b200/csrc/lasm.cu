@@ -48,8 +48,8 @@ __device__ __forceinline__ void lasm_walk(double& x, double& y, double pm, const
                                           uint32_t iters, double2* out) {
 #pragma unroll 1
   for (uint32_t i = 0; i < iters; ++i) {
-    x = gsin::sin_fast(pm * (y + 3.0) * x * (1.0 - x), tab);
-    y = gsin::sin_fast(pm * (x + 3.0) * y * (1.0 - y), tab);
+    x = gsin::sin(pm * (y + 3.0) * x * (1.0 - x), tab);
+    y = gsin::sin(pm * (x + 3.0) * y * (1.0 - y), tab);
     if (out) out[i] = make_double2(x, y);
   }
 }
@@ -118,7 +118,7 @@ __global__ void k_glibc_sin(const double* __restrict__ x, double* __restrict__ y
   load_table(tab);
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
-    y[i] = gsin::sin_fast(x[i], tab);
+    y[i] = gsin::sin(x[i], tab);
 }
 
 uint32_t lasm_ctas(uint32_t nlanes) { return (nlanes + kLanesPerCta - 1) / kLanesPerCta; }
