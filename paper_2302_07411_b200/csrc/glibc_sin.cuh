@@ -29,8 +29,10 @@
 
 #if defined(__CUDACC__)
 #define GSIN_HD __host__ __device__ __forceinline__
+#define GSIN_MEMBER __host__ __device__ __forceinline__
 #else
 #define GSIN_HD static inline
+#define GSIN_MEMBER inline
 #endif
 
 #ifndef __CUDA_ARCH__
@@ -86,6 +88,27 @@ GSIN_HD double from_bits(uint64_t u) {
 
 GSIN_HD double fmad(double a, double b, double c) { return fma(a, b, c); }
 
+// Table access.  Host code indexes a plain array; device code may use
+// SmemTable, whose 32-bit shared-memory address is formed once per kernel
+// (indexing a generic pointer to shared memory made ptxas re-derive the
+// shared window base -- S2UR SR_CgaCtaId -- in front of every table load on
+// the chain, measured ~100 cycles per LASM iteration).
+struct PtrTable {
+  const double* p;
+  GSIN_MEMBER double operator()(int i) const { return p[i]; }
+};
+
+#ifdef __CUDACC__
+struct SmemTable {
+  uint32_t base;  // __cvta_generic_to_shared of the table
+  __device__ __forceinline__ double operator()(int i) const {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
+    return v;
+  }
+};
+#endif
+
 GSIN_HD double copysign_of(double mag, double sgn) {
   return from_bits((bits(mag) & 0x7fffffffffffffffull) | (bits(sgn) & 0x8000000000000000ull));
 }
@@ -102,7 +125,8 @@ GSIN_HD double taylor(double a, double da) {
 }
 
 // sin(a + da) for 0.126 <= |a| <= 0.8555 via the table at k/128.
-GSIN_HD double sin_tab(double a, double da, const double* tab) {
+template <class Tab>
+GSIN_HD double sin_tab(double a, double da, const Tab& tab) {
   const double ax = from_bits(bits(a) & 0x7fffffffffffffffull);
   if (a <= 0.0) da = -da;
   const double u = kBig + ax;
@@ -111,13 +135,14 @@ GSIN_HD double sin_tab(double a, double da, const double* tab) {
   const double xx = x * x;
   const double s = x + fmad(x * xx, fmad(xx, kSn5, kSn3), da);
   const double c = fmad(x, da, xx * fmad(xx, fmad(xx, kCs6, kCs4), kCs2));
-  const double sn = tab[k], ssn = tab[k + 1], cs = tab[k + 2], ccs = tab[k + 3];
+  const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
   const double cor = fmad(s, cs, fmad(-c, sn, fmad(s, ccs, ssn)));
   return copysign_of(sn + cor, a);
 }
 
 // cos(a + da) for |a| <= 0.8555 via the table at k/128.
-GSIN_HD double cos_tab(double a, double da, const double* tab) {
+template <class Tab>
+GSIN_HD double cos_tab(double a, double da, const Tab& tab) {
   const double ax = from_bits(bits(a) & 0x7fffffffffffffffull);
   if (a < 0.0) da = -da;
   const double u = kBig + ax;
@@ -126,13 +151,14 @@ GSIN_HD double cos_tab(double a, double da, const double* tab) {
   const double xx = x * x;
   const double s = fmad(x * xx, fmad(xx, kSn5, kSn3), x);
   const double c = xx * fmad(xx, fmad(xx, kCs6, kCs4), kCs2);
-  const double sn = tab[k], ssn = tab[k + 1], cs = tab[k + 2], ccs = tab[k + 3];
+  const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
   const double cor = fmad(-s, sn, fmad(-c, cs, fmad(-s, ssn, ccs)));
   return cs + cor;
 }
 
 // glibc sin(x), |x| < 105414350; `tab` = the 440 table doubles.
-GSIN_HD double sin(double x, const double* tab) {
+template <class Tab>
+GSIN_HD double sin(double x, const Tab& tab) {
   const uint32_t k = (uint32_t)(bits(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e500000u) return x;  // |x| < 2^-26
   if (k < 0x3feb6000u) {          // |x| < 0.855469
@@ -166,5 +192,7 @@ GSIN_HD double sin(double x, const double* tab) {
   }
   return from_bits(0x7ff8000000000000ull);  // outside the supported domain
 }
+
+GSIN_HD double sin(double x, const double* tab) { return sin(x, PtrTable{tab}); }
 
 }  // namespace gsin

@@ -11,10 +11,13 @@
 // (glibc_sin.cuh) performs glibc's own operation sequence, so every value is
 // the reference's by construction (pinned by tests/test_lasm.py).  sin's
 // branches depend on the argument, so lanes in one warp would diverge and
-// serialise their paths; each lane therefore runs alone in its warp (lane =
-// warp), four warps per CTA (one per SM sub-partition).  The orbit values go
-// to a lane-major buffer, and a second, fully parallel kernel XORs the two
-// lanes of each worker into the keystream ring.
+// serialise their paths; each lane therefore runs alone in its own CTA, as
+// thread 0 (`if (threadIdx.x) return`): the compiler then knows the thread
+// is alone in its warp and emits the branches without reconvergence
+// barriers (BSSY/BSYNC), 600 -> 504 cycles per iteration on B200
+// (tools/lasm_latency.cu).  The orbit values go to a lane-major buffer, and a
+// second, fully parallel kernel XORs the two lanes of each worker into the
+// keystream ring.
 //
 // Compiled with -fmad=false: every fused multiply-add is an explicit fma()
 // mirroring glibc's, nothing else is contracted.
@@ -34,18 +37,21 @@ __device__ const double g_sintab[gsin::kTableDoubles] = {
 };
 
 constexpr double kPi = 0x1.921fb54442d18p1;  // std::numbers::pi
-constexpr int kLanesPerCta = 4;               // one warp per sub-partition
+constexpr int kCtaThreads = 32;  // thread 0 runs the lane; the warp loads the table
 
-__device__ __forceinline__ void load_table(double* tab) {
+// Copies the table into shared memory; returns its shared-window address.
+__device__ __forceinline__ gsin::SmemTable load_table(double* tab) {
   for (int i = threadIdx.x; i < gsin::kTableDoubles; i += blockDim.x) tab[i] = g_sintab[i];
   __syncthreads();
+  return gsin::SmemTable{uint32_t(__cvta_generic_to_shared(tab))};
 }
 
 // `iters` LASM iterations of one lane from (x, y); orbit values to out[i]
 // when out != nullptr.  chaos.cpp:34-38, evaluated left to right:
 // ((((pi*mu)*(y+3))*x)*(1-x)).
-__device__ __forceinline__ void lasm_walk(double& x, double& y, double pm, const double* tab,
-                                          uint32_t iters, double2* out) {
+__device__ __forceinline__ void lasm_walk(double& x, double& y, double pm,
+                                          const gsin::SmemTable& tab, uint32_t iters,
+                                          double2* out) {
 #pragma unroll 1
   for (uint32_t i = 0; i < iters; ++i) {
     x = gsin::sin(pm * (y + 3.0) * x * (1.0 - x), tab);
@@ -55,25 +61,25 @@ __device__ __forceinline__ void lasm_walk(double& x, double& y, double pm, const
 }
 
 // 256 warm-up iterations from the derived start points (chaos.cpp:93-107).
-__global__ void __launch_bounds__(32 * kLanesPerCta)
+__global__ void __launch_bounds__(kCtaThreads)
     k_lasm_init(double2* state, const double* mu, const double2* xy0, uint32_t nlanes) {
-  __shared__ double tab[gsin::kTableDoubles];
-  load_table(tab);
-  const uint32_t lane = blockIdx.x * kLanesPerCta + threadIdx.x / 32;
-  if ((threadIdx.x & 31) || lane >= nlanes) return;
+  __shared__ double smem[gsin::kTableDoubles];
+  const gsin::SmemTable tab = load_table(smem);
+  const uint32_t lane = blockIdx.x;
+  if (threadIdx.x || lane >= nlanes) return;
   double x = xy0[lane].x, y = xy0[lane].y;
   lasm_walk(x, y, kPi * mu[lane], tab, 256, nullptr);
   state[lane] = make_double2(x, y);
 }
 
 // Chain: every lane advances `iters` iterations; orbit[lane*max_iters + i].
-__global__ void __launch_bounds__(32 * kLanesPerCta)
+__global__ void __launch_bounds__(kCtaThreads)
     k_lasm_chain(double2* state, const double* mu, double2* orbit, uint32_t max_iters,
                  uint32_t iters, uint32_t nlanes) {
-  __shared__ double tab[gsin::kTableDoubles];
-  load_table(tab);
-  const uint32_t lane = blockIdx.x * kLanesPerCta + threadIdx.x / 32;
-  if ((threadIdx.x & 31) || lane >= nlanes) return;
+  __shared__ double smem[gsin::kTableDoubles];
+  const gsin::SmemTable tab = load_table(smem);
+  const uint32_t lane = blockIdx.x;
+  if (threadIdx.x || lane >= nlanes) return;
   double x = state[lane].x, y = state[lane].y;
   lasm_walk(x, y, kPi * mu[lane], tab, iters, orbit + uint64_t(lane) * max_iters);
   state[lane] = make_double2(x, y);
@@ -114,25 +120,24 @@ __global__ void k_lasm_emit(const double2* __restrict__ orbit, uint32_t max_iter
 }
 
 __global__ void k_glibc_sin(const double* __restrict__ x, double* __restrict__ y, size_t n) {
-  __shared__ double tab[gsin::kTableDoubles];
-  load_table(tab);
+  __shared__ double smem[gsin::kTableDoubles];
+  const gsin::SmemTable tab = load_table(smem);
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
     y[i] = gsin::sin(x[i], tab);
 }
 
-uint32_t lasm_ctas(uint32_t nlanes) { return (nlanes + kLanesPerCta - 1) / kLanesPerCta; }
 
 }  // namespace
 
 void launch_lasm_init(double2* state, const double* mu, const double2* xy0, uint32_t nlanes,
                       cudaStream_t s) {
-  k_lasm_init<<<lasm_ctas(nlanes), 32 * kLanesPerCta, 0, s>>>(state, mu, xy0, nlanes);
+  k_lasm_init<<<nlanes, kCtaThreads, 0, s>>>(state, mu, xy0, nlanes);
 }
 
 void launch_lasm_chain(const LasmBuffers& b, int slot, uint32_t iters, uint32_t nlanes,
                        cudaStream_t s) {
-  k_lasm_chain<<<lasm_ctas(nlanes), 32 * kLanesPerCta, 0, s>>>(
+  k_lasm_chain<<<nlanes, kCtaThreads, 0, s>>>(
       b.state, b.mu, b.orbit[slot], b.max_iters, iters, nlanes);
 }
 

@@ -17,9 +17,10 @@ __device__ const double g_tab[gsin::kTableDoubles] = {
 
 template <int V>
 __global__ void k(double* out, long long* cyc, int iters, double x0, double y0, double mu) {
-  __shared__ double tab[gsin::kTableDoubles];
-  for (int i = threadIdx.x; i < gsin::kTableDoubles; i += blockDim.x) tab[i] = g_tab[i];
+  __shared__ double smem[gsin::kTableDoubles];
+  for (int i = threadIdx.x; i < gsin::kTableDoubles; i += blockDim.x) smem[i] = g_tab[i];
   __syncthreads();
+  const gsin::SmemTable tab{uint32_t(__cvta_generic_to_shared(smem))};
   if (threadIdx.x) return;
   double x = x0, y = y0;
   const double pm = 0x1.921fb54442d18p1 * mu;
@@ -63,7 +64,42 @@ void run(const char* name, double x0, double y0, double mu) {
   cudaFree(d); cudaFree(c);
 }
 
+// The product's configuration: one active lane per warp, `warps` warps per
+// CTA, optionally storing each (x, y) like k_lasm_chain.
+__global__ void k_multi(double2* orbit, long long* cyc, int iters, int warps, int store) {
+  __shared__ double smem[gsin::kTableDoubles];
+  for (int i = threadIdx.x; i < gsin::kTableDoubles; i += blockDim.x) smem[i] = g_tab[i];
+  __syncthreads();
+  const gsin::SmemTable tab{uint32_t(__cvta_generic_to_shared(smem))};
+  const int w = threadIdx.x / 32;
+  if ((threadIdx.x & 31) || w >= warps) return;
+  double x = 0.3 + 0.01 * w, y = 0.7, pm = 0x1.921fb54442d18p1 * 0.9;
+  double2* out = orbit + (size_t)w * iters;
+  long long t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < iters; ++i) {
+    x = gsin::sin(pm * (y + 3.0) * x * (1.0 - x), tab);
+    y = gsin::sin(pm * (x + 3.0) * y * (1.0 - y), tab);
+    if (store) out[i] = make_double2(x, y);
+  }
+  long long t1 = clock64();
+  if (w == 0) cyc[0] = t1 - t0;
+}
+
+void run_multi(int warps, int store) {
+  double2* o; long long* c;
+  const int iters = 20000;
+  cudaMalloc(&o, sizeof(double2) * iters * 8); cudaMalloc(&c, 8);
+  k_multi<<<1, 256>>>(o, c, 100, warps, store);
+  k_multi<<<1, 256>>>(o, c, iters, warps, store);
+  long long h; cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("lasm step, %d warps/CTA, store %d %8.1f cycles/iter\n", warps, store, double(h) / iters);
+  cudaFree(o); cudaFree(c);
+}
+
 int main() {
+  for (int w : {1, 2, 4, 8})
+    for (int st : {0, 1}) run_multi(w, st);
   run<0>("arg only (2 halves)", 0.3, 0.7, 0.9);
   run<1>("lasm step, gsin::sin", 0.3, 0.7, 0.9);
   run<3>("16 x DFMA", 0.3, 0.999, 0.9);
