@@ -124,9 +124,10 @@ GSIN_HD double taylor(double a, double da) {
   return fmad(xx, t, da) + a;
 }
 
-// sin(a + da) for 0.126 <= |a| <= 0.8555 via the table at k/128.
+// |sin(a + da)| for 0.126 <= |a| <= 0.8555 via the table at k/128 (glibc
+// returns it with the sign of a).
 template <class Tab>
-GSIN_HD double sin_tab(double a, double da, const Tab& tab) {
+GSIN_HD double sin_tab_mag(double a, double da, const Tab& tab) {
   const double ax = from_bits(bits(a) & 0x7fffffffffffffffull);
   if (a <= 0.0) da = -da;
   const double u = kBig + ax;
@@ -137,7 +138,12 @@ GSIN_HD double sin_tab(double a, double da, const Tab& tab) {
   const double c = fmad(x, da, xx * fmad(xx, fmad(xx, kCs6, kCs4), kCs2));
   const double sn = tab(k), ssn = tab(k + 1), cs = tab(k + 2), ccs = tab(k + 3);
   const double cor = fmad(s, cs, fmad(-c, sn, fmad(s, ccs, ssn)));
-  return copysign_of(sn + cor, a);
+  return sn + cor;
+}
+
+template <class Tab>
+GSIN_HD double sin_tab(double a, double da, const Tab& tab) {
+  return copysign_of(sin_tab_mag(a, da, tab), a);
 }
 
 // cos(a + da) for |a| <= 0.8555 via the table at k/128.
@@ -194,5 +200,26 @@ GSIN_HD double sin(double x, const Tab& tab) {
 }
 
 GSIN_HD double sin(double x, const double* tab) { return sin(x, PtrTable{tab}); }
+
+// sin(x) again, arranged for the LASM chain, whose arguments
+// pi*mu*(y+3)*x*(1-x) lie in [0, pi] up to rounding:
+//  * glibc's cos(pi/2 - x) branch, 44% of LASM arguments, is tested first,
+//    with one branch;
+//  * the two range tests read the raw high word, so a negative x fails both;
+//    for positive x every one of these branches yields a positive value, so
+//    glibc's copysign(result, x) is the identity and is left out (it cost an
+//    integer round trip on the chain).
+// Everything else (tiny, the Cody-Waite branch, negative, NaN) takes sin()
+// itself, so sin_0pi(x) == sin(x) for every x.
+template <class Tab>
+GSIN_HD double sin_0pi(double x, const Tab& tab) {
+  const uint32_t k = (uint32_t)(bits(x) >> 32);  // sign bit clear on the domain
+  if (k >= 0x3feb6000u && k < 0x400368fdu) return cos_tab(kHp0 - x, kHp1, tab);
+  if (k >= 0x3e500000u && k < 0x3feb6000u)
+    return x < kTaylorMax ? taylor(x, 0.0) : sin_tab_mag(x, 0.0, tab);
+  return sin(x, tab);
+}
+
+GSIN_HD double sin_0pi(double x, const double* tab) { return sin_0pi(x, PtrTable{tab}); }
 
 }  // namespace gsin

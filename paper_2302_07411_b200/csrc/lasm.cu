@@ -47,16 +47,18 @@ __device__ __forceinline__ gsin::SmemTable load_table(double* tab) {
 }
 
 // `iters` LASM iterations of one lane from (x, y); orbit values to out[i]
-// when out != nullptr.  chaos.cpp:34-38, evaluated left to right:
-// ((((pi*mu)*(y+3))*x)*(1-x)).
+// when kStore.  chaos.cpp:34-38, evaluated left to right:
+// ((((pi*mu)*(y+3))*x)*(1-x)).  sin_0pi is sin() with the branches LASM
+// arguments take ordered for the chain.
+template <bool kStore>
 __device__ __forceinline__ void lasm_walk(double& x, double& y, double pm,
                                           const gsin::SmemTable& tab, uint32_t iters,
                                           double2* out) {
 #pragma unroll 1
   for (uint32_t i = 0; i < iters; ++i) {
-    x = gsin::sin(pm * (y + 3.0) * x * (1.0 - x), tab);
-    y = gsin::sin(pm * (x + 3.0) * y * (1.0 - y), tab);
-    if (out) out[i] = make_double2(x, y);
+    x = gsin::sin_0pi(pm * (y + 3.0) * x * (1.0 - x), tab);
+    y = gsin::sin_0pi(pm * (x + 3.0) * y * (1.0 - y), tab);
+    if (kStore) out[i] = make_double2(x, y);
   }
 }
 
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kCtaThreads)
   const uint32_t lane = blockIdx.x;
   if (threadIdx.x || lane >= nlanes) return;
   double x = xy0[lane].x, y = xy0[lane].y;
-  lasm_walk(x, y, kPi * mu[lane], tab, 256, nullptr);
+  lasm_walk<false>(x, y, kPi * mu[lane], tab, 256, nullptr);
   state[lane] = make_double2(x, y);
 }
 
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(kCtaThreads)
   const uint32_t lane = blockIdx.x;
   if (threadIdx.x || lane >= nlanes) return;
   double x = state[lane].x, y = state[lane].y;
-  lasm_walk(x, y, kPi * mu[lane], tab, iters, orbit + uint64_t(lane) * max_iters);
+  lasm_walk<true>(x, y, kPi * mu[lane], tab, iters, orbit + uint64_t(lane) * max_iters);
   state[lane] = make_double2(x, y);
 }
 

@@ -1,6 +1,7 @@
 // Test helper (tests/test_lasm.py): compares the product's host/device
 // restatement of glibc sin (paper_2302_07411_b200/csrc/glibc_sin.cuh, host
-// build) with this host's libm sin() bit for bit, over seeded random
+// build: gsin::sin and the chain's arrangement gsin::sin_0pi) with this
+// host's libm sin() bit for bit, over seeded random
 // arguments in every branch of the algorithm, every double around the
 // branch edges, and whole LASM orbits (chaos.cpp:34-38).
 // Prints "<cases> <mismatches>" and the first mismatches.
@@ -18,9 +19,19 @@ static const double kTab[gsin::kTableDoubles] = {
 
 static long cases = 0, bad = 0;
 
+// sin_0pi: the LASM chain's arrangement of the same function
+static void check_0pi(double x) {
+  const double a = gsin::sin_0pi(x, kTab), w = std::sin(x);
+  if (std::memcmp(&a, &w, 8) != 0) {
+    if (bad < 5) std::printf("sin_0pi x=%a ours=%a libm=%a\n", x, a, w);
+    ++bad;
+  }
+}
+
 static void check(double x) {
   const double a = gsin::sin(x, kTab), w = std::sin(x);
   ++cases;
+  check_0pi(x);
   if (std::memcmp(&a, &w, 8) != 0) {
     if (bad < 5) std::printf("x=%a ours=%a libm=%a\n", x, a, w);
     ++bad;

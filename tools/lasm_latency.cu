@@ -33,6 +33,9 @@ __global__ void k(double* out, long long* cyc, int iters, double x0, double y0, 
     } else if (V == 1) {  // general glibc sin
       x = gsin::sin(pm * (y + 3.0) * x * (1.0 - x), tab);
       y = gsin::sin(pm * (x + 3.0) * y * (1.0 - y), tab);
+    } else if (V == 2) {  // the chain's arrangement
+      x = gsin::sin_0pi(pm * (y + 3.0) * x * (1.0 - x), tab);
+      y = gsin::sin_0pi(pm * (x + 3.0) * y * (1.0 - y), tab);
     } else if (V == 3) {  // 16 dependent DFMA
 #pragma unroll
       for (int j = 0; j < 16; ++j) x = fma(x, y, 1e-3);
@@ -102,6 +105,7 @@ int main() {
     for (int st : {0, 1}) run_multi(w, st);
   run<0>("arg only (2 halves)", 0.3, 0.7, 0.9);
   run<1>("lasm step, gsin::sin", 0.3, 0.7, 0.9);
+  run<2>("lasm step, sin_0pi", 0.3, 0.7, 0.9);
   run<3>("16 x DFMA", 0.3, 0.999, 0.9);
   run<4>("16 x DADD", 0.3, 1e-9, 0.9);
   run<5>("2 x taylor", 0.3, 0.7, 0.9);
