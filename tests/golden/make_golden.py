@@ -197,7 +197,7 @@ def full_clips() -> None:
 
 
 # LASM geometries (row f2): (config geometry, frames recorded)
-LASM_CLIPS = {"C1": 2, "C2": 4, "C3": 3, "C4": 2}
+LASM_CLIPS = {"C1": 2, "C2": 4, "C3": 3, "C4": 2, "C5": 2}
 
 
 def lasm() -> None:
