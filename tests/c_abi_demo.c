@@ -4,7 +4,7 @@
  * and link check, no-GPU failure mode) and tests/test_gpu_parity.py (GPU:
  * round trip and ciphertext digest).
  *
- *   argv[1]: key hex;  prints "ok <xor of all ciphertext bytes>" on success,
+ *   argv[1]: key hex (PLCM or LASM);  prints "ok <xor of all ciphertext bytes>" on success,
  *   "nogpu <status>" when the cipher cannot be created. */
 #include <stdio.h>
 #include <stdlib.h>
@@ -16,7 +16,7 @@ int main(int argc, char** argv) {
   const char* key = argc > 1 ? argv[1]
                              : "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f";
   cve_map_kind kind;
-  if (cve_key_validate(key, &kind) != CVE_OK || kind != CVE_MAP_PLCM) {
+  if (cve_key_validate(key, &kind) != CVE_OK || (kind != CVE_MAP_PLCM && kind != CVE_MAP_LASM)) {
     printf("badkey %s\n", cve_last_error());
     return 2;
   }

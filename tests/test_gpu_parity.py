@@ -413,14 +413,15 @@ def test_c_caller_matches_oracle(tmp_path):
     subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
                     os.path.join(root, "tests", "c_abi_demo.c"), "-o", exe, "-L", libdir,
                     "-lcve_b200", "-Wl,-rpath," + libdir], check=True, capture_output=True)
-    out = subprocess.run([exe, PLCM], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stdout + out.stderr
-    side, n = 96, 96 * 96 * 3
-    f = np.array([((i * 2654435761) >> 24) & 0xFF for i in range(n)], np.uint8)
-    f = f.reshape(side, side, 3)
-    assert Oracle(PLCM, 8, 5).encrypt(f) == 0
-    x = 0
-    for i, b in enumerate(f.ravel().tolist()):
-        x ^= b << (8 * (i & 3))
-    assert out.stdout.split()[:2] == ["ok", f"{x:08x}"], out.stdout
-    assert "seeds=1" in out.stdout
+    for key in (PLCM, synth.det_key_lasm(3)):
+        out = subprocess.run([exe, key], capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stdout + out.stderr
+        side, n = 96, 96 * 96 * 3
+        f = np.array([((i * 2654435761) >> 24) & 0xFF for i in range(n)], np.uint8)
+        f = f.reshape(side, side, 3)
+        assert Oracle(key, 8, 5).encrypt(f) == 0
+        x = 0
+        for i, b in enumerate(f.ravel().tolist()):
+            x ^= b << (8 * (i & 3))
+        assert out.stdout.split()[:2] == ["ok", f"{x:08x}"], (key, out.stdout)
+        assert "seeds=1" in out.stdout

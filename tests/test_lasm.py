@@ -242,3 +242,59 @@ def test_gpu_lasm_random_shapes_vs_reference():
             c.encrypt_frame(a)
             assert ref.encrypt(b) == 0
             assert np.array_equal(a, b), (side, n, r)
+
+
+@pytest.mark.gpu
+def test_gpu_lasm_and_plcm_handles_concurrently():
+    # cve.h:5-6 with both maps: LASM and PLCM handles driven at once from
+    # threads (the two generator kinds share the device); every frame must
+    # match the oracle.
+    import threading
+    import paper_2302_07411_b200 as cve
+    shapes = [(96, 8, True), (120, 4, False), (64, 16, True), (90, 3, False), (48, 4, True)]
+    results = {}
+
+    def run(k, side, n, lasm):
+        key = synth.det_key_lasm(700 + k) if lasm else synth.det_key(700 + k)
+        frames = np.random.Generator(np.random.PCG64(k)).integers(
+            0, 256, (4, side, side, 3), dtype=np.uint8)
+        ct = frames.copy()
+        c = cve.Cipher(key, n, 5)
+        for t in range(len(ct)):
+            c.encrypt_frame(ct[t])
+        results[k] = (key, n, frames, ct)
+
+    ths = [threading.Thread(target=run, args=(k, s, n, l)) for k, (s, n, l) in enumerate(shapes)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert len(results) == len(shapes)
+    for k, (key, n, frames, ct) in results.items():
+        o = Oracle(key, n, 5)
+        for f, g in zip(frames, ct):
+            a = f.copy()
+            assert o.encrypt(a) == 0
+            assert np.array_equal(a, g), k
+
+
+@pytest.mark.gpu
+def test_gpu_lasm_device_resident_and_sides_change():
+    # device-resident API == host API; a handle whose frame side changes
+    # keeps one continuous keystream (engine.cpp:198-205), LASM key
+    torch = pytest.importorskip("torch")
+    import paper_2302_07411_b200 as cve
+    key = synth.det_key_lasm(41)
+    o = Oracle(key, 4, 5)
+    c = cve.Cipher(key, 4, 5)
+    rng = np.random.Generator(np.random.PCG64(41))
+    for side in (64, 96, 64, 128):
+        f = rng.integers(0, 256, (2, side, side, 3), dtype=np.uint8)
+        want = f.copy()
+        for t in range(2):
+            assert o.encrypt(want[t]) == 0
+        dev = torch.from_numpy(f.copy()).cuda()
+        s = torch.cuda.current_stream()
+        c.encrypt_frames_device(dev.data_ptr(), side, 2, s.cuda_stream)
+        s.synchronize()
+        assert np.array_equal(dev.cpu().numpy(), want), side
