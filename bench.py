@@ -409,11 +409,16 @@ def lasm_row(stream, have_ref: bool) -> dict:
     st1 = ci.stats()
     iters = st1["keystream_iters"] - st0["keystream_iters"]
     chain_ms = st1["chain_ms"] - st0["chain_ms"]
+    ns = chain_ms * 1e6 / iters if iters else None
+    per_frame = synth.ROUNDS * side * side * 3 // (12 * n)  # LASM iterations per lane per frame
     row = {"workload": f"LASM key, C4 geometry ({side}^2, n={n}, r=5), {nl} device-resident "
                        "frames after a 2-frame warm-up",
            "value": nl / (ms / 1e3), "unit": "frames/s",
-           "chain": {"ns_per_iteration": chain_ms * 1e6 / iters if iters else None,
-                     "bytes_per_iteration": 12,
+           "note": "includes one run-ahead frame: reads <= N/(N-1) high; chain_bound is the "
+                   "steady-state rate",
+           "chain": {"ns_per_iteration": ns, "bytes_per_iteration": 12,
+                     "iterations_per_lane_per_frame": per_frame,
+                     "chain_bound_frames_per_s": 1e9 / (per_frame * ns) if ns else None,
                      "note": "one LASM iteration = two dependent glibc-exact sin evaluations"}}
     if have_ref:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
