@@ -373,21 +373,31 @@ def test_every_frame_of_config_clips_vs_reference(name):
             t += len(buf)
 
 
-@pytest.mark.parametrize("side", [8, 16, 64, 512])
-@pytest.mark.parametrize("n", [1, 2, 4, 8])
-@pytest.mark.parametrize("r", [1, 5])
+SIDES, WORKERS, ROUNDS = [8, 16, 64, 512], [1, 2, 4, 8], [1, 5]
+
+
+@pytest.mark.parametrize("side", SIDES)
+@pytest.mark.parametrize("n", WORKERS)
+@pytest.mark.parametrize("r", ROUNDS)
 def test_acceptance_grid_vs_oracle(side, n, r):
-    # the reference acceptance suite's round-trip grid (acceptance.cpp:97-384:
-    # sides {8,16,64,512} x workers {1,2,4,8} x rounds {1,5}), here also
-    # byte-compared with the oracle
-    key = synth.det_key(77 + side + n + r)
-    f = rand_frames(side, 1, side * 100 + n * 10 + r)[0]
-    a, b = f.copy(), f.copy()
-    assert Oracle(key, n, r).encrypt(a) == 0
-    cve.Cipher(key, n, r).encrypt_frame(b)
-    assert np.array_equal(a, b)
-    cve.Cipher(key, n, r).decrypt_frame(b)
-    assert np.array_equal(b, f)
+    # the reference acceptance suite's round-trip grid (acceptance.cpp:97-121:
+    # sides {8,16,64,512} x workers {1,2,4,8} x rounds {1,5}, key map by
+    # combination parity -- odd PLCM, even LASM -- seeded 1000 + combo), here
+    # also byte-compared with the oracle over consecutive frames of a handle
+    combo = SIDES.index(side) * 8 + WORKERS.index(n) * 2 + ROUNDS.index(r)
+    key = synth.det_key(1000 + combo) if combo % 2 else synth.det_key_lasm(1000 + combo)
+    frames = rand_frames(side, 3, side * 100 + n * 10 + r)
+    want = frames.copy()
+    o = Oracle(key, n, r)
+    for t in range(len(want)):
+        assert o.encrypt(want[t]) == 0
+    got = frames.copy()
+    enc = cve.Cipher(key, n, r)
+    for t in range(len(got)):
+        enc.encrypt_frame(got[t])
+    assert np.array_equal(got, want)
+    cve.Cipher(key, n, r).decrypt_frames(got)
+    assert np.array_equal(got, frames)
 
 
 def test_workers_change_ciphertext():
