@@ -14,6 +14,9 @@ paper_2302_07411_b200.synth and records:
 * clips.json (--full-clips) -- SHA-256 of the plaintext and of the reference
   ciphertext of EVERY frame of the C3 (240), C4 (1000) and C5 (500) clips
   (SURVEY 8(d) parity gate: per-frame digest equality for every frame).
+* lasm_clips.json (--lasm-full-clips) -- the reference's ciphertext digest of
+  EVERY frame of the C3/C4/C5 clips under a LASM key (the frames' plaintext
+  digests are those of clips.json).
 * lasm.json (--lasm) -- row f2, LASM keys (acceptance.cpp det_key recipe):
   full ciphertexts of small shapes, the reference's per-frame digests of the
   config geometries C1-C4 under a LASM key, and worker keystream digests.
@@ -244,6 +247,30 @@ def lasm() -> None:
     print("wrote lasm.json")
 
 
+def lasm_full_clips() -> None:
+    """Every frame of C3/C4/C5 through the reference with a LASM key."""
+    import multiprocessing as mp
+    out = {}
+    with mp.Pool(max(1, (os.cpu_count() or 2) - 1)) as pool:
+        for name in ("C3", "C4", "C5"):
+            c = synth.CONFIGS[name]
+            key = synth.det_key_lasm(4242 + c["workers"])
+            ref = Reference(key, c["workers"], synth.ROUNDS, 1)
+            cipher_sha = []
+            jobs = ((name, t) for t in range(c["frames"]))
+            for t, f in enumerate(pool.imap(_frame_job, jobs, chunksize=2)):
+                assert ref.encrypt(f) == 0
+                cipher_sha.append(sha(f))
+                if t % 100 == 0:
+                    print(name, t, flush=True)
+            out[name] = {"key": key, "workers": c["workers"], "rounds": synth.ROUNDS,
+                         "frames": c["frames"], "cipher_sha256": cipher_sha}
+            ref.close()
+    with open(os.path.join(HERE, "lasm_clips.json"), "w") as fh:
+        json.dump(out, fh)
+    print("wrote lasm_clips.json")
+
+
 def _frame_job(arg):
     name, t = arg
     return synth.config_frame(name, t)
@@ -252,6 +279,8 @@ def _frame_job(arg):
 if __name__ == "__main__":
     if "--full-clips" in sys.argv:
         full_clips()
+    elif "--lasm-full-clips" in sys.argv:
+        lasm_full_clips()
     elif "--lasm" in sys.argv:
         lasm()
     else:
