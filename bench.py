@@ -382,6 +382,51 @@ def rows_measure(stream) -> dict:
     return rows
 
 
+def one_frame_clip() -> dict:
+    """BASELINE config C1 as specified: one 480x480 frame encrypted then
+    decrypted, each with a fresh handle (create, the drop-in per-frame call on
+    a host buffer, destroy), wall clock, median of 10 after a warm-up; the
+    reference library the same way on the host cores."""
+    import paper_2302_07411_b200 as cve
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Reference  # CPU baseline leg only
+    c = synth.CONFIGS["C1"]
+    key, n = synth.config_key("C1"), c["workers"]
+    plain = synth.config_frame("C1", 0)
+
+    def ours():
+        f = plain.copy()
+        with cve.Cipher(key, n, synth.ROUNDS) as e:
+            e.encrypt_frame(f)
+        with cve.Cipher(key, n, synth.ROUNDS) as d:
+            d.decrypt_frame(f)
+        return f
+
+    def theirs():
+        f = plain.copy()
+        e = Reference(key, n, synth.ROUNDS, 1)
+        assert e.encrypt(f) == 0
+        e.close()
+        d = Reference(key, n, synth.ROUNDS, 1)
+        assert d.decrypt(f) == 0
+        d.close()
+        return f
+
+    out = {"workload": "C1: one 480x480 frame, encrypt then decrypt, a fresh handle for each "
+                       "(create + per-frame call on a host buffer + destroy), median of 10",
+           "unit": "ms per round trip"}
+    legs = [("value", ours)] + ([("reference", theirs)] if Reference.available() else [])
+    for label, fn in legs:
+        assert np.array_equal(fn(), plain)  # warm-up + round-trip check
+        ts = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        out[label] = float(np.median(ts))
+    return out
+
+
 def lasm_row(stream, have_ref: bool) -> dict:
     """Row f2: a LASM key (acceptance det_key recipe) on the C4 geometry.
     Ours: 12 device-resident frames after a 2-frame warm-up, CUDA events on
@@ -622,6 +667,8 @@ def run_b200(args) -> None:
                                  "ms_per_frame": cms / nfr,
                                  "note": "includes one run-ahead frame: reads <= N/(N-1) high"}
             del hh, buf
+        if dist.world == 1:
+            per_config["C1"]["one_frame_clip"] = one_frame_clip()
 
     # ---- labelled multi-clip line: M independent clips (keys) on this GPU ----
     multi = None

@@ -7,9 +7,11 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 #include <string>
+#include <vector>
 
 namespace cveb {
 namespace {
@@ -23,18 +25,121 @@ void ck(cudaError_t e, const char* what) {
 
 uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
+// ---- process-wide device resources -----------------------------------------
+// Handles are cheap to create and destroy (a one-frame clip is a real use,
+// BASELINE config C1): device buffers come from the device's stream-ordered
+// memory pool, which keeps freed memory for the next handle, and streams
+// from a free list.  Measured before: cudaMalloc/cudaFree and stream
+// create/destroy made a C1 handle's create + first frame + destroy cost
+// ~9 ms, as much as the reference's whole CPU frame.
+constexpr uint64_t kPoolRetainBytes = 4ull << 30;  // kept by the pool when freed
+
+struct DevPool {
+  std::mutex mu;
+  std::map<int, std::vector<cudaStream_t>> idle;  // idle non-blocking streams
+  std::map<int, cudaStream_t> alloc;              // allocation stream per device
+};
+
+DevPool& devpool() {
+  static DevPool* p = new DevPool;  // process lifetime (no teardown-order issues at exit)
+  return *p;
+}
+
+int current_dev() {
+  int d = 0;
+  ck(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+
+cudaStream_t alloc_stream(int dev) {
+  DevPool& P = devpool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  cudaStream_t& s = P.alloc[dev];
+  if (!s) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  return s;
+}
+
+// Device memory of the current device, usable from any stream on return.
+template <class T>
+void dmalloc(T** p, uint64_t bytes, const char* what) {
+  *p = nullptr;
+  if (!bytes) return;
+  const cudaStream_t s = alloc_stream(current_dev());
+  void* v = nullptr;
+  ck(cudaMallocAsync(&v, bytes, s), what);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(v, s);
+    ck(e, what);
+  }
+  *p = static_cast<T*>(v);
+}
+
+// Returns memory to the pool.  s == nullptr: no stream may still use it
+// (callers synchronise first); otherwise the memory is released when `s`
+// reaches this point, and every user of it must be ordered before.
+void dfree(void* p, cudaStream_t s = nullptr) noexcept {
+  if (!p) return;
+  if (!s) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return;
+    try {
+      s = alloc_stream(d);
+    } catch (...) {
+      return;
+    }
+  }
+  cudaFreeAsync(p, s);
+}
+
+// An idle pooled stream (streams of destroyed handles may still be
+// finishing their last work: those are skipped), else a new one.
+cudaStream_t stream_get() {
+  const int dev = current_dev();
+  DevPool& P = devpool();
+  {
+    std::lock_guard<std::mutex> lock(P.mu);
+    auto& v = P.idle[dev];
+    for (size_t i = v.size(); i-- > 0;) {
+      if (cudaStreamQuery(v[i]) == cudaSuccess) {
+        cudaStream_t s = v[i];
+        v.erase(v.begin() + long(i));
+        return s;
+      }
+    }
+    cudaGetLastError();  // cudaErrorNotReady from the queries is not an error
+  }
+  cudaStream_t s = nullptr;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  return s;
+}
+
+// Back to the pool (it may still be finishing queued work).
+void stream_put(cudaStream_t s) noexcept {
+  if (!s) return;
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return;
+  DevPool& P = devpool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  try {
+    P.idle[d].push_back(s);
+  } catch (...) {
+    cudaStreamDestroy(s);
+  }
+}
+
 constexpr uint32_t kSlots = 3;  // host frames in flight (H2D / work / D2H)
 constexpr uint64_t kOrbitBytes = 128ull << 20;  // per generator launch
 
-void free_prbg(PrbgBuffers& b) {
-  cudaFree(b.state);
-  cudaFree(b.verified_end);
+void free_prbg(PrbgBuffers& b, cudaStream_t s = nullptr) {
+  dfree(b.state, s);
+  dfree(b.verified_end, s);
   for (int k = 0; k < 2; ++k) {
-    cudaFree(b.ckpt[k]);
-    cudaFree(b.orbit[k]);
+    dfree(b.ckpt[k], s);
+    dfree(b.orbit[k], s);
   }
-  cudaFree(b.bad);
-  cudaFree(b.replays);
+  dfree(b.bad, s);
+  dfree(b.replays, s);
   b = PrbgBuffers{};
 }
 
@@ -48,16 +153,16 @@ PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
   PrbgBuffers b{};
   try {
     const size_t lanes_bytes = nlanes * sizeof(double);
-    ck(cudaMalloc(&b.state, lanes_bytes), "cudaMalloc state");
-    ck(cudaMalloc(&b.verified_end, lanes_bytes), "cudaMalloc state");
+    dmalloc(&b.state, lanes_bytes, "cudaMalloc state");
+    dmalloc(&b.verified_end, lanes_bytes, "cudaMalloc state");
     for (int k = 0; k < 2; ++k) {
-      ck(cudaMalloc(&b.ckpt[k], lanes_bytes), "cudaMalloc ckpt");
+      dmalloc(&b.ckpt[k], lanes_bytes, "cudaMalloc ckpt");
       if (orbit_iters)
-        ck(cudaMalloc(&b.orbit[k], uint64_t(orbit_iters) * lanes_bytes), "cudaMalloc orbit");
+        dmalloc(&b.orbit[k], uint64_t(orbit_iters) * lanes_bytes, "cudaMalloc orbit");
     }
     b.max_iters = orbit_iters;
-    ck(cudaMalloc(&b.bad, (nlanes / 2) * sizeof(unsigned)), "cudaMalloc flags");
-    ck(cudaMalloc(&b.replays, sizeof(unsigned long long)), "cudaMalloc");
+    dmalloc(&b.bad, (nlanes / 2) * sizeof(unsigned), "cudaMalloc flags");
+    dmalloc(&b.replays, sizeof(unsigned long long), "cudaMalloc");
     ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
     ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
   } catch (...) {
@@ -71,12 +176,12 @@ PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
 // synchronised: no kernel may be using them).
 void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
   for (int k = 0; k < 2; ++k) {
-    cudaFree(b.orbit[k]);
+    dfree(b.orbit[k]);
     b.orbit[k] = nullptr;
   }
   b.max_iters = 0;
   for (int k = 0; k < 2; ++k)
-    ck(cudaMalloc(&b.orbit[k], uint64_t(iters) * nlanes * sizeof(double)), "cudaMalloc orbit");
+    dmalloc(&b.orbit[k], uint64_t(iters) * nlanes * sizeof(double), "cudaMalloc orbit");
   b.max_iters = iters;
 }
 
@@ -84,11 +189,15 @@ void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
 // end point.
 void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
                uint32_t nlanes, cudaStream_t s) {
-  struct Staging {  // freed on every path (cudaFree waits for the device)
+  struct Staging {  // freed on every path, once the stream is done with it
     double* p = nullptr;
-    ~Staging() { cudaFree(p); }
-  } x0d;
-  ck(cudaMalloc(&x0d.p, nlanes * sizeof(double)), "cudaMalloc x0");
+    cudaStream_t s;
+    ~Staging() {
+      if (p) cudaStreamSynchronize(s);
+      dfree(p);
+    }
+  } x0d{nullptr, s};
+  dmalloc(&x0d.p, nlanes * sizeof(double), "cudaMalloc x0");
   ck(cudaMemcpyAsync(x0d.p, x0, nlanes * sizeof(double), cudaMemcpyHostToDevice, s),
      "upload x0");
   launch_prbg_init(b.state, d_lc, x0d.p, nlanes, s);
@@ -98,10 +207,10 @@ void init_prbg(const PrbgBuffers& b, const LaneConst* d_lc, const double* x0,
   ck(cudaStreamSynchronize(s), "prbg_init");
 }
 
-void free_lasm(LasmBuffers& b) {
-  cudaFree(b.state);
-  cudaFree(b.mu);
-  for (auto& o : b.orbit) cudaFree(o);
+void free_lasm(LasmBuffers& b, cudaStream_t s = nullptr) {
+  dfree(b.state, s);
+  dfree(b.mu, s);
+  for (auto& o : b.orbit) dfree(o, s);
   b = LasmBuffers{};
 }
 }  // namespace
@@ -121,7 +230,7 @@ void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaSt
       x0[2 * i + 1] = lanes[i].b.x0;
     }
     pb_ = alloc_prbg(nl_, s, orbit_iters);
-    ck(cudaMalloc(&d_lc_, nl_ * sizeof(LaneConst)), "cudaMalloc lanes");
+    dmalloc(&d_lc_, nl_ * sizeof(LaneConst), "cudaMalloc lanes");
     ck(cudaMemcpyAsync(d_lc_, lc.data(), nl_ * sizeof(LaneConst), cudaMemcpyHostToDevice, s),
        "upload lanes");
     init_prbg(pb_, d_lc_, x0.data(), nl_, s);
@@ -135,13 +244,17 @@ void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaSt
     xy0[2 * i] = make_double2(lanes[i].la.x0, lanes[i].la.y0);
     xy0[2 * i + 1] = make_double2(lanes[i].lb.x0, lanes[i].lb.y0);
   }
-  struct Staging {  // freed on every path (cudaFree waits for the device)
+  struct Staging {  // freed on every path, once the stream is done with it
     double2* p = nullptr;
-    ~Staging() { cudaFree(p); }
-  } d_xy0;
-  ck(cudaMalloc(&lb_.state, nl_ * sizeof(double2)), "cudaMalloc lasm state");
-  ck(cudaMalloc(&lb_.mu, nl_ * sizeof(double)), "cudaMalloc lasm mu");
-  ck(cudaMalloc(&d_xy0.p, nl_ * sizeof(double2)), "cudaMalloc lasm x0");
+    cudaStream_t s;
+    ~Staging() {
+      if (p) cudaStreamSynchronize(s);
+      dfree(p);
+    }
+  } d_xy0{nullptr, s};
+  dmalloc(&lb_.state, nl_ * sizeof(double2), "cudaMalloc lasm state");
+  dmalloc(&lb_.mu, nl_ * sizeof(double), "cudaMalloc lasm mu");
+  dmalloc(&d_xy0.p, nl_ * sizeof(double2), "cudaMalloc lasm x0");
   ck(cudaMemcpyAsync(lb_.mu, mu.data(), nl_ * sizeof(double), cudaMemcpyHostToDevice, s),
      "upload mu");
   ck(cudaMemcpyAsync(d_xy0.p, xy0.data(), nl_ * sizeof(double2), cudaMemcpyHostToDevice, s),
@@ -152,11 +265,11 @@ void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaSt
   ck(cudaStreamSynchronize(s), "lasm_init");
 }
 
-void Generator::release() noexcept {
-  free_prbg(pb_);
-  cudaFree(d_lc_);
+void Generator::release(cudaStream_t after) noexcept {
+  free_prbg(pb_, after);
+  dfree(d_lc_, after);
   d_lc_ = nullptr;
-  free_lasm(lb_);
+  free_lasm(lb_, after);
 }
 
 uint32_t Generator::orbit_cap_iters() const {
@@ -171,12 +284,12 @@ void Generator::resize(uint32_t iters) {
     return;
   }
   for (auto& o : lb_.orbit) {
-    cudaFree(o);
+    dfree(o);
     o = nullptr;
   }
   lb_.max_iters = 0;
   for (auto& o : lb_.orbit)
-    ck(cudaMalloc(&o, uint64_t(iters) * nl_ * sizeof(double2)), "cudaMalloc lasm orbit");
+    dmalloc(&o, uint64_t(iters) * nl_ * sizeof(double2), "cudaMalloc lasm orbit");
   lb_.max_iters = iters;
 }
 
@@ -235,6 +348,10 @@ void configure_kernels_once(int device) {
   configure_prbg_kernels();
   configure_cipher_kernels();
   ck(cudaGetLastError(), "kernel attributes");
+  cudaMemPool_t pool = nullptr;  // keep freed handle buffers for the next handle
+  ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+  uint64_t retain = kPoolRetainBytes;
+  ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &retain), "mempool");
   done.insert(device);
 }
 
@@ -249,11 +366,13 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     raise(Errc::internal, "no CUDA device: the B200 engine has no CPU path");
-  cudaDeviceProp prop{};
-  ck(cudaGetDeviceProperties(&prop, dev_), "cudaGetDeviceProperties");
-  if (prop.major != 10)
-    raise(Errc::internal, std::string("engine is built for sm_100a; device is ") +
-                              prop.name);
+  int major = 0;
+  ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev_), "device query");
+  if (major != 10) {
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev_);
+    raise(Errc::internal, std::string("engine is built for sm_100a; device is ") + prop.name);
+  }
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   configure_kernels_once(dev_);
   if (const char* e = std::getenv("CVE_B200_GEN_CHUNK")) {  // experiments only; 0 = unset
@@ -271,16 +390,16 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
 }
 
 void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
-  ck(cudaStreamCreateWithFlags(&s_gen_, cudaStreamNonBlocking), "stream");
+  s_gen_ = stream_get();
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-  ck(cudaStreamCreateWithFlags(&s_work_, cudaStreamNonBlocking), "stream");
+  s_work_ = stream_get();
   // Verification runs on s_work: every frame's rounds wait for their
   // keystream's verify anyway, and a device-API handle then occupies two
   // hardware queues, so 16 concurrent handles fit CUDA_DEVICE_MAX_CONNECTIONS
   // = 32 without sharing a queue with another handle's long chain launches.
   if (one_stream_) {  // generator on the rounds stream too: one hardware queue per handle
-    ck(cudaStreamDestroy(s_gen_), "stream");
+    stream_put(s_gen_);
     s_gen_ = s_work_;
   }
 
@@ -295,12 +414,26 @@ Engine::~Engine() { release(); }
 // and idempotent.
 void Engine::release() noexcept {
   cudaSetDevice(dev_);
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
-    if (s) cudaStreamSynchronize(s);
+  // Asynchronous teardown: work still queued -- typically the generator's
+  // run-ahead for a next frame that will never come -- finishes on the
+  // device, and every buffer goes back to the pool in stream order after it,
+  // so destroying a handle does not wait for it.  `fin` joins every stream.
+  cudaStream_t fin = s_work_;
+  for (cudaStream_t s : {s_gen_, s_h2d_, s_d2h_}) {
+    if (!s || s == fin) continue;
+    cudaEvent_t e = nullptr;
+    if (fin && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(e, s) == cudaSuccess && cudaStreamWaitEvent(fin, e, 0) == cudaSuccess) {
+      cudaEventDestroy(e);
+    } else {
+      if (e) cudaEventDestroy(e);
+      cudaStreamSynchronize(s);
+    }
+  }
   for (auto& c : consumers_) ev_put(c.done);
   consumers_.clear();
   for (auto& e : ver_done_) {
-    if (e) cudaEventDestroy(e);
+    if (e) cudaEventDestroy(e);  // pending events are released once complete
     e = nullptr;
   }
   for (auto& e : chain_done_) {
@@ -320,21 +453,21 @@ void Engine::release() noexcept {
   tev_pool_.clear();
   for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
   slot_free_.clear();
-  for (uint8_t* p : slots_) cudaFree(p);
+  for (uint8_t* p : slots_) dfree(p, fin);
   slots_.clear();
-  for (auto& kv : sines_) cudaFree(kv.second);
+  for (auto& kv : sines_) dfree(kv.second, fin);
   sines_.clear();
   for (uint8_t*& p : scratch_) {
-    cudaFree(p);
+    dfree(p, fin);
     p = nullptr;
   }
-  cudaFree(d_shift_);
+  dfree(d_shift_, fin);
   d_shift_ = nullptr;
-  cudaFree(ring_);
+  dfree(ring_, fin);
   ring_ = nullptr;
-  gen_.release();
+  gen_.release(fin);
   for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_h2d_, s_work_, s_d2h_})
-    if (s) cudaStreamDestroy(s);
+    stream_put(s);  // reused only once idle (stream_get)
   s_gen_ = s_h2d_ = s_work_ = s_d2h_ = nullptr;
 }
 
@@ -438,14 +571,14 @@ void Engine::ensure_ring(uint64_t need) {
   const uint64_t want = round_up(4 * need + 48 * 1024, 48 * 1024);
   synchronize();
   uint8_t* fresh = nullptr;
-  ck(cudaMalloc(&fresh, want * n_), "cudaMalloc keystream ring");
+  dmalloc(&fresh, want * n_, "cudaMalloc keystream ring");
   const uint64_t gen_bytes = gen_iters_ * bpi_;
   if (ring_ && gen_bytes > cons_) {
     launch_ring_move(ring_, ring_bytes_, fresh, want, cons_, gen_bytes, n_, s_gen_);
     ++st_.kernel_launches;
     ck(cudaStreamSynchronize(s_gen_), "ring move");
   }
-  cudaFree(ring_);
+  dfree(ring_);
   ring_ = fresh;
   ring_bytes_ = want;
   // orbit buffers for the longest launch gen_until will issue (a quarter of
@@ -468,25 +601,25 @@ void Engine::ensure_buffers(const Geom& g, uint32_t slots) {
   if (scratch_bytes_ < scratch_need || (generic && !scratch_[2])) {
     synchronize();
     for (auto& p : scratch_) {
-      cudaFree(p);
+      dfree(p);
       p = nullptr;
     }
-    ck(cudaMalloc(&scratch_[0], scratch_need), "cudaMalloc scratch");
-    ck(cudaMalloc(&scratch_[1], scratch_need), "cudaMalloc scratch");
-    if (generic) ck(cudaMalloc(&scratch_[2], scratch_need), "cudaMalloc scratch");
+    dmalloc(&scratch_[0], scratch_need, "cudaMalloc scratch");
+    dmalloc(&scratch_[1], scratch_need, "cudaMalloc scratch");
+    if (generic) dmalloc(&scratch_[2], scratch_need, "cudaMalloc scratch");
     scratch_bytes_ = scratch_need;
   }
   if (shift_cap_ < g.side) {
     synchronize();
-    cudaFree(d_shift_);
-    ck(cudaMalloc(&d_shift_, sizeof(int32_t) * g.side), "cudaMalloc shift");
+    dfree(d_shift_);
+    dmalloc(&d_shift_, sizeof(int32_t) * g.side, "cudaMalloc shift");
     shift_cap_ = g.side;
   }
   if (slots && (slots_.size() < slots || slot_bytes_ < fb)) {
     synchronize();
-    for (uint8_t* p : slots_) cudaFree(p);
+    for (uint8_t* p : slots_) dfree(p);
     slots_.assign(slots, nullptr);
-    for (auto& p : slots_) ck(cudaMalloc(&p, fb), "cudaMalloc frame slot");
+    for (auto& p : slots_) dmalloc(&p, fb, "cudaMalloc frame slot");
     slot_bytes_ = fb;
     while (slot_free_.size() < slots) {
       cudaEvent_t e;
@@ -502,7 +635,7 @@ const double* Engine::sine_for(uint32_t side) {
   if (it != sines_.end()) return it->second;
   const std::vector<double> s = sine_table(side);
   double* d = nullptr;
-  ck(cudaMalloc(&d, sizeof(double) * side), "cudaMalloc sine");
+  dmalloc(&d, sizeof(double) * side, "cudaMalloc sine");
   // ordered before k_shift, which runs on s_work
   ck(cudaMemcpyAsync(d, s.data(), sizeof(double) * side, cudaMemcpyHostToDevice, s_work_),
      "upload sine");
@@ -611,8 +744,13 @@ void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
   ck(cudaEventRecord(c.done, s_work_), "cudaEventRecord");
   consumers_.push_back(c);
   ++st_.frames;
-  // run-ahead: start the next frame's keystream behind this one's
-  gen_until(cons_ + need);
+  // Run-ahead: start the next frame's keystream behind this one's, so a
+  // caller's next call finds it (partly) generated.  Not after a handle's
+  // first frame: a one-frame clip (BASELINE config C1) would leave a whole
+  // frame of chain + verify work running after it is destroyed, where the
+  // next clip's work collides with it.  From the second frame on the clip is
+  // a stream of frames and the run-ahead pays.
+  if (st_.frames >= 2) gen_until(cons_ + need);
 }
 
 void Engine::run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt) {
@@ -627,8 +765,8 @@ void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool d
     raise(Errc::invalid_argument, "frame region exceeds the padded side");
   const Geom g = geometry(side);
   if (!s_h2d_) {  // copy streams only for handles that use the host API
-    ck(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+    s_h2d_ = stream_get();
+    s_d2h_ = stream_get();
   }
   ensure_ring(uint64_t(r_) * g.region);
   ensure_buffers(g, kSlots);
@@ -740,20 +878,20 @@ void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len) {
   auto cleanup = [&] {
     if (s) cudaStreamSynchronize(s);
     gen.release();
-    cudaFree(d_out);
-    if (s) cudaStreamDestroy(s);
+    dfree(d_out);
+    stream_put(s);
   };
   try {
     int dev = 0;
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     configure_kernels_once(dev);
-    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    s = stream_get();
     gen.init({w}, kind, s, 0);
     gen.resize(gen.orbit_cap_iters());
     const uint32_t bpi = gen.bytes_per_iter();
     const uint64_t iters = round_up((len + bpi - 1) / bpi, 8);
     const uint64_t ring = iters * bpi;  // multiple of 48
-    ck(cudaMalloc(&d_out, ring), "cudaMalloc");
+    dmalloc(&d_out, ring, "cudaMalloc");
     int slot = 0;
     for (uint64_t it = 0; it < iters; it += gen.max_iters(), slot ^= 1) {
       const uint32_t n = uint32_t(std::min<uint64_t>(gen.max_iters(), iters - it));
@@ -796,10 +934,10 @@ KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind 
   ck(cudaSetDevice(device), "cudaSetDevice");
   configure_kernels_once(device);
   try {
-    ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+    s_ = stream_get();
     gen_.init(lanes, kind, s_, 0);
     gen_.resize(gen_.orbit_cap_iters());
-    ck(cudaMalloc(&d_buf_, chunk_bytes() * n_), "cudaMalloc keystream");
+    dmalloc(&d_buf_, chunk_bytes() * n_, "cudaMalloc keystream");
   } catch (...) {
     release();
     throw;
@@ -811,9 +949,9 @@ KeystreamSource::~KeystreamSource() { release(); }
 void KeystreamSource::release() noexcept {
   if (s_) cudaStreamSynchronize(s_);
   gen_.release();
-  cudaFree(d_buf_);
+  dfree(d_buf_);
   d_buf_ = nullptr;
-  if (s_) cudaStreamDestroy(s_);
+  stream_put(s_);
   s_ = nullptr;
 }
 

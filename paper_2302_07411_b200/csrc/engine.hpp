@@ -79,7 +79,9 @@ class Generator {
   // orbit_iters = 0: no orbit buffers yet (see resize).
   void init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaStream_t s,
             uint32_t orbit_iters);
-  void release() noexcept;
+  // after == nullptr: nothing may still use the buffers; otherwise they are
+  // released in the stream order of `after`, behind every user of them.
+  void release(cudaStream_t after = nullptr) noexcept;
   MapKind kind() const { return kind_; }
   uint32_t bytes_per_iter() const { return kind_ == MapKind::Lasm ? 12 : 6; }
   uint32_t max_iters() const { return kind_ == MapKind::Lasm ? lb_.max_iters : pb_.max_iters; }
