@@ -435,3 +435,36 @@ def test_c_caller_matches_oracle(tmp_path):
             x ^= b << (8 * (i & 3))
         assert out.stdout.split()[:2] == ["ok", f"{x:08x}"], (key, out.stdout)
         assert "seeds=1" in out.stdout
+
+
+def test_handle_churn_async_teardown():
+    # Handles are destroyed without waiting for queued work (buffers are
+    # freed in stream order behind it) and streams/memory are pooled: many
+    # short clips created and destroyed back to back, PLCM and LASM, with
+    # and without a run-ahead frame left queued, must all match the first
+    # run's ciphertext and must not grow device memory without bound.
+    torch = pytest.importorskip("torch")
+    side = 192
+    f = rand_frames(side, 2, 77)
+    want = {}
+    free0 = None
+    for it in range(60):
+        key = synth.det_key(31) if it % 2 else synth.det_key_lasm(31)
+        frames = f.copy()
+        c = cve.Cipher(key, 8, 5)
+        c.encrypt_frame(frames[0])
+        if it % 3 == 0:
+            c.encrypt_frame(frames[1])  # second frame: run-ahead queued at destroy
+        c.close()
+        tag = (it % 2, it % 3 == 0)
+        got = frames[0].tobytes() + (frames[1].tobytes() if tag[1] else b"")
+        assert want.setdefault(tag, got) == got, it
+        if it == 10:
+            torch.cuda.synchronize()
+            free0 = torch.cuda.mem_get_info()[0]
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] > free0 - (1 << 30)
+    o = Oracle(synth.det_key(31), 8, 5)
+    a = f[0].copy()
+    assert o.encrypt(a) == 0
+    assert want[(1, False)][: a.nbytes] == a.tobytes()
