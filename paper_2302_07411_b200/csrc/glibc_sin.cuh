@@ -12,7 +12,8 @@
 // polynomial corrections, Taylor series near 0, Cody-Waite reduction by pi/2
 // below 105414350), in the operation order and FMA contractions of the
 // `sin` ifunc variant the dynamic linker selects on hosts with FMA + AVX2
-// (every B200 host).  The polynomial and reduction constants are the
+// (every B200 host); which operations that variant fuses was read from the
+// installed libm's machine code (objdump), not from glibc's sources.  The polynomial and reduction constants are the
 // algorithm's published coefficients; the 110-entry sin/cos table is read
 // from the installed libm at build time (gen_sincostab.py -> the generated
 // glibc_sincostab.inc), because its low parts are not reproducible by
