@@ -13,12 +13,13 @@
 // below 105414350), in the operation order and FMA contractions of the
 // `sin` ifunc variant the dynamic linker selects on hosts with FMA + AVX2
 // (every B200 host); which operations that variant fuses was read from the
-// installed libm's machine code (objdump), not from glibc's sources.  The polynomial and reduction constants are the
-// algorithm's published coefficients; the 110-entry sin/cos table is read
-// from the installed libm at build time (gen_sincostab.py -> the generated
-// glibc_sincostab.inc), because its low parts are not reproducible by
-// recomputation.  Parity is pinned by tests/test_lasm.py against the host's
-// libm `sin` on ~10^7 arguments per branch and on the LASM orbits themselves.
+// installed libm's machine code (objdump), not from glibc's sources.  The
+// polynomial and reduction constants are the algorithm's published
+// coefficients; the 110-entry sin/cos table is read from the installed libm
+// at build time (gen_sincostab.py -> the generated glibc_sincostab.inc),
+// because its low parts are not reproducible by recomputation.  Parity is
+// pinned by tests/test_lasm.py against the host's libm `sin` on ~4 million
+// arguments across every branch and edge and on whole LASM orbits.
 //
 // Domain: |x| < 105414350 (the Cody-Waite branch).  LASM arguments are
 // pi*mu*(y+3)*x*(1-x) with x, y in [0,1], mu <= 1, i.e. in [0, pi]; larger
