@@ -887,9 +887,9 @@ void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len) {
     configure_kernels_once(dev);
     s = stream_get();
     gen.init({w}, kind, s, 0);
-    gen.resize(gen.orbit_cap_iters());
     const uint32_t bpi = gen.bytes_per_iter();
     const uint64_t iters = round_up((len + bpi - 1) / bpi, 8);
+    gen.resize(uint32_t(std::min<uint64_t>(gen.orbit_cap_iters(), iters)));
     const uint64_t ring = iters * bpi;  // multiple of 48
     dmalloc(&d_out, ring, "cudaMalloc");
     int slot = 0;
@@ -929,14 +929,18 @@ void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_
 }
 
 KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind,
-                                 int device)
+                                 int device, uint64_t max_bytes)
     : n_(uint32_t(lanes.size())) {
   ck(cudaSetDevice(device), "cudaSetDevice");
   configure_kernels_once(device);
   try {
     s_ = stream_get();
     gen_.init(lanes, kind, s_, 0);
-    gen_.resize(gen_.orbit_cap_iters());
+    // chunks no longer than the whole request: a short export generates
+    // (and allocates for) only what it returns
+    const uint64_t bpi = gen_.bytes_per_iter();
+    const uint64_t need = round_up((std::max<uint64_t>(max_bytes, 1) + bpi - 1) / bpi, 8);
+    gen_.resize(uint32_t(std::min<uint64_t>(gen_.orbit_cap_iters(), need)));
     dmalloc(&d_buf_, chunk_bytes() * n_, "cudaMalloc keystream");
   } catch (...) {
     release();

@@ -220,7 +220,9 @@ void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_
 // with a stride of chunk_bytes().
 class KeystreamSource {
  public:
-  KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind, int device);
+  // max_bytes: the most any worker will be asked for (sizes the chunks)
+  KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind, int device,
+                  uint64_t max_bytes = ~uint64_t(0));
   ~KeystreamSource();
   KeystreamSource(const KeystreamSource&) = delete;
   KeystreamSource& operator=(const KeystreamSource&) = delete;

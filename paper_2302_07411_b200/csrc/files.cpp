@@ -232,7 +232,7 @@ void keystream_export(const char* key_hex, uint32_t workers, uint64_t byte_count
     len[i] = base + (i < extra ? 1 : 0);
     start[i] = i ? start[i - 1] + len[i - 1] : 0;
   }
-  KeystreamSource src(lanes, key.kind, device);
+  KeystreamSource src(lanes, key.kind, device, longest);
   const uint64_t chunk = src.chunk_bytes();
   Pinned host(size_t(chunk) * n);
   for (uint64_t done = 0; done < longest; done += chunk) {
