@@ -45,6 +45,18 @@ __global__ void k(double* out, long long* cyc, int iters, double x0, double y0, 
     } else if (V == 5) {  // taylor only
       x = gsin::taylor(x * 1e-3, 0.0);
       y = gsin::taylor(y * 1e-3 + x, 0.0);
+    } else if (V == 7) {  // arg + glibc's cos(pi/2 - x) branch body, forced (no range tests)
+      // keeps the argument in the C range: pm' = 1.3/0.25 scale keeps a in ~[0.9, 1.6]
+      x = gsin::cos_tab(gsin::kHp0 - (0.9 + pm * (y + 3.0) * x * (1.0 - x)), gsin::kHp1, tab);
+      y = gsin::cos_tab(gsin::kHp0 - (0.9 + pm * (x + 3.0) * y * (1.0 - y)), gsin::kHp1, tab);
+    } else if (V == 8) {  // the same through sin_0pi (range tests + branch)
+      x = gsin::sin_0pi(0.9 + pm * (y + 3.0) * x * (1.0 - x), tab);
+      y = gsin::sin_0pi(0.9 + pm * (x + 3.0) * y * (1.0 - y), tab);
+    } else if (V == 9) {  // 17 dependent FP64 ops per half: the C path's op count
+#pragma unroll
+      for (int j = 0; j < 17; ++j) x = fma(x, 0.999, y * 0.0);
+#pragma unroll
+      for (int j = 0; j < 17; ++j) y = fma(y, 0.999, x * 0.0);
     } else if (V == 6) {  // sin_tab only
       x = gsin::sin_tab(0.2 + x * 1e-3, 0.0, tab);
       y = gsin::sin_tab(0.2 + y * 1e-3 + x * 1e-3, 0.0, tab);
@@ -109,6 +121,9 @@ int main() {
   run<3>("16 x DFMA", 0.3, 0.999, 0.9);
   run<4>("16 x DADD", 0.3, 1e-9, 0.9);
   run<5>("2 x taylor", 0.3, 0.7, 0.9);
+  run<7>("2 x (arg + cos branch body)", 0.3, 0.7, 0.05);
+  run<8>("2 x (arg + sin_0pi, C path)", 0.3, 0.7, 0.05);
+  run<9>("2 x 17 dependent DFMA", 0.3, 0.7, 0.9);
   run<6>("2 x sin_tab", 0.3, 0.7, 0.9);
   return 0;
 }
