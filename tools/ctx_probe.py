@@ -1,3 +1,5 @@
+"""CUDA driver init and primary-context cost vs this library's first handle
+(fresh process).  Tool."""
 import ctypes, time, os, sys
 t0=time.perf_counter()
 cuda=ctypes.CDLL("libcuda.so.1")
