@@ -116,7 +116,7 @@ typedef enum cve_out_format {
 /* replaces cve.h:97-99.  P6 file, directory of P6 frames, or raw RGB24 ->
  * CVE1 container (27-byte header + frame_count padded-square ciphertexts).
  * Frames are padded on the device; the container is byte-identical to the
- * reference's for PLCM keys. */
+ * reference's (PLCM and LASM keys). */
 CVE_B200_API cve_status cve_encrypt_file(const char* key_hex,
                                          const cve_io_options* io,
                                          const char* in_path,
