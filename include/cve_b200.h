@@ -254,6 +254,48 @@ CVE_B200_API cve_status cve_cipher_decrypt_frames_async(cve_cipher* cipher,
                                                         uint32_t count,
                                                         void* stream);
 
+/* ---- additive: one clip sharded across GPUs (north star "independent frames
+ * of a clip are partitioned across the B200s") -------------- */
+
+/* Like cve_cipher_create, but the clip's cipher work is spread over
+ * `device_count` CUDA devices: the keystream generator of the clip (its 2n
+ * sequential chaotic orbits, reference engine.cpp:174-176, 198-205) runs on
+ * devices[0]; frame k is ciphered on shard k mod device_count, which pulls
+ * that frame's keystream window (rounds * region bytes per subframe) out of
+ * the generator's ring with a peer copy over NVLink and runs the shift table
+ * and the rounds on its own device.  Entries may repeat (e.g. {0, 0}: two
+ * shards on one GPU, each with its own streams and buffers).  Output is
+ * byte-identical to a single-device handle: the k-th call still binds to
+ * frame k (reference cve.h:72-74).  The host-buffer calls
+ * (cve_cipher_encrypt_frame(s), _wh) deal frames to the shards round-robin
+ * across calls.  device_count == 1 is cve_cipher_create on devices[0].
+ * A device index out of range -> INVALID_ARGUMENT. */
+CVE_B200_API cve_status cve_cipher_create_devices(const char* key_hex, uint32_t workers,
+                                                  uint32_t rounds, const int* devices,
+                                                  uint32_t device_count, cve_cipher** out);
+
+/* Number of cipher shards of the handle (1 for cve_cipher_create) and, if
+ * devices_out is not NULL, the device of shard i in devices_out[i] (i < cap). */
+CVE_B200_API cve_status cve_cipher_shards(const cve_cipher* cipher, uint32_t* count_out,
+                                          int* devices_out, uint32_t cap);
+
+/* Device-resident frames of a sharded handle: batch frame f is processed on
+ * shard g = f % G (G = cve_cipher_shards) and lives in that shard's device
+ * memory at shard_pixels[g] + (f / G) * side*side*3, in place.  streams[g]
+ * (a cudaStream_t of shard g's device, or NULL for its legacy default
+ * stream; `streams` itself may be NULL) orders shard g's frames like
+ * cve_cipher_encrypt_frames_async: after prior work on it, and it waits for
+ * their completion; the call does not block the host.  On a single-device
+ * handle this is cve_cipher_encrypt_frames_async(shard_pixels[0], streams[0]). */
+CVE_B200_API cve_status cve_cipher_encrypt_frames_sharded_async(cve_cipher* cipher,
+                                                                uint8_t* const* shard_pixels,
+                                                                uint32_t side, uint32_t count,
+                                                                void* const* streams);
+CVE_B200_API cve_status cve_cipher_decrypt_frames_sharded_async(cve_cipher* cipher,
+                                                                uint8_t* const* shard_pixels,
+                                                                uint32_t side, uint32_t count,
+                                                                void* const* streams);
+
 /* Blocks until every operation of the handle has finished. */
 CVE_B200_API cve_status cve_cipher_synchronize(cve_cipher* cipher);
 

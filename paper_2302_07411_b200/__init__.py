@@ -89,6 +89,14 @@ def _load() -> C.CDLL:
         "cve_key_validate": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
         "cve_cipher_create": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_int,
                                         C.POINTER(vp)]),
+        "cve_cipher_create_devices": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32,
+                                                C.POINTER(C.c_int), C.c_uint32, C.POINTER(vp)]),
+        "cve_cipher_shards": (C.c_int, [vp, C.POINTER(C.c_uint32), C.POINTER(C.c_int),
+                                        C.c_uint32]),
+        "cve_cipher_encrypt_frames_sharded_async": (C.c_int, [vp, C.POINTER(vp), C.c_uint32,
+                                                              C.c_uint32, C.POINTER(vp)]),
+        "cve_cipher_decrypt_frames_sharded_async": (C.c_int, [vp, C.POINTER(vp), C.c_uint32,
+                                                              C.c_uint32, C.POINTER(vp)]),
         "cve_cipher_destroy": (None, [vp]),
         "cve_cipher_encrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
         "cve_cipher_decrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
@@ -295,12 +303,22 @@ class Cipher:
     """One streaming cipher handle (reference cve_cipher, cve.h:62-82).
 
     The k-th encrypt or decrypt call binds to frame index k of the clip.
+    ``devices`` (additive, cve_cipher_create_devices): shard the clip's cipher
+    work over these CUDA devices -- the generator runs on devices[0], frame k
+    on devices[k % len(devices)]; entries may repeat.
     """
 
-    def __init__(self, key_hex, workers: int, rounds: int = 5, parallel: bool = True):
+    def __init__(self, key_hex, workers: int, rounds: int = 5, parallel: bool = True,
+                 devices=None):
         h = C.c_void_p()
-        _check(lib.cve_cipher_create(_as_key(key_hex), workers, rounds,
-                                     1 if parallel else 0, C.byref(h)))
+        if devices is None:
+            _check(lib.cve_cipher_create(_as_key(key_hex), workers, rounds,
+                                         1 if parallel else 0, C.byref(h)))
+        else:
+            devs = list(devices)
+            arr = (C.c_int * max(1, len(devs)))(*devs)
+            _check(lib.cve_cipher_create_devices(_as_key(key_hex), workers, rounds, arr,
+                                                 len(devs), C.byref(h)))
         self._h = h
         self.workers = workers
         self.rounds = rounds
@@ -365,6 +383,28 @@ class Cipher:
         _check(lib.cve_cipher_decrypt_frames_async(self.handle, C.c_void_p(ptr), side,
                                                    count, C.c_void_p(stream)))
 
+    @property
+    def shards(self) -> list:
+        """Device of each cipher shard (one entry for a single-device handle)."""
+        n = C.c_uint32()
+        devs = (C.c_int * 64)()
+        _check(lib.cve_cipher_shards(self.handle, C.byref(n), devs, 64))
+        return [devs[i] for i in range(min(n.value, 64))]
+
+    def _sharded(self, fn, ptrs, side: int, count: int, streams=None) -> None:
+        g = len(ptrs)
+        arr = (C.c_void_p * g)(*[C.c_void_p(p) for p in ptrs])
+        sarr = (C.c_void_p * g)(*[C.c_void_p(s) for s in (streams or [0] * g)])
+        _check(fn(self.handle, arr, side, count, sarr))
+
+    def encrypt_frames_sharded(self, ptrs, side: int, count: int, streams=None) -> None:
+        """Device-resident frames of a sharded handle: batch frame f lives on
+        shard f % G at ptrs[f % G] + (f // G) * side*side*3."""
+        self._sharded(lib.cve_cipher_encrypt_frames_sharded_async, ptrs, side, count, streams)
+
+    def decrypt_frames_sharded(self, ptrs, side: int, count: int, streams=None) -> None:
+        self._sharded(lib.cve_cipher_decrypt_frames_sharded_async, ptrs, side, count, streams)
+
     def encrypt_frames_wh(self, rgb: np.ndarray) -> np.ndarray:
         """(count, h, w, 3) unpadded frames -> (count, side, side, 3) ciphertexts,
         padded on the device."""
@@ -372,6 +412,8 @@ class Cipher:
             rgb = rgb[None]
         if rgb.dtype != np.uint8 or not rgb.flags.c_contiguous:
             raise CveError(CVE_ERROR_INVALID_ARGUMENT, "need a C-contiguous uint8 array")
+        if rgb.ndim != 4 or rgb.shape[-1] != 3:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "need (h,w,3) or (n,h,w,3) RGB24 frames")
         count, h, w = rgb.shape[:3]
         side = padded_side(w, h, self.workers)
         out = np.empty((count, side, side, 3), dtype=np.uint8)
@@ -383,7 +425,7 @@ class Cipher:
         """(count, side, side, 3) ciphertexts -> (count, height, width, 3) plaintexts."""
         if square.ndim == 3:
             square = square[None]
-        count, side = square.shape[0], square.shape[1]
+        count, side = self._frames(square)
         out = np.empty((count, height, width, 3), dtype=np.uint8)
         _check(lib.cve_cipher_decrypt_frames_wh(self.handle, square.ctypes.data, side, width,
                                                 height, count, out.ctypes.data))

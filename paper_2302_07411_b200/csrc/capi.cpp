@@ -53,23 +53,7 @@ void require(bool ok, const char* what) {
   if (!ok) cveb::raise(cveb::Errc::invalid_argument, what);
 }
 
-// Runs the handle's work on its own device, restoring the caller's.
-struct DeviceScope {
-  int prev = -1;
-  explicit DeviceScope(int dev) {
-    // No usable device: leave it to the engine to report INTERNAL once the
-    // host-side checks (files, keys) have run, as the reference orders them.
-    if (cudaGetDevice(&prev) != cudaSuccess) {
-      prev = -1;
-      return;
-    }
-    if (prev != dev && cudaSetDevice(dev) != cudaSuccess)
-      cveb::raise(cveb::Errc::internal, "cannot select the handle's CUDA device");
-  }
-  ~DeviceScope() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
+using cveb::DeviceScope;  // runs the handle's work on its device, restoring the caller's
 
 cve_status run_frames(cve_cipher* c, uint8_t* px, uint32_t side,
                       uint32_t count, bool decrypt) {
@@ -164,6 +148,36 @@ cve_status cve_cipher_create(const char* key_hex, uint32_t workers,
   });
 }
 
+cve_status cve_cipher_create_devices(const char* key_hex, uint32_t workers, uint32_t rounds,
+                                     const int* devices, uint32_t device_count,
+                                     cve_cipher** out) {
+  return guarded([&] {
+    require(out != nullptr, "out is null");
+    require(key_hex != nullptr, "key_hex is null");
+    require(devices != nullptr, "devices is null");
+    require(device_count >= 1, "device_count must be >= 1");
+    const cveb::Key key = cveb::parse_key(key_hex);
+    auto c = std::make_unique<cve_cipher>();
+    c->engine = std::make_unique<cveb::Engine>(
+        key, workers, rounds, std::vector<int>(devices, devices + device_count));
+    *out = c.release();
+  });
+}
+
+cve_status cve_cipher_shards(const cve_cipher* cipher, uint32_t* count_out, int* devices_out,
+                             uint32_t cap) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(count_out != nullptr, "count_out is null");
+    const uint32_t n = cipher->engine->shard_count();
+    *count_out = n;
+    for (uint32_t i = 0; i < n && i < cap && devices_out; ++i)
+      devices_out[i] = cipher->engine->shard_device(i);
+  });
+}
+
+// Engine::~Engine restores the caller's device itself (it may run on a
+// garbage-collection thread, where no DeviceScope is in place).
 void cve_cipher_destroy(cve_cipher* cipher) { delete cipher; }
 
 cve_status cve_cipher_encrypt_frame(cve_cipher* cipher, uint8_t* pixels,
@@ -348,6 +362,35 @@ cve_status cve_cipher_decrypt_frames_wh(cve_cipher* cipher, const uint8_t* squar
   });
 }
 
+static cve_status run_frames_sharded(cve_cipher* c, uint8_t* const* shard_px, uint32_t side,
+                                     uint32_t count, void* const* streams, bool decrypt) {
+  return guarded([&] {
+    require(c != nullptr, "cipher is null");
+    require(shard_px != nullptr, "pixels is null");
+    const uint32_t G = c->engine->shard_count();
+    for (uint32_t i = 0; i < G && i < count; ++i) require(shard_px[i] != nullptr, "pixels is null");
+    require(side != 0, "side must be >= 1");
+    require(count != 0, "count must be >= 1");
+    std::vector<cudaStream_t> users(G, nullptr);
+    if (streams)
+      for (uint32_t i = 0; i < G; ++i) users[i] = static_cast<cudaStream_t>(streams[i]);
+    DeviceScope scope(c->engine->device());
+    c->engine->run_device_sharded(shard_px, side, count, decrypt, users.data());
+  });
+}
+
+cve_status cve_cipher_encrypt_frames_sharded_async(cve_cipher* cipher, uint8_t* const* shard_pixels,
+                                                   uint32_t side, uint32_t count,
+                                                   void* const* streams) {
+  return run_frames_sharded(cipher, shard_pixels, side, count, streams, false);
+}
+
+cve_status cve_cipher_decrypt_frames_sharded_async(cve_cipher* cipher, uint8_t* const* shard_pixels,
+                                                   uint32_t side, uint32_t count,
+                                                   void* const* streams) {
+  return run_frames_sharded(cipher, shard_pixels, side, count, streams, true);
+}
+
 cve_status cve_cipher_synchronize(cve_cipher* cipher) {
   return guarded([&] {
     require(cipher != nullptr, "cipher is null");
@@ -410,6 +453,7 @@ cve_status cve_keystream_generate(const double lanes[4], uint8_t* out,
   return guarded([&] {
     require(lanes != nullptr, "lanes is null");
     require(out != nullptr || len == 0, "out is null");
+    DeviceScope scope(current_device());
     cveb::standalone_stream(cveb::Lane{lanes[0], lanes[1]},
                             cveb::Lane{lanes[2], lanes[3]}, out, len);
   });
@@ -420,6 +464,7 @@ cve_status cve_keystream_generate_lasm(const double lanes[6], uint8_t* out,
   return guarded([&] {
     require(lanes != nullptr, "lanes is null");
     require(out != nullptr || len == 0, "out is null");
+    DeviceScope scope(current_device());
     cveb::standalone_stream(cveb::LasmLane{lanes[0], lanes[1], lanes[2]},
                             cveb::LasmLane{lanes[3], lanes[4], lanes[5]}, out, len);
   });
@@ -429,6 +474,7 @@ cve_status cve_glibc_sin(const double* x, double* y, size_t count) {
   return guarded([&] {
     require((x != nullptr && y != nullptr) || count == 0, "null buffer");
     if (count == 0) return;
+    DeviceScope scope(current_device());
     struct Buf {
       double* p = nullptr;
       ~Buf() { cudaFree(p); }

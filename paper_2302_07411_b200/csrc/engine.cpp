@@ -38,6 +38,8 @@ struct DevPool {
   std::mutex mu;
   std::map<int, std::vector<cudaStream_t>> idle;  // idle non-blocking streams
   std::map<int, cudaStream_t> alloc;              // allocation stream per device
+  std::map<int, cudaMemPool_t> pools;             // the library's private memory pools
+  std::set<std::pair<int, int>> access;           // (pool device, peer) granted
 };
 
 DevPool& devpool() {
@@ -59,14 +61,60 @@ cudaStream_t alloc_stream(int dev) {
   return s;
 }
 
+// The library's own stream-ordered memory pool of `dev` (not the device's
+// default pool, which the host application -- e.g. PyTorch's cudaMallocAsync
+// backend -- owns and tunes): it keeps up to kPoolRetainBytes of freed
+// handle buffers for the next handle.
+cudaMemPool_t mem_pool(int dev) {
+  DevPool& P = devpool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  cudaMemPool_t& pool = P.pools[dev];
+  if (!pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t fresh = nullptr;
+    ck(cudaMemPoolCreate(&fresh, &props), "cudaMemPoolCreate");
+    uint64_t retain = kPoolRetainBytes;
+    ck(cudaMemPoolSetAttribute(fresh, cudaMemPoolAttrReleaseThreshold, &retain), "mempool");
+    pool = fresh;
+  }
+  return pool;
+}
+
+// Lets `peer` read and write allocations of `dev`'s pool (a sharded handle's
+// shards pull keystream windows out of the generator device's ring).  A
+// no-op without peer capability: the copies are then staged by the driver.
+void grant_peer_access(int dev, int peer) {
+  if (dev == peer) return;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, peer, dev) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return;
+  }
+  const cudaMemPool_t pool = mem_pool(dev);
+  DevPool& P = devpool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  if (P.access.count({dev, peer})) return;
+  cudaMemAccessDesc d{};
+  d.location.type = cudaMemLocationTypeDevice;
+  d.location.id = peer;
+  d.flags = cudaMemAccessFlagsProtReadWrite;
+  ck(cudaMemPoolSetAccess(pool, &d, 1), "cudaMemPoolSetAccess");
+  P.access.insert({dev, peer});
+}
+
 // Device memory of the current device, usable from any stream on return.
 template <class T>
 void dmalloc(T** p, uint64_t bytes, const char* what) {
   *p = nullptr;
   if (!bytes) return;
-  const cudaStream_t s = alloc_stream(current_dev());
+  const int dev = current_dev();
+  const cudaStream_t s = alloc_stream(dev);
   void* v = nullptr;
-  ck(cudaMallocAsync(&v, bytes, s), what);
+  ck(cudaMallocFromPoolAsync(&v, bytes, mem_pool(dev), s), what);
   const cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     cudaFreeAsync(v, s);
@@ -345,44 +393,209 @@ void configure_kernels_once(int device) {
   static std::set<int> done;
   std::lock_guard<std::mutex> lock(mu);
   if (done.count(device)) return;
+  DeviceScope scope(device);
   configure_prbg_kernels();
   configure_cipher_kernels();
   ck(cudaGetLastError(), "kernel attributes");
-  cudaMemPool_t pool = nullptr;  // keep freed handle buffers for the next handle
-  ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
-  uint64_t retain = kPoolRetainBytes;
-  ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &retain), "mempool");
   done.insert(device);
 }
 
+DeviceScope::DeviceScope(int dev) {
+  if (cudaGetDevice(&prev) != cudaSuccess) {
+    cudaGetLastError();
+    prev = -1;
+    return;
+  }
+  if (prev != dev && cudaSetDevice(dev) != cudaSuccess)
+    raise(Errc::internal, "cannot select the handle's CUDA device");
+}
+
+DeviceScope::~DeviceScope() {
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+cudaEvent_t EventPool::get(bool timing) {
+  auto& v = timing ? timed_ : plain_;
+  if (!v.empty()) {
+    cudaEvent_t e = v.back();
+    v.pop_back();
+    return e;
+  }
+  DeviceScope scope(dev_);
+  cudaEvent_t e;
+  ck(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming),
+     "cudaEventCreate");
+  return e;
+}
+
+void EventPool::release() noexcept {
+  for (cudaEvent_t e : plain_) cudaEventDestroy(e);
+  for (cudaEvent_t e : timed_) cudaEventDestroy(e);
+  plain_.clear();
+  timed_.clear();
+}
+
+void CipherCtx::ensure_copy_streams() {
+  if (s_h2d) return;
+  s_h2d = stream_get();
+  s_d2h = stream_get();
+}
+
+void CipherCtx::sync() {
+  for (cudaStream_t s : {s_h2d, s_work, s_d2h})
+    if (s) ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+}
+
+void CipherCtx::ensure_buffers(const Geom& g, uint32_t nslots) {
+  const uint64_t fb = g.frame_bytes;
+  const uint64_t scratch_need =
+      round_up(fb, 256) + 4 * uint64_t(g.n) * ((g.region + 4095) / 4096) + 256;
+  const bool generic = !plan_encrypt(g).fused;
+  if (scratch_bytes < scratch_need || (generic && !scratch[2])) {
+    sync();
+    for (auto& p : scratch) {
+      dfree(p);
+      p = nullptr;
+    }
+    scratch_bytes = 0;
+    dmalloc(&scratch[0], scratch_need, "cudaMalloc scratch");
+    dmalloc(&scratch[1], scratch_need, "cudaMalloc scratch");
+    if (generic) dmalloc(&scratch[2], scratch_need, "cudaMalloc scratch");
+    scratch_bytes = scratch_need;
+  }
+  if (shift_cap < g.side) {
+    sync();
+    dfree(d_shift);
+    d_shift = nullptr;
+    shift_cap = 0;
+    dmalloc(&d_shift, sizeof(int32_t) * g.side, "cudaMalloc shift");
+    shift_cap = g.side;
+  }
+  if (nslots && (slots.size() < nslots || slot_bytes < fb)) {
+    sync();
+    for (uint8_t* p : slots) dfree(p);
+    slots.assign(nslots, nullptr);
+    slot_bytes = 0;
+    for (auto& p : slots) dmalloc(&p, fb, "cudaMalloc frame slot");
+    slot_bytes = fb;
+    while (slot_free.size() < nslots) {
+      cudaEvent_t e;
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(e, s_d2h), "cudaEventRecord");
+      slot_free.push_back(e);
+    }
+  }
+}
+
+void CipherCtx::ensure_windows(uint64_t bytes_per_worker, uint32_t workers) {
+  const uint64_t need = bytes_per_worker * workers;
+  if (win_bytes >= need) return;
+  sync();
+  for (auto& w : win) {
+    dfree(w);
+    w = nullptr;
+  }
+  win_bytes = 0;
+  for (auto& w : win) dmalloc(&w, need, "cudaMalloc keystream window");
+  win_bytes = need;
+  for (auto& e : win_free) {
+    if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(e, s_work), "cudaEventRecord");
+  }
+}
+
+const double* CipherCtx::sine_for(uint32_t side) {
+  auto it = sines.find(side);
+  if (it != sines.end()) return it->second;
+  const std::vector<double> sv = sine_table(side);
+  double* d = nullptr;
+  dmalloc(&d, sizeof(double) * side, "cudaMalloc sine");
+  sines[side] = d;
+  // ordered before k_shift, which runs on s_work
+  // (pageable source: the call returns once the bytes are staged)
+  ck(cudaMemcpyAsync(d, sv.data(), sizeof(double) * side, cudaMemcpyHostToDevice, s_work),
+     "upload sine");
+  return d;
+}
+
+void CipherCtx::release() noexcept {
+  int prev = -1;  // everything below belongs to `dev` (stream pools are per device)
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != dev) cudaSetDevice(dev);
+  cudaStream_t fin = s_work;
+  for (cudaStream_t s : {s_h2d, s_d2h}) {
+    if (!s) continue;
+    cudaEvent_t e = nullptr;
+    if (fin && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(e, s) == cudaSuccess && cudaStreamWaitEvent(fin, e, 0) == cudaSuccess) {
+      cudaEventDestroy(e);
+    } else {
+      if (e) cudaEventDestroy(e);
+      cudaStreamSynchronize(s);
+    }
+  }
+  for (cudaEvent_t e : slot_free) cudaEventDestroy(e);
+  slot_free.clear();
+  for (auto& e : win_free) {
+    if (e) cudaEventDestroy(e);
+    e = nullptr;
+  }
+  for (uint8_t* p : slots) dfree(p, fin);
+  slots.clear();
+  for (auto& w : win) {
+    dfree(w, fin);
+    w = nullptr;
+  }
+  for (auto& kv : sines) dfree(kv.second, fin);
+  sines.clear();
+  for (uint8_t*& p : scratch) {
+    dfree(p, fin);
+    p = nullptr;
+  }
+  dfree(d_shift, fin);
+  d_shift = nullptr;
+  events.release();
+  for (cudaStream_t s : {owns_work ? s_work : nullptr, s_h2d, s_d2h}) stream_put(s);
+  s_work = s_h2d = s_d2h = nullptr;
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+}
+
 Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
-    : key_(key), n_(workers), r_(rounds), dev_(device), coord_(key) {
+    : Engine(key, workers, rounds, std::vector<int>{device}) {}
+
+Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds,
+               const std::vector<int>& devices)
+    : key_(key), n_(workers), r_(rounds), dev_(devices.empty() ? 0 : devices[0]), coord_(key) {
   // engine.cpp:168-179: coordinator first, then workers/rounds checks.
   if (workers == 0) raise(Errc::invalid_argument, "workers must be >= 1");
   if (rounds == 0 || rounds > 255)
     raise(Errc::invalid_argument, "rounds must be in 1..255");
+  if (devices.empty()) raise(Errc::invalid_argument, "no device given");
   const std::vector<WorkerLanes> lanes = coord_.derive_workers(n_);
 
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     raise(Errc::internal, "no CUDA device: the B200 engine has no CPU path");
-  int major = 0;
-  ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev_), "device query");
-  if (major != 10) {
-    cudaDeviceProp prop{};
-    cudaGetDeviceProperties(&prop, dev_);
-    raise(Errc::internal, std::string("engine is built for sm_100a; device is ") + prop.name);
+  for (int d : devices) {
+    if (d < 0 || d >= count) raise(Errc::invalid_argument, "device index out of range");
+    int major = 0;
+    ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d), "device query");
+    if (major != 10) {
+      cudaDeviceProp prop{};
+      cudaGetDeviceProperties(&prop, d);
+      raise(Errc::internal, std::string("engine is built for sm_100a; device is ") + prop.name);
+    }
   }
-  ck(cudaSetDevice(dev_), "cudaSetDevice");
-  configure_kernels_once(dev_);
   if (const char* e = std::getenv("CVE_B200_GEN_CHUNK")) {  // experiments only; 0 = unset
     const uint64_t v = std::strtoull(e, nullptr, 10) / 8 * 8;
     if (v) gen_chunk_cap_ = v;
   }
-
   one_stream_ = streams_per_handle() == 1;
   try {
+    for (int d : devices) configure_kernels_once(d);
+    DeviceScope scope(dev_);  // the caller's device is restored on return
     acquire(lanes);
+    init(devices);
   } catch (...) {
     release();  // the destructor does not run for a throwing constructor
     throw;
@@ -390,6 +603,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds, int device)
 }
 
 void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
+  gen_events_ = std::make_unique<EventPool>(dev_);
   s_gen_ = stream_get();
   for (auto& e : ver_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   for (auto& e : chain_done_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -408,18 +622,45 @@ void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
   ++st_.kernel_launches;
 }
 
+// Cipher contexts: the handle's own device (rounds share s_work with the
+// verifier), or one shard per entry of `devices` with its own streams.
+void Engine::init(const std::vector<int>& devices) {
+  if (devices.size() == 1) {
+    local_ = std::make_unique<CipherCtx>(dev_);
+    local_->s_work = s_work_;
+    return;
+  }
+  for (int d : devices) {
+    grant_peer_access(dev_, d);  // the shard reads the generator's ring
+    if (d != dev_) {
+      DeviceScope scope(d);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dev_, 0);
+      if (e != cudaSuccess) cudaGetLastError();  // already enabled / not capable: copies still work
+    }
+    DeviceScope scope(d);
+    auto c = std::make_unique<CipherCtx>(d);
+    c->s_work = stream_get();
+    c->owns_work = true;
+    shards_.push_back(std::move(c));
+  }
+}
+
 Engine::~Engine() { release(); }
 
 // Frees everything the engine holds; safe on a partially constructed engine
-// and idempotent.
+// and idempotent.  Restores the caller's device.
 void Engine::release() noexcept {
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   cudaSetDevice(dev_);
   // Asynchronous teardown: work still queued -- typically the generator's
   // run-ahead for a next frame that will never come -- finishes on the
   // device, and every buffer goes back to the pool in stream order after it,
   // so destroying a handle does not wait for it.  `fin` joins every stream.
   cudaStream_t fin = s_work_;
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_d2h_}) {
+  std::vector<cudaStream_t> others = {s_gen_};
+  if (local_) others.insert(others.end(), {local_->s_h2d, local_->s_d2h});
+  for (cudaStream_t s : others) {
     if (!s || s == fin) continue;
     cudaEvent_t e = nullptr;
     if (fin && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess &&
@@ -430,8 +671,16 @@ void Engine::release() noexcept {
       cudaStreamSynchronize(s);
     }
   }
-  for (auto& c : consumers_) ev_put(c.done);
+  for (auto& c : consumers_) {
+    // a shard's last window copy out of the ring must finish before the
+    // ring is freed behind `fin`
+    if (fin && c.pool->device() != dev_ && cudaStreamWaitEvent(fin, c.done, 0) != cudaSuccess)
+      cudaDeviceSynchronize();
+    c.pool->put(c.done);
+  }
   consumers_.clear();
+  for (auto& c : shards_) c->release();  // each in its own stream order
+  cudaSetDevice(dev_);
   for (auto& e : ver_done_) {
     if (e) cudaEventDestroy(e);  // pending events are released once complete
     e = nullptr;
@@ -440,35 +689,26 @@ void Engine::release() noexcept {
     if (e) cudaEventDestroy(e);
     e = nullptr;
   }
-  for (auto& g : gens_) ev_put(g.ev);
+  for (auto& g : gens_) gen_events_->put(g.ev);
   gens_.clear();
   for (auto& t : timed_) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
   }
   timed_.clear();
-  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
-  ev_pool_.clear();
-  for (cudaEvent_t e : tev_pool_) cudaEventDestroy(e);
-  tev_pool_.clear();
-  for (cudaEvent_t e : slot_free_) cudaEventDestroy(e);
-  slot_free_.clear();
-  for (uint8_t* p : slots_) dfree(p, fin);
-  slots_.clear();
-  for (auto& kv : sines_) dfree(kv.second, fin);
-  sines_.clear();
-  for (uint8_t*& p : scratch_) {
-    dfree(p, fin);
-    p = nullptr;
+  if (local_) {
+    local_->s_work = s_work_;  // freed below, in the order of s_work_
+    local_->release();
+    local_.reset();
   }
-  dfree(d_shift_, fin);
-  d_shift_ = nullptr;
+  shards_.clear();
+  if (gen_events_) gen_events_->release();
   dfree(ring_, fin);
   ring_ = nullptr;
   gen_.release(fin);
-  for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_h2d_, s_work_, s_d2h_})
-    stream_put(s);  // reused only once idle (stream_get)
-  s_gen_ = s_h2d_ = s_work_ = s_d2h_ = nullptr;
+  for (cudaStream_t s : {s_gen_ == s_work_ ? nullptr : s_gen_, s_work_}) stream_put(s);
+  s_gen_ = s_work_ = nullptr;
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 Geom Engine::geometry(uint32_t side) const {
@@ -497,34 +737,11 @@ uint32_t Engine::draw_and_check(uint32_t side, uint32_t count) {
   return 0;
 }
 
-cudaEvent_t Engine::ev_get() {
-  if (!ev_pool_.empty()) {
-    cudaEvent_t e = ev_pool_.back();
-    ev_pool_.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-  return e;
-}
-
-void Engine::ev_put(cudaEvent_t e) { ev_pool_.push_back(e); }
-
-cudaEvent_t Engine::tev_get() {
-  if (!tev_pool_.empty()) {
-    cudaEvent_t e = tev_pool_.back();
-    tev_pool_.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  ck(cudaEventCreate(&e), "cudaEventCreate");
-  return e;
-}
-
-void Engine::timed_begin(cudaStream_t s, bool chain, bool verify) {
+void Engine::timed_begin(EventPool& pool, cudaStream_t s, bool chain, bool verify) {
   Timed t{};
-  t.a = tev_get();
-  t.b = tev_get();
+  t.a = pool.get(true);
+  t.b = pool.get(true);
+  t.pool = &pool;
   t.chain = chain;
   t.verify = verify;
   ck(cudaEventRecord(t.a, s), "cudaEventRecord");
@@ -557,9 +774,10 @@ void Engine::fold_timings(bool wait) {
     } else {
       st_.cipher_ms += ms;
     }
-    tev_pool_.push_back(t.a);
-    tev_pool_.push_back(t.b);
+    t.pool->put(t.a, true);
+    t.pool->put(t.b, true);
   }
+  cudaGetLastError();  // cudaErrorNotReady from the queries is not an error
   timed_.swap(keep);
 }
 
@@ -587,64 +805,15 @@ void Engine::ensure_ring(uint64_t need) {
   const uint64_t launch = std::max<uint64_t>(8, ring_bytes_ / 4 / bpi_ / 8 * 8);
   const uint32_t iters = uint32_t(std::min<uint64_t>(launch, cap));
   if (iters > gen_.max_iters()) gen_.resize(iters);
-  for (auto& c : consumers_) ev_put(c.done);
+  for (auto& c : consumers_) c.pool->put(c.done);
   consumers_.clear();
-  for (auto& g : gens_) ev_put(g.ev);
+  for (auto& g : gens_) gen_events_->put(g.ev);
   gens_.clear();
-}
-
-void Engine::ensure_buffers(const Geom& g, uint32_t slots) {
-  const uint64_t fb = g.frame_bytes;
-  const uint64_t scratch_need =
-      round_up(fb, 256) + 4 * uint64_t(g.n) * ((g.region + 4095) / 4096) + 256;
-  const bool generic = !plan_encrypt(g).fused;
-  if (scratch_bytes_ < scratch_need || (generic && !scratch_[2])) {
-    synchronize();
-    for (auto& p : scratch_) {
-      dfree(p);
-      p = nullptr;
-    }
-    dmalloc(&scratch_[0], scratch_need, "cudaMalloc scratch");
-    dmalloc(&scratch_[1], scratch_need, "cudaMalloc scratch");
-    if (generic) dmalloc(&scratch_[2], scratch_need, "cudaMalloc scratch");
-    scratch_bytes_ = scratch_need;
-  }
-  if (shift_cap_ < g.side) {
-    synchronize();
-    dfree(d_shift_);
-    dmalloc(&d_shift_, sizeof(int32_t) * g.side, "cudaMalloc shift");
-    shift_cap_ = g.side;
-  }
-  if (slots && (slots_.size() < slots || slot_bytes_ < fb)) {
-    synchronize();
-    for (uint8_t* p : slots_) dfree(p);
-    slots_.assign(slots, nullptr);
-    for (auto& p : slots_) dmalloc(&p, fb, "cudaMalloc frame slot");
-    slot_bytes_ = fb;
-    while (slot_free_.size() < slots) {
-      cudaEvent_t e;
-      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-      ck(cudaEventRecord(e, s_d2h_), "cudaEventRecord");
-      slot_free_.push_back(e);
-    }
-  }
-}
-
-const double* Engine::sine_for(uint32_t side) {
-  auto it = sines_.find(side);
-  if (it != sines_.end()) return it->second;
-  const std::vector<double> s = sine_table(side);
-  double* d = nullptr;
-  dmalloc(&d, sizeof(double) * side, "cudaMalloc sine");
-  // ordered before k_shift, which runs on s_work
-  ck(cudaMemcpyAsync(d, s.data(), sizeof(double) * side, cudaMemcpyHostToDevice, s_work_),
-     "upload sine");
-  sines_[side] = d;
-  return d;
 }
 
 // Enqueue generator launches on s_gen until stream byte `end_byte` (per
 // worker) is produced.  Launches cover whole 8-iteration (48-byte) blocks.
+// Runs on dev_ (the caller's scope).
 void Engine::gen_until(uint64_t end_byte) {
   NvtxRange nvtx("cve: generator launches");
   uint64_t target = round_up((end_byte + bpi_ - 1) / bpi_, 8);
@@ -660,13 +829,14 @@ void Engine::gen_until(uint64_t end_byte) {
     const int slot = int(launches_ & 1);
     // (1) chain on s_gen, once the verifier is done with this slot's buffers
     if (launches_ >= 2) ck(cudaStreamWaitEvent(s_gen_, ver_done_[slot], 0), "wait slot");
-    timed_begin(s_gen_, true);
+    timed_begin(*gen_events_, s_gen_, true);
     gen_.chain(slot, uint32_t(chunk), s_gen_);
     timed_end(s_gen_);
     ck(cudaEventRecord(chain_done_[slot], s_gen_), "cudaEventRecord");
     // (2)+(3) verify, emit, fix up on s_work while the next chain runs.
     // Ring bytes below write_end - R get overwritten: their readers must be
-    // done.
+    // done (the rounds of a single-device handle, the window copies of a
+    // sharded one).
     ck(cudaStreamWaitEvent(s_work_, chain_done_[slot], 0), "wait chain");
     const uint64_t write_end = (gen_iters_ + chunk) * bpi_;
     if (write_end > ring_bytes_) {
@@ -674,14 +844,14 @@ void Engine::gen_until(uint64_t end_byte) {
       while (!consumers_.empty() && consumers_.front().lo < dead) {
         ck(cudaStreamWaitEvent(s_work_, consumers_.front().done, 0), "wait");
         if (consumers_.front().hi <= dead) {
-          ev_put(consumers_.front().done);
+          consumers_.front().pool->put(consumers_.front().done);
           consumers_.pop_front();
         } else {
           break;
         }
       }
     }
-    timed_begin(s_work_, false, true);
+    timed_begin(*gen_events_, s_work_, false, true);
     gen_.emit(slot, ring_, ring_bytes_, gen_iters_, uint32_t(chunk), s_work_);
     timed_end(s_work_);
     ck(cudaEventRecord(ver_done_[slot], s_work_), "cudaEventRecord");
@@ -690,7 +860,7 @@ void Engine::gen_until(uint64_t end_byte) {
     ++launches_;
     gen_iters_ += chunk;
     st_.keystream_iters += chunk;
-    GenMark m{gen_iters_ * bpi_, ev_get()};
+    GenMark m{gen_iters_ * bpi_, gen_events_->get()};
     ck(cudaEventRecord(m.ev, s_work_), "cudaEventRecord");
     gens_.push_back(m);
   }
@@ -698,14 +868,59 @@ void Engine::gen_until(uint64_t end_byte) {
 
 cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
   while (!gens_.empty() && gens_.front().end_byte < end_byte) {
-    ev_put(gens_.front().ev);
+    gen_events_->put(gens_.front().ev);
     gens_.pop_front();
   }
   return gens_.empty() ? nullptr : gens_.front().ev;  // null: already synced
 }
 
-void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
-                           bool decrypt) {
+// K4 + r rounds of one frame on c.s_work, which already waits for the
+// frame's input and keystream.  Round 0 reads buf; middle rounds ping-pong
+// the two scratch frames; the last round writes buf (r == 1 goes through
+// scratch and a copy).  The generic encrypt path stages y in a third
+// scratch frame.
+cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
+                                   bool decrypt, KsWindow ks, uint64_t lo) {
+  timed_begin(c.events, c.s_work, false, false);
+  launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
+  ++st_.kernel_launches;
+  const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
+  const uint64_t base = ks.pos;
+  const uint8_t* src = buf;
+  for (uint32_t step = 0; step < r_; ++step) {
+    const uint32_t k = decrypt ? r_ - 1 - step : step;
+    uint8_t* dst = (step + 1 == r_ && r_ > 1)
+                       ? buf
+                       : (src == c.scratch[0] ? c.scratch[1] : c.scratch[0]);
+    ks.pos = (base + uint64_t(k) * g.region) % ks.ring_bytes;
+    if (decrypt)
+      launch_decrypt_round(g, src, dst, ks, c.d_shift, c.s_work, &st_.kernel_launches);
+    else
+      launch_encrypt_round(plan, g, src, dst, ks, c.d_shift, c.scratch[2], c.s_work,
+                           &st_.kernel_launches);
+    src = dst;
+  }
+  if (r_ == 1)
+    ck(cudaMemcpyAsync(buf, src, g.frame_bytes, cudaMemcpyDeviceToDevice, c.s_work), "d2d");
+  timed_end(c.s_work);
+  (void)lo;
+  cudaEvent_t done = c.events.get();
+  ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
+  ++st_.frames;
+  return done;
+}
+
+// Run-ahead: start the next frame's keystream behind this one's, so a
+// caller's next call finds it (partly) generated.  Not after a handle's
+// first frame: a one-frame clip (BASELINE config C1) would leave a whole
+// frame of chain + verify work running after it is destroyed, where the
+// next clip's work collides with it.  From the second frame on the clip is
+// a stream of frames and the run-ahead pays.
+void Engine::after_frame(uint64_t need) {
+  if (st_.frames >= 2) gen_until(cons_ + need);
+}
+
+cudaEvent_t Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed, bool decrypt) {
   NvtxRange nvtx("cve: frame");
   const uint64_t need = uint64_t(r_) * g.region;
   const uint64_t lo = cons_;
@@ -713,44 +928,58 @@ void Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed,
   gen_until(lo + need);
   if (cudaEvent_t ge = gen_event_covering(lo + need))
     ck(cudaStreamWaitEvent(s_work_, ge, 0), "wait keystream");
+  cudaEvent_t done =
+      enqueue_rounds(*local_, buf, g, seed, decrypt, KsWindow{ring_, ring_bytes_, lo % ring_bytes_}, lo);
+  // the rounds read the ring: they are its consumer
+  consumers_.push_back(Consumer{lo, lo + need, done, &local_->events});
+  after_frame(need);
+  return done;
+}
 
-  timed_begin(s_work_, false, false);
-  launch_shift_table(sine_for(g.side), seed, d_shift_, g.side, s_work_);
-  ++st_.kernel_launches;
-  KsWindow ks{ring_, ring_bytes_, 0};
-  const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
-  // Round 0 reads buf; middle rounds ping-pong the two scratch frames; the
-  // last round writes buf (r == 1 goes through scratch and a copy).  The
-  // generic encrypt path stages y in a third scratch frame.
-  const uint8_t* src = buf;
-  for (uint32_t step = 0; step < r_; ++step) {
-    const uint32_t k = decrypt ? r_ - 1 - step : step;
-    uint8_t* dst = (step + 1 == r_ && r_ > 1)
-                       ? buf
-                       : (src == scratch_[0] ? scratch_[1] : scratch_[0]);
-    ks.pos = (lo + uint64_t(k) * g.region) % ring_bytes_;
-    if (decrypt)
-      launch_decrypt_round(g, src, dst, ks, d_shift_, s_work_, &st_.kernel_launches);
-    else
-      launch_encrypt_round(plan, g, src, dst, ks, d_shift_, scratch_[2], s_work_,
-                           &st_.kernel_launches);
-    src = dst;
+// Copies `rows` rows of `width` bytes between (possibly different) devices.
+static void copy_rows(uint8_t* dst, uint64_t dpitch, int ddev, const uint8_t* src, uint64_t spitch,
+               int sdev, uint64_t width, uint32_t rows, cudaStream_t s) {
+  if (ddev == sdev) {
+    ck(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToDevice, s),
+       "keystream window copy");
+    return;
   }
-  if (r_ == 1)
-    ck(cudaMemcpyAsync(buf, src, g.frame_bytes, cudaMemcpyDeviceToDevice, s_work_),
-       "d2d");
-  timed_end(s_work_);
-  Consumer c{lo, lo + need, ev_get()};
-  ck(cudaEventRecord(c.done, s_work_), "cudaEventRecord");
-  consumers_.push_back(c);
-  ++st_.frames;
-  // Run-ahead: start the next frame's keystream behind this one's, so a
-  // caller's next call finds it (partly) generated.  Not after a handle's
-  // first frame: a one-frame clip (BASELINE config C1) would leave a whole
-  // frame of chain + verify work running after it is destroyed, where the
-  // next clip's work collides with it.  From the second frame on the clip is
-  // a stream of frames and the run-ahead pays.
-  if (st_.frames >= 2) gen_until(cons_ + need);
+  cudaMemcpy3DPeerParms p{};
+  p.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(src), spitch, width, rows);
+  p.srcDevice = sdev;
+  p.dstPtr = make_cudaPitchedPtr(dst, dpitch, width, rows);
+  p.dstDevice = ddev;
+  p.extent = make_cudaExtent(width, rows, 1);
+  ck(cudaMemcpy3DPeerAsync(&p, s), "keystream window peer copy");
+}
+
+cudaEvent_t Engine::enqueue_shard_frame(CipherCtx& c, uint8_t* buf, const Geom& g,
+                                        uint32_t seed, bool decrypt) {
+  NvtxRange nvtx("cve: frame (shard)");
+  const uint64_t need = uint64_t(r_) * g.region;
+  const uint64_t lo = cons_;
+  cons_ += need;
+  gen_until(lo + need);
+  cudaEvent_t ge = gen_event_covering(lo + need);
+  DeviceScope scope(c.dev);
+  c.ensure_windows(need, n_);
+  const uint32_t w = c.win_next;
+  c.win_next = (c.win_next + 1) % CipherCtx::kWindows;
+  ck(cudaStreamWaitEvent(c.s_work, c.win_free[w], 0), "wait window");
+  if (ge) ck(cudaStreamWaitEvent(c.s_work, ge, 0), "wait keystream");
+  // worker i's window = ring stream bytes [lo, lo + need), wrapping at most once
+  const uint64_t pos = lo % ring_bytes_;
+  const uint64_t first = std::min(need, ring_bytes_ - pos);
+  copy_rows(c.win[w], need, c.dev, ring_ + pos, ring_bytes_, dev_, first, n_, c.s_work);
+  if (first < need)
+    copy_rows(c.win[w] + first, need, c.dev, ring_, ring_bytes_, dev_, need - first, n_,
+              c.s_work);
+  cudaEvent_t copied = c.events.get();
+  ck(cudaEventRecord(copied, c.s_work), "cudaEventRecord");
+  consumers_.push_back(Consumer{lo, lo + need, copied, &c.events});
+  cudaEvent_t done = enqueue_rounds(c, buf, g, seed, decrypt, KsWindow{c.win[w], need, 0}, lo);
+  ck(cudaEventRecord(c.win_free[w], c.s_work), "cudaEventRecord");
+  return done;
 }
 
 void Engine::run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt) {
@@ -764,73 +993,137 @@ void Engine::run_host_io(const HostIo& io, uint32_t side, uint32_t count, bool d
       !io.in_w || !io.in_h || !io.out_w || !io.out_h)
     raise(Errc::invalid_argument, "frame region exceeds the padded side");
   const Geom g = geometry(side);
-  if (!s_h2d_) {  // copy streams only for handles that use the host API
-    s_h2d_ = stream_get();
-    s_d2h_ = stream_get();
-  }
   ensure_ring(uint64_t(r_) * g.region);
-  ensure_buffers(g, kSlots);
+  std::vector<CipherCtx*> ctxs;
+  if (shards_.empty()) {
+    ctxs.push_back(local_.get());
+  } else {
+    for (auto& c : shards_) ctxs.push_back(c.get());
+  }
+  for (CipherCtx* c : ctxs) {
+    DeviceScope scope(c->dev);
+    c->ensure_copy_streams();  // copy streams only for handles that use the host API
+    c->ensure_buffers(g, kSlots);
+  }
   const uint64_t row = uint64_t(side) * 3;
   const uint64_t in_fb = uint64_t(io.in_w) * io.in_h * 3;
   const uint64_t out_fb = uint64_t(io.out_w) * io.out_h * 3;
 
   for (uint32_t f = 0; f < count; ++f) {
     const uint32_t seed = coord_.next_seed();
-    const uint32_t slot = f % kSlots;
+    CipherCtx& c = shards_.empty() ? *local_ : *shards_[shard_rr_++ % shards_.size()];
+    const uint32_t slot = c.slot_next;
+    c.slot_next = (c.slot_next + 1) % kSlots;
     const uint8_t* hin = io.in + uint64_t(f) * in_fb;
     uint8_t* hout = io.out + uint64_t(f) * out_fb;
-    uint8_t* dbuf = slots_[slot];
-    ck(cudaStreamWaitEvent(s_h2d_, slot_free_[slot], 0), "wait slot");
-    if (io.in_w == side && io.in_h == side) {
-      ck(cudaMemcpyAsync(dbuf, hin, g.frame_bytes, cudaMemcpyHostToDevice, s_h2d_), "H2D");
-    } else {  // pad on the device: only the w*h payload crosses PCIe
-      ck(cudaMemcpy2DAsync(dbuf, row, hin, uint64_t(io.in_w) * 3, uint64_t(io.in_w) * 3,
-                           io.in_h, cudaMemcpyHostToDevice, s_h2d_), "H2D 2D");
-      if (io.in_w < side)
-        ck(cudaMemset2DAsync(dbuf + uint64_t(io.in_w) * 3, row, 0,
-                             uint64_t(side - io.in_w) * 3, io.in_h, s_h2d_), "pad right");
-      if (io.in_h < side)
-        ck(cudaMemsetAsync(dbuf + uint64_t(io.in_h) * row, 0,
-                           uint64_t(side - io.in_h) * row, s_h2d_), "pad bottom");
+    uint8_t* dbuf = c.slots[slot];
+    cudaEvent_t done;
+    {
+      DeviceScope scope(c.dev);
+      ck(cudaStreamWaitEvent(c.s_h2d, c.slot_free[slot], 0), "wait slot");
+      if (io.in_w == side && io.in_h == side) {
+        ck(cudaMemcpyAsync(dbuf, hin, g.frame_bytes, cudaMemcpyHostToDevice, c.s_h2d), "H2D");
+      } else {  // pad on the device: only the w*h payload crosses PCIe
+        ck(cudaMemcpy2DAsync(dbuf, row, hin, uint64_t(io.in_w) * 3, uint64_t(io.in_w) * 3,
+                             io.in_h, cudaMemcpyHostToDevice, c.s_h2d), "H2D 2D");
+        if (io.in_w < side)
+          ck(cudaMemset2DAsync(dbuf + uint64_t(io.in_w) * 3, row, 0,
+                               uint64_t(side - io.in_w) * 3, io.in_h, c.s_h2d), "pad right");
+        if (io.in_h < side)
+          ck(cudaMemsetAsync(dbuf + uint64_t(io.in_h) * row, 0,
+                             uint64_t(side - io.in_h) * row, c.s_h2d), "pad bottom");
+      }
+      cudaEvent_t in = c.events.get();
+      ck(cudaEventRecord(in, c.s_h2d), "record");
+      ck(cudaStreamWaitEvent(c.s_work, in, 0), "wait H2D");
+      c.events.put(in);
     }
-    cudaEvent_t in = ev_get();
-    ck(cudaEventRecord(in, s_h2d_), "record");
-    ck(cudaStreamWaitEvent(s_work_, in, 0), "wait H2D");
-    ev_put(in);
-    enqueue_frame(dbuf, g, seed, decrypt);
-    ck(cudaStreamWaitEvent(s_d2h_, consumers_.back().done, 0), "wait work");
+    if (shards_.empty()) {
+      done = enqueue_frame(dbuf, g, seed, decrypt);  // the consumer list owns `done`
+    } else {
+      done = enqueue_shard_frame(c, dbuf, g, seed, decrypt);
+      after_frame(uint64_t(r_) * g.region);
+    }
+    DeviceScope scope(c.dev);
+    ck(cudaStreamWaitEvent(c.s_d2h, done, 0), "wait work");
+    if (!shards_.empty()) c.events.put(done);
     if (io.out_w == side && io.out_h == side) {
-      ck(cudaMemcpyAsync(hout, dbuf, g.frame_bytes, cudaMemcpyDeviceToHost, s_d2h_), "D2H");
+      ck(cudaMemcpyAsync(hout, dbuf, g.frame_bytes, cudaMemcpyDeviceToHost, c.s_d2h), "D2H");
     } else {  // crop on the way out
       ck(cudaMemcpy2DAsync(hout, uint64_t(io.out_w) * 3, dbuf, row, uint64_t(io.out_w) * 3,
-                           io.out_h, cudaMemcpyDeviceToHost, s_d2h_), "D2H 2D");
+                           io.out_h, cudaMemcpyDeviceToHost, c.s_d2h), "D2H 2D");
     }
-    ck(cudaEventRecord(slot_free_[slot], s_d2h_), "record");
+    ck(cudaEventRecord(c.slot_free[slot], c.s_d2h), "record");
   }
-  ck(cudaStreamSynchronize(s_d2h_), "frame pipeline");
+  for (CipherCtx* c : ctxs) ck(cudaStreamSynchronize(c->s_d2h), "frame pipeline");
 }
 
 void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
                         bool decrypt, cudaStream_t user) {
   NvtxRange nvtx("cve: frames (device-resident)");
+  if (!shards_.empty()) {
+    // a sharded handle's frames live on all its devices: run_device_sharded
+    raise(Errc::invalid_argument, "sharded handle: use the per-shard device API");
+  }
   draw_and_check(side, count);
   const Geom g = geometry(side);
   ensure_ring(uint64_t(r_) * g.region);
-  ensure_buffers(g, 0);
-  cudaEvent_t in = ev_get();
+  local_->ensure_buffers(g, 0);
+  cudaEvent_t in = gen_events_->get();
   ck(cudaEventRecord(in, user), "record user stream");
   ck(cudaStreamWaitEvent(s_work_, in, 0), "wait user stream");
-  ev_put(in);
+  gen_events_->put(in);
+  cudaEvent_t done = nullptr;
   for (uint32_t f = 0; f < count; ++f) {
     const uint32_t seed = coord_.next_seed();
-    enqueue_frame(d_px + uint64_t(f) * g.frame_bytes, g, seed, decrypt);
+    done = enqueue_frame(d_px + uint64_t(f) * g.frame_bytes, g, seed, decrypt);
   }
-  ck(cudaStreamWaitEvent(user, consumers_.back().done, 0), "join user stream");
+  ck(cudaStreamWaitEvent(user, done, 0), "join user stream");
+}
+
+void Engine::run_device_sharded(uint8_t* const* shard_px, uint32_t side, uint32_t count,
+                                bool decrypt, const cudaStream_t* users) {
+  NvtxRange nvtx("cve: frames (device-resident, sharded)");
+  if (shards_.empty()) {
+    run_device(shard_px[0], side, count, decrypt, users ? users[0] : nullptr);
+    return;
+  }
+  draw_and_check(side, count);
+  const Geom g = geometry(side);
+  ensure_ring(uint64_t(r_) * g.region);
+  const uint32_t G = uint32_t(shards_.size());
+  for (uint32_t i = 0; i < G && i < count; ++i) {
+    CipherCtx& c = *shards_[i];
+    DeviceScope scope(c.dev);
+    c.ensure_buffers(g, 0);
+    cudaEvent_t in = c.events.get();
+    ck(cudaEventRecord(in, users ? users[i] : nullptr), "record user stream");
+    ck(cudaStreamWaitEvent(c.s_work, in, 0), "wait user stream");
+    c.events.put(in);
+  }
+  std::vector<cudaEvent_t> last(G, nullptr);
+  for (uint32_t f = 0; f < count; ++f) {
+    const uint32_t seed = coord_.next_seed();
+    const uint32_t i = f % G;
+    CipherCtx& c = *shards_[i];
+    if (last[i]) c.events.put(last[i]);
+    last[i] = enqueue_shard_frame(c, shard_px[i] + uint64_t(f / G) * g.frame_bytes, g, seed,
+                                  decrypt);
+    after_frame(uint64_t(r_) * g.region);
+  }
+  for (uint32_t i = 0; i < G; ++i) {
+    if (!last[i]) continue;
+    DeviceScope scope(shards_[i]->dev);
+    ck(cudaStreamWaitEvent(users ? users[i] : nullptr, last[i], 0), "join user stream");
+    shards_[i]->events.put(last[i]);
+  }
 }
 
 void Engine::synchronize() {
-  for (cudaStream_t s : {s_gen_, s_h2d_, s_work_, s_d2h_})
+  for (cudaStream_t s : {s_gen_, s_work_})
     if (s) ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  if (local_) local_->sync();
+  for (auto& c : shards_) c->sync();
 }
 
 void Engine::peek(uint32_t worker, uint8_t* out, size_t len) {
@@ -930,9 +1223,9 @@ void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_
 
 KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind,
                                  int device, uint64_t max_bytes)
-    : n_(uint32_t(lanes.size())) {
-  ck(cudaSetDevice(device), "cudaSetDevice");
+    : n_(uint32_t(lanes.size())), dev_(device) {
   configure_kernels_once(device);
+  DeviceScope scope(device);  // the caller's device is restored on return
   try {
     s_ = stream_get();
     gen_.init(lanes, kind, s_, 0);
@@ -951,17 +1244,22 @@ KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind 
 KeystreamSource::~KeystreamSource() { release(); }
 
 void KeystreamSource::release() noexcept {
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != dev_) cudaSetDevice(dev_);
   if (s_) cudaStreamSynchronize(s_);
   gen_.release();
   dfree(d_buf_);
   d_buf_ = nullptr;
   stream_put(s_);
   s_ = nullptr;
+  if (prev >= 0 && prev != dev_) cudaSetDevice(prev);
 }
 
 // Generates whole chunks of max_iters iterations; a request that does not
 // end on a chunk boundary leaves the rest of the chunk for the next call.
 void KeystreamSource::next(uint8_t* host, uint64_t bytes) {
+  DeviceScope scope(dev_);
   const uint64_t cb = chunk_bytes();
   if (bytes > cb) raise(Errc::invalid_argument, "request larger than a chunk");
   uint64_t got = 0;

@@ -18,6 +18,15 @@
 // The keystream lives in one ring per worker (ring_bytes each).  Stream byte
 // s of worker i sits at ring[i*ring_bytes + s % ring_bytes]; the generator
 // never overwrites bytes a frame still has to read (event gating).
+//
+// A handle may also shard ONE clip across several devices (north star:
+// "independent frames of a clip are partitioned across the B200s"): the
+// generator (chain, verify, ring) stays on devices[0]; frame k is ciphered on
+// shard k mod G, which first pulls that frame's keystream window (r * region
+// bytes per worker, engine.cpp:198-205) from the ring with one peer copy per
+// contiguous piece, then runs the shift table and the rounds on its own
+// device and streams.  Frames stay independent given (seed, window), so no
+// collective is needed; only the copy crosses NVLink.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -25,6 +34,7 @@
 #include <cstdint>
 #include <deque>
 #include <map>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -62,6 +72,73 @@ struct EngineStats {
 // a lone clip 261 vs 251 frames/s).  Initial value: CVE_B200_STREAMS_PER_HANDLE.
 void set_streams_per_handle(int n);
 int streams_per_handle();
+
+// Runs on `dev` until the scope ends, then restores the caller's device.  If
+// no device can be queried (no driver), does nothing and lets the first CUDA
+// call report INTERNAL, after the host-side checks ran (reference order).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev);
+  ~DeviceScope();
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
+// Pool of CUDA events created on one device (events can only be recorded
+// on streams of their own device).
+class EventPool {
+ public:
+  explicit EventPool(int dev = 0) : dev_(dev) {}
+  ~EventPool() { release(); }
+  EventPool(const EventPool&) = delete;
+  EventPool& operator=(const EventPool&) = delete;
+  int device() const { return dev_; }
+  cudaEvent_t get(bool timing = false);
+  void put(cudaEvent_t e, bool timing = false) { (timing ? timed_ : plain_).push_back(e); }
+  void release() noexcept;
+
+ private:
+  int dev_;
+  std::vector<cudaEvent_t> plain_, timed_;
+};
+
+// Per-device resources of the cipher rounds of one handle: the handle's own
+// device, or one shard of a clip sharded across devices.
+struct CipherCtx {
+  static constexpr uint32_t kWindows = 2;  // keystream windows in flight (shards)
+  explicit CipherCtx(int device) : dev(device), events(device) {}
+  ~CipherCtx() { release(); }
+  CipherCtx(const CipherCtx&) = delete;
+  CipherCtx& operator=(const CipherCtx&) = delete;
+
+  int dev;
+  cudaStream_t s_work = nullptr;  // rounds (for the handle's own device: shared with verify)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // created on first host-API use
+  bool owns_work = false;
+  uint8_t* scratch[3] = {nullptr, nullptr, nullptr};
+  uint64_t scratch_bytes = 0;
+  int32_t* d_shift = nullptr;
+  uint32_t shift_cap = 0;
+  std::map<uint32_t, double*> sines;
+  std::vector<uint8_t*> slots;  // host-API frame slots
+  uint64_t slot_bytes = 0;
+  std::vector<cudaEvent_t> slot_free;
+  uint32_t slot_next = 0;
+  // sharded handles: keystream windows pulled from the generator's ring
+  uint8_t* win[kWindows] = {nullptr, nullptr};
+  uint64_t win_bytes = 0;
+  cudaEvent_t win_free[kWindows] = {nullptr, nullptr};
+  uint32_t win_next = 0;
+  EventPool events;
+
+  void ensure_copy_streams();
+  void ensure_buffers(const Geom& g, uint32_t nslots);
+  void ensure_windows(uint64_t bytes_per_worker, uint32_t workers);
+  const double* sine_for(uint32_t side);
+  void sync();
+  // Frees everything in the stream order of s_work (after all queued work).
+  void release() noexcept;
+};
 
 // Keystream generator of 2n lanes of either map on one device: the PLCM
 // kernels (prbg.cu: speculative chain, verify/emit, fix-up) or the LASM
@@ -107,6 +184,9 @@ class Generator {
 class Engine {
  public:
   Engine(const Key& key, uint32_t workers, uint32_t rounds, int device);
+  // One clip sharded over `devices` (size >= 1, entries may repeat): the
+  // generator runs on devices[0], frame k of the clip on devices[k mod G].
+  Engine(const Key& key, uint32_t workers, uint32_t rounds, const std::vector<int>& devices);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -115,6 +195,9 @@ class Engine {
   uint32_t rounds() const { return r_; }
   uint64_t seeds_drawn() const { return coord_.seeds_drawn(); }
   int device() const { return dev_; }
+  // Cipher shards: 1 for a single-device handle.
+  uint32_t shard_count() const { return shards_.empty() ? 1u : uint32_t(shards_.size()); }
+  int shard_device(uint32_t i) const { return shards_.empty() ? dev_ : shards_[i]->dev; }
 
   // `count` frames in host memory, in place.
   void run_host(uint8_t* px, uint32_t side, uint32_t count, bool decrypt);
@@ -132,6 +215,11 @@ class Engine {
   // `count` frames in device memory, in place, ordered on `user` stream.
   void run_device(uint8_t* d_px, uint32_t side, uint32_t count, bool decrypt,
                   cudaStream_t user);
+  // Sharded handles: batch frame f lives on shard f % G at
+  // shard_px[f % G] + (f / G) * frame_bytes, ordered on users[f % G]
+  // (entries may be null: the legacy default stream of that device).
+  void run_device_sharded(uint8_t* const* shard_px, uint32_t side, uint32_t count, bool decrypt,
+                          const cudaStream_t* users);
   void synchronize();
   void peek(uint32_t worker, uint8_t* out, size_t len);
   void prefetch(uint64_t bytes);
@@ -144,6 +232,7 @@ class Engine {
   struct Consumer {
     uint64_t lo, hi;
     cudaEvent_t done;
+    EventPool* pool;  // the device the event belongs to
   };
   struct GenMark {
     uint64_t end_byte;
@@ -151,21 +240,27 @@ class Engine {
   };
   struct Timed {
     cudaEvent_t a, b;
+    EventPool* pool;
     bool chain, verify;  // neither: cipher rounds
   };
 
+  void init(const std::vector<int>& devices);
   Geom geometry(uint32_t side) const;
   uint32_t draw_and_check(uint32_t side, uint32_t count);
   void ensure_ring(uint64_t need);
-  void ensure_buffers(const Geom& g, uint32_t slots);
-  const double* sine_for(uint32_t side);
   void gen_until(uint64_t end_byte);
   cudaEvent_t gen_event_covering(uint64_t end_byte);
-  void enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed, bool decrypt);
-  cudaEvent_t ev_get();
-  cudaEvent_t tev_get();
-  void ev_put(cudaEvent_t e);
-  void timed_begin(cudaStream_t s, bool chain, bool verify = false);
+  // Rounds of one frame on ctx (the keystream is read from `ks`); returns
+  // the event recorded on ctx.s_work behind them.
+  cudaEvent_t enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
+                             bool decrypt, KsWindow ks, uint64_t lo);
+  // Single-device handle: rounds read the ring directly.
+  cudaEvent_t enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed, bool decrypt);
+  // Sharded handle: pull the window into the shard, then the rounds there.
+  cudaEvent_t enqueue_shard_frame(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
+                                  bool decrypt);
+  void after_frame(uint64_t need);
+  void timed_begin(EventPool& pool, cudaStream_t s, bool chain, bool verify = false);
   void timed_end(cudaStream_t s);
   void fold_timings(bool wait);
   void acquire(const std::vector<WorkerLanes>& lanes);  // constructor's CUDA resources
@@ -176,8 +271,7 @@ class Engine {
   int dev_;
   Coordinator coord_;
 
-  // s_h2d_/s_d2h_ are created on first host-API use.
-  cudaStream_t s_gen_ = nullptr, s_h2d_ = nullptr, s_work_ = nullptr, s_d2h_ = nullptr;
+  cudaStream_t s_gen_ = nullptr, s_work_ = nullptr;
   cudaEvent_t chain_done_[2] = {nullptr, nullptr};
   cudaEvent_t ver_done_[2] = {nullptr, nullptr};
   uint64_t launches_ = 0;  // generator launches (slot = launches_ & 1)
@@ -193,17 +287,11 @@ class Engine {
   std::deque<Consumer> consumers_;
   std::deque<GenMark> gens_;
 
-  uint8_t* scratch_[3] = {nullptr, nullptr, nullptr};
-  uint64_t scratch_bytes_ = 0;
-  std::vector<uint8_t*> slots_;
-  uint64_t slot_bytes_ = 0;
-  std::vector<cudaEvent_t> slot_free_;
-  int32_t* d_shift_ = nullptr;
-  uint32_t shift_cap_ = 0;
-  std::map<uint32_t, double*> sines_;
+  std::unique_ptr<CipherCtx> local_;                // rounds on dev_ (single-device handles)
+  std::vector<std::unique_ptr<CipherCtx>> shards_;  // sharded handles
+  uint64_t shard_rr_ = 0;                           // host-API frames dealt so far
 
-  std::vector<cudaEvent_t> ev_pool_;
-  std::vector<cudaEvent_t> tev_pool_;  // timing-enabled events
+  std::unique_ptr<EventPool> gen_events_;  // events of dev_
   std::vector<Timed> timed_;
   Timed open_{};
   std::vector<float> prbg_times_;
@@ -232,6 +320,7 @@ class KeystreamSource {
  private:
   void release() noexcept;
   uint32_t n_;
+  int dev_;
   Generator gen_;
   uint8_t* d_buf_ = nullptr;
   cudaStream_t s_ = nullptr;

@@ -2,7 +2,7 @@
 
 Runs the reference's own C ABI (oracle/_ref/libcve_ref.so, compiled from
 /root/reference/proj/src by oracle/Makefile) on the seeded synthetic frames of
-paper_2302_07411_b200.synth and records:
+workloads.synth and records:
 
 * reference_unit.json -- literal golden constants from the reference's own
   unit tests (cited file:line), re-checked here against the reference.
@@ -38,7 +38,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(HERE))
 
-from paper_2302_07411_b200 import synth  # noqa: E402
+from workloads import synth  # noqa: E402
 from _oracle import Oracle, Reference  # noqa: E402
 
 PLCM_HEX = "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f"

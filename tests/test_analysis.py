@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import (Reference, ref_add_noise_file, ref_analyze, ref_crop_file,
                      ref_encrypt_file)
 

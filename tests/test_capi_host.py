@@ -115,7 +115,7 @@ def test_host_keying_matches_reference_goldens():
 @pytest.mark.parametrize("workers", [1, 8, 64, 128])
 def test_host_keying_matches_oracle(workers):
     from _oracle import Oracle
-    from paper_2302_07411_b200 import synth
+    from workloads import synth
     key = synth.det_key(workers + 77)
     lanes, seeds = cve.derive_worker_lanes(key, workers, 5)
     o = Oracle(key, workers)
@@ -135,7 +135,7 @@ def test_host_keying_lasm_matches_reference_goldens():
 @pytest.mark.parametrize("workers", [1, 8, 64])
 def test_host_keying_lasm_matches_oracle(workers):
     from _oracle import Oracle
-    from paper_2302_07411_b200 import synth
+    from workloads import synth
     key = synth.det_key_lasm(workers + 5)
     lanes, seeds = cve.derive_worker_lanes(key, workers, 5)
     o = Oracle(key, workers)

@@ -21,7 +21,7 @@ def _worker(rank, world, port, out):
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank),
                       MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import bench
-    from paper_2302_07411_b200 import synth
+    from workloads import synth
     d = bench.Dist(use_cuda=False)
     d.barrier()
     m = d.max(float(rank + 1) * 1.5)

@@ -9,7 +9,7 @@ import pytest
 
 import paper_2302_07411_b200 as cve
 from conftest import gpu_present
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import Reference, ref_decrypt_file, ref_encrypt_file
 
 PLCM = "005f633937dd9abf3f93ba8c762f1bd43fb8560e3cdd9aef3f7c74d008a265d13f"

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import Oracle, plcm_stream
 
 pytestmark = pytest.mark.gpu
@@ -348,29 +348,101 @@ def test_one_stream_handles_match_oracle():
 def test_every_frame_of_config_clips_vs_reference(name):
     # SURVEY 8(d) parity gate: per-frame digest equality with the reference
     # for EVERY frame of the clip (C3 240, C4 1000, C5 500 frames; digests of
-    # the reference's own ciphertext, tests/golden/clips.json).  Plaintext
+    # the reference's own ciphertext, tests/golden/clips.json), and the whole
+    # clip decrypted back by a fresh in-order handle (BASELINE C5 "encrypt +
+    # decrypt round-trip"; reference test_capi.cpp:116-134).  Plaintext
     # digests are checked too, so a drift in the synthetic frames would show
     # as such rather than as a cipher mismatch.
-    import multiprocessing as mp
+    from _clips import run_clip
     path = os.path.join(GOLD, "clips.json")
     if not os.path.exists(path):
         pytest.skip("tests/golden/clips.json not generated")
     g = load("clips.json")[name]
-    c = cve.Cipher(g["key"], g["workers"], g["rounds"])
-    batch = {"C3": 48, "C4": 25, "C5": 10}[name]
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(max(1, min(16, (os.cpu_count() or 2) - 1))) as pool:
-        frames = pool.imap(synth.config_frame_job, ((name, t) for t in range(g["frames"])),
-                           chunksize=2)
-        t = 0
-        while t < g["frames"]:
-            buf = np.stack([next(frames) for _ in range(min(batch, g["frames"] - t))])
-            for i in range(len(buf)):
-                assert sha(buf[i]) == g["plain_sha256"][t + i], (name, t + i, "plaintext")
-            c.encrypt_frames(buf)
-            for i in range(len(buf)):
-                assert sha(buf[i]) == g["cipher_sha256"][t + i], (name, t + i)
-            t += len(buf)
+    assert run_clip(name, g, g["plain_sha256"]) == g["frames"]
+
+
+@pytest.mark.parametrize("name,devices,mode,frames", [
+    ("C3", [0, 0], "host", 0),
+    ("C3", [0, 0, 0, 0], "sharded", 0),
+    ("C4", [0, 0, 0], "host", 60),
+    ("C4", [0, 0, 0, 0], "sharded", 48),
+    ("C5", [0, 0], "sharded", 20),
+])
+def test_sharded_clip_vs_reference(name, devices, mode, frames):
+    # One clip sharded over cipher devices (cve_cipher_create_devices; north
+    # star "independent frames of a clip are partitioned across the B200s"):
+    # the generator stays on devices[0], frame k runs on shard k mod G from
+    # its keystream window copied out of the ring.  Repeated device entries
+    # put G shards (own streams and buffers, window copies through the same
+    # code path) on the one GPU of the test box.  Every frame (C3) or a prefix
+    # (C4, C5) must match the reference digests and round-trip.
+    from _clips import run_clip
+    path = os.path.join(GOLD, "clips.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/clips.json not generated")
+    g = load("clips.json")[name]
+    h = cve.Cipher(g["key"], g["workers"], g["rounds"], devices=devices)
+    assert h.shards == devices
+    h.close()
+    assert run_clip(name, g, g["plain_sha256"], devices=devices, mode=mode,
+                    frames=frames) == (frames or g["frames"])
+
+
+def test_sharded_per_frame_calls_and_lasm_vs_oracle():
+    # Per-frame drop-in calls on a sharded handle are dealt round-robin over
+    # the shards; sides change between calls; a LASM key shards the same way.
+    for key in (synth.det_key(61), synth.det_key_lasm(61)):
+        o = Oracle(key, 4, 5)
+        h = cve.Cipher(key, 4, 5, devices=[0, 0, 0])
+        for t, side in enumerate([64, 64, 96, 64, 128, 96, 64]):
+            f = rand_frames(side, 1, 500 + t)[0]
+            want = f.copy()
+            assert o.encrypt(want) == 0
+            h.encrypt_frame(f)
+            assert np.array_equal(f, want), (key[:2], t, side)
+        assert h.seeds_drawn == 7
+
+
+def test_sharded_errors():
+    key = synth.det_key(62)
+    with pytest.raises(cve.CveError) as e:
+        cve.Cipher(key, 4, 5, devices=[0, 99])
+    assert e.value.status == cve.CVE_ERROR_INVALID_ARGUMENT
+    with pytest.raises(cve.CveError) as e:
+        cve.Cipher(key, 4, 5, devices=[])
+    assert e.value.status == cve.CVE_ERROR_INVALID_ARGUMENT
+    h = cve.Cipher(key, 4, 5, devices=[0, 0])
+    f = rand_frames(66, 1, 1)[0]  # 66 % 4 != 0: MISMATCH after the seed draw
+    with pytest.raises(cve.CveError) as e:
+        h.encrypt_frame(f)
+    assert e.value.status == cve.CVE_ERROR_MISMATCH and h.seeds_drawn == 1
+    torch = pytest.importorskip("torch")
+    d = torch.zeros((2, 64, 64, 3), dtype=torch.uint8, device="cuda")
+    with pytest.raises(cve.CveError) as e:  # device API of a single-device kind
+        h.encrypt_frames_device(d.data_ptr(), 64, 2)
+    assert e.value.status == cve.CVE_ERROR_INVALID_ARGUMENT
+
+
+def test_device_unchanged_by_handle_lifecycle():
+    # A handle restores the caller's current device on create, run and
+    # destroy (also when its engine lives on another device).
+    torch = pytest.importorskip("torch")
+    ndev = torch.cuda.device_count()
+    for dev in range(min(ndev, 2)):
+        torch.cuda.set_device(0)
+        cve.set_device(dev)
+        try:
+            h = cve.Cipher(synth.det_key(63), 4, 5)
+            assert torch.cuda.current_device() == 0
+            f = rand_frames(64, 1, 2)[0]
+            h.encrypt_frame(f)
+            assert torch.cuda.current_device() == 0
+            h.close()
+            assert torch.cuda.current_device() == 0
+            cve.keystream_generate([0.1, 0.2, 0.3, 0.4], 48)
+            assert torch.cuda.current_device() == 0
+        finally:
+            cve.set_device(0)
 
 
 SIDES, WORKERS, ROUNDS = [8, 16, 64, 512], [1, 2, 4, 8], [1, 5]

@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 from _oracle import Oracle, Reference, lasm_iterate, lasm_stream
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
@@ -305,26 +305,12 @@ def test_gpu_lasm_device_resident_and_sides_change():
 def test_gpu_lasm_every_frame_of_config_clips_vs_reference(name):
     # The per-frame parity gate of SURVEY 8(d), with a LASM key: the digest of
     # EVERY frame of the C3 (240), C4 (1000) and C5 (500) clips equals the
-    # reference's own (tests/golden/lasm_clips.json); plaintext digests from
+    # reference's own (tests/golden/lasm_clips.json), and a fresh in-order
+    # handle decrypts every frame back (round trip); plaintext digests from
     # clips.json guard the synthetic frames.
-    import multiprocessing as mp
-    import paper_2302_07411_b200 as cve
+    from _clips import run_clip
     for f in ("lasm_clips.json", "clips.json"):
         if not os.path.exists(os.path.join(GOLD, f)):
             pytest.skip(f"tests/golden/{f} not generated")
     g, plain = load("lasm_clips.json")[name], load("clips.json")[name]["plain_sha256"]
-    c = cve.Cipher(g["key"], g["workers"], g["rounds"])
-    batch = {"C3": 48, "C4": 25, "C5": 10}[name]
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(max(1, min(16, (os.cpu_count() or 2) - 1))) as pool:
-        frames = pool.imap(synth.config_frame_job, ((name, t) for t in range(g["frames"])),
-                           chunksize=2)
-        t = 0
-        while t < g["frames"]:
-            buf = np.stack([next(frames) for _ in range(min(batch, g["frames"] - t))])
-            for i in range(len(buf)):
-                assert sha(buf[i]) == plain[t + i], (name, t + i, "plaintext")
-            c.encrypt_frames(buf)
-            for i in range(len(buf)):
-                assert sha(buf[i]) == g["cipher_sha256"][t + i], (name, t + i)
-            t += len(buf)
+    assert run_clip(name, g, plain) == g["frames"]

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from _oracle import Oracle, Reference, plcm_stream
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 

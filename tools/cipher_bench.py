@@ -5,7 +5,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 for name in sys.argv[1:] or ["C1", "C3", "C4", "C5"]:
     c = synth.CONFIGS[name]; n = c["workers"]; side = synth.config_side(name)

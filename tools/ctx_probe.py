@@ -13,7 +13,7 @@ print("primary ctx retain", r, f"{1e3*(time.perf_counter()-t2):.0f} ms")
 sys.path.insert(0, os.getcwd())
 t3=time.perf_counter()
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 t4=time.perf_counter()
 h=cve.Cipher(synth.config_key("C4"), 64, 5); h.close()
 t5=time.perf_counter()

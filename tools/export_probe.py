@@ -4,7 +4,7 @@ import os, sys, tempfile, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import Reference
 key = synth.config_key("C4")
 d = tempfile.mkdtemp(dir="/dev/shm")

@@ -5,7 +5,7 @@ import os, sys, tempfile, time
 t0 = time.perf_counter()
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 t1 = time.perf_counter()
 c = synth.CONFIGS["C4"]; W, H, n = c["width"], c["height"], c["workers"]
 key = synth.config_key("C4")

@@ -3,7 +3,7 @@ frames after a warm-up, and the chain kernel's ns per iteration.  Tool."""
 import time, numpy as np, sys
 sys.path.insert(0, '.')
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 for name in ("C1", "C4"):
     c = synth.CONFIGS[name]; side = synth.config_side(name); n = c["workers"]
     key = synth.det_key_lasm(4242 + n)

@@ -6,7 +6,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import Reference
 for name in ("C1", "C2", "C3", "C4"):
     c = synth.CONFIGS[name]; n = c["workers"]; side = synth.config_side(name)

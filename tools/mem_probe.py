@@ -1,7 +1,7 @@
 import sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 torch.cuda.init(); torch.zeros(1).cuda()
 for name in ["C1", "C4"]:
     c = synth.CONFIGS[name]; side = synth.config_side(name)

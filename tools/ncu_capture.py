@@ -5,7 +5,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 name = "C4"; c = synth.CONFIGS[name]; side = synth.config_side(name); n = c["workers"]
 h = cve.Cipher(synth.config_key(name), n, 5)

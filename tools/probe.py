@@ -4,7 +4,7 @@ import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 for name in sys.argv[1:] or ["C1", "C4"]:
     c = synth.CONFIGS[name]

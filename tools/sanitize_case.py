@@ -5,7 +5,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 shapes = [(64, 4, 2), (96, 8, 1), (90, 3, 1), (48, 3, 1), (160, 16, 1), (16, 1, 1)]
 for side, n, r in shapes:

@@ -5,7 +5,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 from _oracle import ref_analyze, ref_encrypt_file, ref_decrypt_file
 key = synth.config_key("C1")
 d = tempfile.mkdtemp(dir="/dev/shm")

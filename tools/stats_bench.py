@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 
 side = synth.config_side("C4"); fb = side * side * 3; P = 8
 a = torch.from_numpy(np.stack([synth.config_frame("C4", 2 + t) for t in range(4)])).repeat(2, 1, 1, 1).contiguous().cuda()

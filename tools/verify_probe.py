@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2302_07411_b200 as cve
-from paper_2302_07411_b200 import synth
+from workloads import synth
 c = synth.CONFIGS["C4"]
 side = synth.config_side("C4")
 h = cve.Cipher(synth.config_key("C4"), c["workers"], 5)
