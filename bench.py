@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config lines")
     ap.add_argument("--no-rows", action="store_true",
                     help="skip the row f1/f3/f4 measurements")
+    ap.add_argument("--shard-devices", default="",
+                    help="debug: comma-separated cipher devices of the clip instead of one per "
+                         "rank (e.g. 0,0 runs the sharded path on one GPU)")
     ap.add_argument("--clips", type=int, default=32,
                     help="independent clips for the labelled multi-clip line (0: skip)")
     return ap.parse_args()
@@ -520,7 +523,7 @@ METRIC = "encrypted frames/s (5 rounds)"
 def frames_per_step(args) -> int:
     """Frames per step: --frames rounded up to a multiple of the GPU count, so
     every shard of the clip gets the same number of frames per step."""
-    g = max(1, args.gpus)
+    g = len(args.shard_devices.split(",")) if args.shard_devices else max(1, args.gpus)
     return (max(1, args.frames) + g - 1) // g * g
 
 
@@ -587,7 +590,8 @@ def run_reference(args) -> None:
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": scaling_of(args.gpus), "vs_baseline": None,
             "dtype": "f64/u8", "data": "synthetic",
-            "config": config_dict(name, F, args.gpus)}
+            "config": config_dict(name, F, len(args.shard_devices.split(","))
+                                  if args.shard_devices else args.gpus)}
     if not Reference.available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libcve_ref.so was not built"}))
@@ -639,8 +643,9 @@ def run_b200(args) -> None:
     c = synth.CONFIGS[name]
     side, n, F = synth.config_side(name), c["workers"], frames_per_step(args)
     fb = side * side * 3
-    G = dist.world
-    devs = list(range(G))
+    devs = ([int(v) for v in args.shard_devices.split(",")] if args.shard_devices
+            else list(range(dist.world)))
+    G = len(devs)
     key = synth.config_key(name)  # THE clip: one key, sharded over the GPUs
     pool = frame_pool(name, 8)
     lead = dist.rank == 0  # rank 0 drives the sharded clip on every GPU
@@ -650,9 +655,9 @@ def run_b200(args) -> None:
         hnp[t] = pool[t % len(pool)]
     stream = torch.cuda.current_stream()
     # frame f of a step lives on shard f % G (its own GPU's HBM)
-    shard_frames = [host[g::G].contiguous().to(f"cuda:{g}") for g in devs] if lead else []
-    shard_streams = [torch.cuda.current_stream(g) if g == dist.local else torch.cuda.Stream(device=g)
-                     for g in devs] if lead else []
+    shard_frames = [host[i::G].contiguous().to(f"cuda:{d}") for i, d in enumerate(devs)] \
+        if lead else []
+    shard_streams = ([stream] + [torch.cuda.Stream(device=d) for d in devs[1:]]) if lead else []
 
     def make(k):
         return cve.Cipher(k, n, synth.ROUNDS, devices=devs if G > 1 else None)
@@ -667,8 +672,8 @@ def run_b200(args) -> None:
                [s_.cuda_stream for s_ in shard_streams])
 
     def sync_all():
-        for g in (devs if lead else [dist.local]):
-            torch.cuda.synchronize(g)
+        for d in sorted(set(devs if lead else [dist.local])):
+            torch.cuda.synchronize(d)
 
     def timed(h, steps, decrypt=False):
         """Device time (ms) of `steps` steps: CUDA events on every shard's
@@ -676,14 +681,14 @@ def run_b200(args) -> None:
         e0 = [torch.cuda.Event(enable_timing=True) for _ in devs]
         e1 = [torch.cuda.Event(enable_timing=True) for _ in devs]
         sync_all()
-        for g in devs:
-            e0[g].record(shard_streams[g])
+        for i in range(G):
+            e0[i].record(shard_streams[i])
         for _ in range(steps):
             run_step(h, decrypt)
-        for g in devs:
-            e1[g].record(shard_streams[g])
+        for i in range(G):
+            e1[i].record(shard_streams[i])
         sync_all()
-        return max(e0[g].elapsed_time(e1[g]) for g in devs)
+        return max(e0[i].elapsed_time(e1[i]) for i in range(G))
 
     # ---- value: device-resident frames of the one clip ----
     enc = make(key) if lead else None
@@ -694,7 +699,7 @@ def run_b200(args) -> None:
         enc.take_prbg_times()
         st0 = enc.stats()
     dist.barrier()
-    with ClockSampler(devs if lead else [dist.local]) as clk:
+    with ClockSampler(sorted(set(devs)) if lead else [dist.local]) as clk:
         ms_local = timed(enc, args.steps) if lead else 0.0
     dist.barrier()
     ms = dist.max(ms_local)
@@ -850,7 +855,7 @@ def run_b200(args) -> None:
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling_of(G),
         "vs_baseline": None, "dtype": "f64/u8", "data": "synthetic",
-        "config": config_dict(name, F, dist.world),
+        "config": config_dict(name, F, G),
         "gbps": value * fb / 1e9,
         "gbps_payload": value * c["width"] * c["height"] * 3 / 1e9,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": F * fb,
