@@ -205,8 +205,8 @@ PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
     dmalloc(&b.verified_end, lanes_bytes, "cudaMalloc state");
     for (int k = 0; k < 2; ++k) {
       dmalloc(&b.ckpt[k], lanes_bytes, "cudaMalloc ckpt");
-      if (orbit_iters)
-        dmalloc(&b.orbit[k], uint64_t(orbit_iters) * lanes_bytes, "cudaMalloc orbit");
+      if (orbit_iters)  // one checkpoint per 8 iterations
+        dmalloc(&b.orbit[k], uint64_t(orbit_iters / 8) * lanes_bytes, "cudaMalloc orbit");
     }
     b.max_iters = orbit_iters;
     dmalloc(&b.bad, (nlanes / 2) * sizeof(unsigned), "cudaMalloc flags");
@@ -228,8 +228,8 @@ void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
     b.orbit[k] = nullptr;
   }
   b.max_iters = 0;
-  for (int k = 0; k < 2; ++k)
-    dmalloc(&b.orbit[k], uint64_t(iters) * nlanes * sizeof(double), "cudaMalloc orbit");
+  for (int k = 0; k < 2; ++k)  // one checkpoint per 8 iterations
+    dmalloc(&b.orbit[k], uint64_t(iters / 8) * nlanes * sizeof(double), "cudaMalloc orbit");
   b.max_iters = iters;
 }
 
@@ -321,7 +321,9 @@ void Generator::release(cudaStream_t after) noexcept {
 }
 
 uint32_t Generator::orbit_cap_iters() const {
-  const uint64_t per = (kind_ == MapKind::Lasm ? 16ull : 8ull) * nl_;
+  // orbit bytes per iteration: LASM keeps every (x, y); PLCM one 8-byte
+  // checkpoint per 8 iterations
+  const uint64_t per = (kind_ == MapKind::Lasm ? 16ull : 1ull) * nl_;
   const uint64_t iters = std::min<uint64_t>(kOrbitBytes / per, 1u << 20) / 8 * 8;
   return uint32_t(std::max<uint64_t>(iters, 8));
 }

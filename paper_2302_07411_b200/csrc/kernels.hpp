@@ -42,7 +42,8 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
 struct PrbgBuffers {
   double* state;          // nlanes: chain position (written by the chain)
   double* ckpt[2];        // nlanes: start point of launch L (slot L&1)
-  double* orbit[2];       // max_iters * nlanes: orbit values of launch L
+  double* orbit[2];       // (max_iters / 8) * nlanes: checkpoints of launch L, the
+                          // orbit value ending each 8-iteration group
   double* verified_end;   // nlanes: verified end point of the last launch
   unsigned* bad;          // nworkers: verification failure flags
   unsigned long long* replays;  // workers recomputed exactly (cumulative)
@@ -50,7 +51,7 @@ struct PrbgBuffers {
 };
 
 // (1) Chain: advances every lane by `iters` (multiple of 8, <= max_iters)
-// iterations, orbit values into orbit[slot], start point into ckpt[slot].
+// iterations, group checkpoints into orbit[slot], start point into ckpt[slot].
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
                        uint32_t iters, uint32_t nlanes, cudaStream_t s);
 // (2) Verify every step of launch `slot` against the reference's exact step

@@ -154,8 +154,12 @@ __global__ void __launch_bounds__(128)
 }
 
 // (1) The chain.  One orbit per thread, 4 warps per CTA, one CTA per SM, so
-// every warp owns an SM sub-partition's in-order issue.  Per step: the
-// speculative iteration and one coalesced 8-byte store of the orbit value.
+// every warp owns an SM sub-partition's in-order issue.  Per 8-iteration
+// group: 8 speculative iterations and ONE coalesced 8-byte store of the
+// group's last orbit value (a checkpoint).  plcm_fast is deterministic (IEEE
+// _rn intrinsics, integer compares, selects), so the verifier regenerates the
+// 7 values in between bit for bit from the previous checkpoint instead of
+// reading them: 1/8 of the stores on the chain and 1/8 of the orbit traffic.
 __global__ void __launch_bounds__(128, 1)
     k_prbg_chain(double* __restrict__ state, double* __restrict__ ckpt,
                  const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
@@ -168,11 +172,9 @@ __global__ void __launch_bounds__(128, 1)
   double* o = orbit + l;
   for (uint32_t i = 0; i < iters; i += 8) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      x = plcm_fast(x, c);
-      o[size_t(t) * nlanes] = x;
-    }
-    o += size_t(8) * nlanes;
+    for (int t = 0; t < 8; ++t) x = plcm_fast(x, c);
+    *o = x;
+    o += nlanes;
   }
   state[l] = x;
 }
@@ -180,10 +182,13 @@ __global__ void __launch_bounds__(128, 1)
 // (2) Verify every step in parallel against the reference's exact step, and
 // emit the keystream: 6 bytes per iteration per worker = the little-endian
 // low 48 mantissa bits of x_a ^ x_b (extract_bytes, chaos.cpp:46-56).
-// Thread = (lane, 8-iteration group), lanes fastest (coalesced orbit loads);
-// lanes a/b of a worker are shuffle partners: the even one emits iterations
-// 0-3 of the group, the odd one 4-7.  Group 0 also checks continuity: the
-// launch must start where the previous launch verifiably ended.
+// Thread = (lane, 8-iteration group), lanes fastest (coalesced checkpoint
+// loads); the group's 8 orbit values are regenerated from the previous
+// group's checkpoint with the chain's own plcm_fast and must end on the
+// group's checkpoint (so they are the values the chain walked).  Lanes a/b of
+// a worker are shuffle partners: the even one emits iterations 0-3 of the
+// group, the odd one 4-7.  Group 0 also checks continuity: the launch must
+// start where the previous launch verifiably ended.
 __global__ void __launch_bounds__(256)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
                        const double* __restrict__ verified_end,
@@ -211,18 +216,20 @@ __global__ void __launch_bounds__(256)
     const uint32_t gr = g0 + k * gs;
     const bool live = live_thread && gr < groups;
     const uint32_t g = live ? gr : groups - 1;
-    const size_t i0 = size_t(g) * 8;
     double x;
     bool cont = true;  // continuity with the previous launch (group 0 only)
     if (g) {
-      x = orbit[(i0 - 1) * nlanes + l];
+      x = orbit[size_t(g - 1) * nlanes + l];
     } else {
       x = ckpt[l];
       cont = x == verified_end[l];
     }
+    const double end = __ldg(orbit + size_t(g) * nlanes + l);
     double y[8];
+    y[0] = plcm_fast(x, c);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) y[t] = __ldg(orbit + (i0 + t) * nlanes + l);  // all in flight
+    for (int t = 1; t < 8; ++t) y[t] = plcm_fast(y[t - 1], c);
+    cont &= y[7] == end;  // the chain walked exactly these values
     bool suspect = false;
     bool ok = plcm_verify_fast(x, y[0], c, suspect);
 #pragma unroll
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(256)
                    w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
                    w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
     if (live) {
-      const uint64_t off = ((it0 + i0) * 6u) % ring_bytes;  // 48-byte aligned
+      const uint64_t off = ((it0 + uint64_t(g) * 8) * 6u) % ring_bytes;  // 48-byte aligned
       uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
       if (!odd) {
         *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
@@ -280,9 +287,9 @@ __global__ void k_prbg_fixup(const double* __restrict__ orbit,
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
   const uint32_t nl = 2 * nworkers;
-  if (!bad[w]) {
-    verified_end[2 * w] = orbit[size_t(iters - 1) * nl + 2 * w];
-    verified_end[2 * w + 1] = orbit[size_t(iters - 1) * nl + 2 * w + 1];
+  if (!bad[w]) {  // the launch's last checkpoint is its last orbit value
+    verified_end[2 * w] = orbit[size_t(iters / 8 - 1) * nl + 2 * w];
+    verified_end[2 * w + 1] = orbit[size_t(iters / 8 - 1) * nl + 2 * w + 1];
     return;
   }
   bad[w] = 0;
