@@ -14,12 +14,14 @@ namespace cveb {
 //   cthr     = largest double <= 1-p  (x > cthr  <=>  1 - x < p, exactly)
 //   a_b, a_d = offsets of the quotient correction term for cases B and D
 //   hp, hq   = p/2, q/2               (rounding-verification thresholds)
+//   nyl_*    = -yl_p, -yl_q           (the verifier's operand-selected step)
 //   plo      = low 32 bits of p
 struct LaneConst {
   double p, q;
   double yh_p, yl_p, yh_q, yl_q;
   double cthr, a_b, a_d;
   double hp, hq;
+  double nyl_p, nyl_q;
   uint32_t plo, pad;
 };
 

@@ -57,6 +57,8 @@ LaneConst make_lane_const(double p) {
   c.a_d = (one - c.p) * c.yl_q;
   c.hp = 0.5 * c.p;
   c.hq = 0.5 * c.q;
+  c.nyl_p = -c.yl_p;
+  c.nyl_q = -c.yl_q;
   uint64_t bits;
   std::memcpy(&bits, &c.p, 8);
   c.plo = uint32_t(bits);
@@ -133,6 +135,42 @@ __device__ __forceinline__ bool plcm_verify_fast(double x, double y, const LaneC
   return fabs(r) < thr;
 }
 
+// The verifier's step: regenerates y = plcm_fast(x) bit for bit -- the same
+// FMAs on the same operands, but the case's operands are selected BEFORE the
+// arithmetic, so one quotient is computed instead of four -- and checks that
+// y is the reference's correctly rounded quotient num/den, where num and den
+// are exactly the reference's (chaos.cpp:28-32: f = x > 0.5 ? 1 - x : x;
+// f < p ? f/p : (f - p)/q).  fold tests x >= 0.5; at x == 0.5, 1 - x == x,
+// so num and den are the reference's there too.  Same residual test and
+// suspect flags as plcm_verify_fast.
+__device__ __forceinline__ double plcm_regen_verify(double x, const LaneConst& c, bool& ok,
+                                                    bool& suspect) {
+  // The chain's predicates (x >= 0, so the integer compares there equal these
+  // FP64 compares).  Here they go to the FP64 pipe: the verifier is bound by
+  // the ALU pipe (selects, integer tests), the chain by FP64 latency.
+  const bool a = x < c.p, cc = x > c.cthr;
+  const bool fold = x >= 0.5;
+  const double t1 = __dsub_rn(1.0, x);
+  const double nb = __dsub_rn(x, c.p);
+  const double nd = __dsub_rn(t1, c.p);
+  const bool low = fold ? cc : a;  // f < p
+  const double num = fold ? (cc ? t1 : nd) : (a ? x : nb);
+  const double yh = low ? c.yh_p : c.yh_q;
+  // (-x) * yl == x * (-yl) exactly: the sign goes into the selected constant
+  const double yl = fold ? (cc ? c.nyl_p : c.nyl_q) : (a ? c.yl_p : c.yl_q);
+  const double off = fold ? (cc ? c.yl_p : c.a_d) : (a ? 0.0 : c.a_b);
+  const double y = __fma_rn(num, yh, __fma_rn(x, yl, off));
+  const unsigned hi = unsigned(__double2hiint(y));
+  const unsigned lo = unsigned(__double2loint(y));
+  const unsigned ex = hi & 0x7FF00000u;
+  const double r = __fma_rn(-y, low ? c.p : c.q, num);
+  const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
+  const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
+  suspect |= (lo == 0u) | (lo == c.plo) | (ex < (53u << 20));
+  ok &= fabs(r) < thr;
+  return y;
+}
+
 // Exact decision: the reference step itself (IEEE division + guard).
 __device__ __noinline__ bool plcm_verify_exact(double x, double y, const LaneConst& c) {
   return y == plcm_exact(x, c.p, c.q);
@@ -189,7 +227,15 @@ __global__ void __launch_bounds__(128, 1)
 // a worker are shuffle partners: the even one emits iterations 0-3 of the
 // group, the odd one 4-7.  Group 0 also checks continuity: the launch must
 // start where the previous launch verifiably ended.
-__global__ void __launch_bounds__(256)
+#ifndef VERIFY_ILP
+#define VERIFY_ILP 1
+#endif
+constexpr int kVerifyIlp = VERIFY_ILP;
+#ifndef VERIFY_MIN_BLOCKS
+#define VERIFY_MIN_BLOCKS 1
+#endif
+
+__global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
                        const double* __restrict__ verified_end,
                        const LaneConst* __restrict__ lcs,
@@ -210,63 +256,78 @@ __global__ void __launch_bounds__(256)
   const uint32_t g0 = uint32_t(me / nlanes);
   const LaneConst c = lcs[l];
   const uint32_t odd = l & 1u;
+  // kVerifyIlp groups per trip, regenerated interleaved: a group's 8 steps
+  // are one dependent chain, so independent groups are the ILP
   const uint32_t trips = (groups + gs - 1) / gs;
+  // ring offset of group g0 + k gs, advanced without a 64-bit modulo per trip
+  // (48 bytes per group; ring_bytes % 48 == 0 and every group is whole)
+  uint64_t off0 = ((it0 + uint64_t(g0) * 8) * 6u) % ring_bytes;
+  const uint64_t off_step = (uint64_t(gs) * 48u) % ring_bytes;
   bool flagged = false;
-  for (uint32_t k = 0; k < trips; ++k) {
-    const uint32_t gr = g0 + k * gs;
-    const bool live = live_thread && gr < groups;
-    const uint32_t g = live ? gr : groups - 1;
-    double x;
-    bool cont = true;  // continuity with the previous launch (group 0 only)
-    if (g) {
-      x = orbit[size_t(g - 1) * nlanes + l];
-    } else {
-      x = ckpt[l];
-      cont = x == verified_end[l];
-    }
-    const double end = __ldg(orbit + size_t(g) * nlanes + l);
-    double y[8];
-    y[0] = plcm_fast(x, c);
+  for (uint32_t k = 0; k < trips; k += kVerifyIlp) {
+    uint32_t g[kVerifyIlp];
+    bool live[kVerifyIlp], cont[kVerifyIlp], ok[kVerifyIlp], suspect[kVerifyIlp];
+    double x[kVerifyIlp], end[kVerifyIlp], y[kVerifyIlp][8];
 #pragma unroll
-    for (int t = 1; t < 8; ++t) y[t] = plcm_fast(y[t - 1], c);
-    cont &= y[7] == end;  // the chain walked exactly these values
-    bool suspect = false;
-    bool ok = plcm_verify_fast(x, y[0], c, suspect);
-#pragma unroll
-    for (int t = 1; t < 8; ++t) ok &= plcm_verify_fast(y[t - 1], y[t], c, suspect);
-    if (suspect) {  // rare: decide this group exactly
-      ok = true;
-      for (int t = 0; t < 8; ++t) ok &= plcm_verify_exact(t ? y[t - 1] : x, y[t], c);
-    }
-    flagged |= live && !(ok && cont);
-    uint32_t lo[8], hi[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      lo[t] = unsigned(__double2loint(y[t]));
-      hi[t] = unsigned(__double2hiint(y[t]));
-    }
-    uint32_t mlo[4], mhi[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t slo = odd ? lo[t] : lo[t + 4];
-      const uint32_t shi = odd ? hi[t] : hi[t + 4];
-      const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
-      const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
-      mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
-      mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
-    }
-    const uint32_t w0 = mlo[0], w1 = mhi[0] | (mlo[1] << 16),
-                   w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
-                   w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
-    if (live) {
-      const uint64_t off = ((it0 + uint64_t(g) * 8) * 6u) % ring_bytes;  // 48-byte aligned
-      uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
-      if (!odd) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
-        *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w4, w5);
+    for (int j = 0; j < kVerifyIlp; ++j) {
+      const uint32_t gr = g0 + (k + j) * gs;
+      live[j] = live_thread && gr < groups;
+      g[j] = live[j] ? gr : groups - 1;
+      cont[j] = true;  // continuity with the previous launch (group 0 only)
+      if (g[j]) {
+        x[j] = orbit[size_t(g[j] - 1) * nlanes + l];
       } else {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
-        *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w2, w3, w4, w5);
+        x[j] = ckpt[l];
+        cont[j] = x[j] == verified_end[l];
+      }
+      end[j] = __ldg(orbit + size_t(g[j]) * nlanes + l);
+      ok[j] = true;
+      suspect[j] = false;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+#pragma unroll
+      for (int j = 0; j < kVerifyIlp; ++j)
+        y[j][t] = plcm_regen_verify(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
+#pragma unroll
+    for (int j = 0; j < kVerifyIlp; ++j) {
+      cont[j] &= y[j][7] == end[j];  // the chain walked exactly these values
+      if (suspect[j]) {  // rare: decide this group exactly
+        ok[j] = true;
+        for (int t = 0; t < 8; ++t) ok[j] &= plcm_verify_exact(t ? y[j][t - 1] : x[j], y[j][t], c);
+      }
+      flagged |= live[j] && !(ok[j] && cont[j]);
+      uint32_t lo[8], hi[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        lo[t] = unsigned(__double2loint(y[j][t]));
+        hi[t] = unsigned(__double2hiint(y[j][t]));
+      }
+      uint32_t mlo[4], mhi[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t slo = odd ? lo[t] : lo[t + 4];
+        const uint32_t shi = odd ? hi[t] : hi[t + 4];
+        const uint32_t rlo = __shfl_xor_sync(kFull, slo, 1);
+        const uint32_t rhi = __shfl_xor_sync(kFull, shi, 1);
+        mlo[t] = (odd ? lo[t + 4] : lo[t]) ^ rlo;
+        mhi[t] = ((odd ? hi[t + 4] : hi[t]) ^ rhi) & 0xFFFFu;
+      }
+      const uint32_t w0 = mlo[0], w1 = mhi[0] | (mlo[1] << 16),
+                     w2 = (mlo[1] >> 16) | (mhi[1] << 16), w3 = mlo[2],
+                     w4 = mhi[2] | (mlo[3] << 16), w5 = (mlo[3] >> 16) | (mhi[3] << 16);
+      const uint64_t off = off0;  // of group g0 + (k + j) gs
+      off0 += off_step;
+      off0 -= off0 >= ring_bytes ? ring_bytes : 0;
+      if (live[j]) {
+        uint8_t* dst = ring + uint64_t(l >> 1) * ring_bytes + off + (odd ? 24 : 0);
+        if (!odd) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w0, w1, w2, w3);
+          *reinterpret_cast<uint2*>(dst + 16) = make_uint2(w4, w5);
+        } else {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+          *reinterpret_cast<uint4*>(dst + 8) = make_uint4(w2, w3, w4, w5);
+        }
       }
     }
   }
