@@ -1045,6 +1045,235 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// K3t: the inverse round on 2-D output tiles (side % 16 == 0, 16-byte
+// aligned frames and keystream) -- the production decrypt round.
+//
+// Output tile = rows a0 .. a0+tv-1 x columns o0 .. o0+wv-1 (tv <= 15,
+// wv <= W, W % 16 == 0).  Output pixel (a0+i, o0+j) is cipher pixel
+// (al, be) with al = (a0 + o0 + i + j) mod side, be = (o0 + j + shift[al])
+// mod side (inverse_confuse_rows, engine.cpp:49-64), inverse-diffused
+// elementwise from the cipher byte, the byte before it and the keystream
+// byte (engine.hpp:36-38).  The pixels with i + j = s all come from cipher
+// row al_s = (a0 + o0 + s) mod side, at the consecutive columns of
+// j in [max(0, s-tv+1), min(wv-1, s)]: the tile reads tv + wv - 1 runs of
+// <= tv pixels.  One staging phase: 64-byte cipher and keystream windows of
+// every run by cp.async, thread = run realigns, inverse-diffuses four bytes
+// at a time and stores its pixels as 32-bit slots of the tile; runs through
+// a band head (which needs the next band's recovered last byte, engine.cpp:
+// 271-276) or wrapping past the row end go pixel by pixel.  Then the tile's
+// tv row segments of 3 wv bytes are written with 16-byte stores.
+//
+// Unlike K3s (full-width tiles, 184-215 KB of shared memory, one CTA per
+// SM), a tile needs ~25 KB, so ~8 CTAs share an SM and hide each other's
+// staging latency.
+constexpr uint32_t kTileThreads = 256;
+constexpr uint32_t kTileMaxT = 15;
+constexpr uint32_t kTileMaxW = 128;
+constexpr uint32_t kTileMaxRuns = kTileMaxT + kTileMaxW - 1;  // <= kTileThreads
+constexpr uint32_t kTileDefer = 64;
+
+struct TileArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  const uint8_t* ring;
+  uint64_t ring_bytes;
+  uint64_t pos;
+  const int32_t* shift;
+  uint32_t side, n, rows, T, W;
+  uint32_t region;
+  FastDiv div_rows;
+  uint64_t frame_bytes;  // bounds checks only
+};
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_decrypt_round_tiles(const TileArgs a) {
+  extern __shared__ uint4 smem[];
+  __shared__ uint4 rinfo[kTileMaxRuns];  // P0, kp0 lo, kp0 hi, band | fast << 31
+  __shared__ uint32_t dlist[kTileDefer];
+  __shared__ uint32_t dcount;
+  const uint32_t tid = threadIdx.x, side = a.side, W = a.W;
+  const uint32_t a0 = blockIdx.y * a.T, o0 = blockIdx.x * W;
+  const uint32_t tv = min(a.T, side - a0), wv = min(W, side - o0);
+  const uint32_t nruns = tv + wv - 1;
+  const uint32_t slots_base = uint32_t(__cvta_generic_to_shared(smem));
+  const uint32_t win_base = slots_base + a.T * W * 4u;
+  const uint32_t region = a.region;
+  uint32_t diag = a0 + o0;  // al of run 0
+  diag -= diag >= side ? side : 0u;
+
+  // geometry of run s: cipher row al, first j, length, first column
+  struct Run {
+    uint32_t al, jlo, len, be_lo, band;
+  };
+  auto run_of = [&](uint32_t s) {
+    Run r;
+    r.al = diag + s;
+    r.al -= r.al >= side ? side : 0u;
+    r.jlo = s + 1 > tv ? s + 1 - tv : 0u;
+    r.len = min(wv - 1, s) - r.jlo + 1;
+    uint32_t b = o0 + r.jlo + uint32_t(a.shift[r.al]);  // < 3 side
+    b -= b >= side ? side : 0u;
+    b -= b >= side ? side : 0u;
+    r.be_lo = b;
+    r.band = fdiv(r.al, a.div_rows);
+    return r;
+  };
+  // slot of tile pixel (i, j); granules of 16 slots swizzled as in K2s/K3s
+  auto put = [&](uint32_t i, uint32_t j, uint32_t pix) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots_base + 4u * slot_word(i * W + j)),
+                 "r"(pix));
+  };
+  auto ks_at = [&](uint32_t band, uint32_t j) {  // keystream byte j of this round
+    uint64_t kp = a.pos + j;
+    if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    CVE_CHECK(band < a.n && kp < a.ring_bytes);
+    return uint32_t(__ldg(a.ring + uint64_t(band) * a.ring_bytes + kp));
+  };
+  // pixel m of run r, byte by byte from global
+  auto slow_pixel = [&](const Run& r, uint32_t m) {
+    const uint32_t nb = r.band + 1 == a.n ? 0 : r.band + 1;
+    uint32_t be = r.be_lo + m;
+    be -= be >= side ? side : 0u;
+    const uint32_t P = (r.al * side + be) * 3u;
+    uint32_t pix = 0;
+#pragma unroll
+    for (uint32_t ch = 0; ch < 3; ++ch) {
+      const uint32_t j = P + ch - r.band * region;
+      const uint32_t b = ks_at(r.band, j);
+      uint32_t prev;
+      if (j == 0) {  // band head: the next band's recovered last byte
+        const uint32_t L = (nb + 1) * region - 1;
+        const uint32_t bl = ks_at(nb, region - 1);
+        prev = (bl ^ __ldg(a.src + L) ^ __ldg(a.src + L - 1)) - bl;
+      } else {
+        prev = __ldg(a.src + P + ch - 1);
+      }
+      CVE_CHECK(P + ch < a.frame_bytes && (j == 0 || P + ch >= 1));
+      pix |= (((b ^ __ldg(a.src + P + ch) ^ prev) - b) & 0xFFu) << (8 * ch);
+    }
+    return pix;
+  };
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
+  if (tid == 0) dcount = 0;
+  if (tid < nruns) {
+    const Run r = run_of(tid);
+    const uint32_t P0 = (r.al * side + r.be_lo) * 3u;
+    uint64_t kp = a.pos + (P0 - r.band * region);
+    if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+    const bool head = r.al == r.band * a.rows && r.be_lo == 0;
+    const bool fast = r.be_lo + r.len <= side && !head;
+    rinfo[tid] = make_uint4(P0, uint32_t(kp), uint32_t(kp >> 32), r.band | (fast ? 0x80000000u : 0u));
+  }
+  __syncthreads();
+  // windows: 8 x 16 B per run (4 cipher from (P0 - 1) & ~15, 4 keystream)
+  for (uint32_t q = tid; q < nruns * 8u; q += kTileThreads) {
+    const uint32_t r = q >> 3, c = q & 7u;
+    const uint4 e = rinfo[r];
+    const uint32_t dst = win_base + r * 128u + 16u * (c ^ (r & 7u));
+    bool need = false;
+    const uint8_t* src = a.src;
+    if (e.w >> 31) {
+      const uint32_t len3 = 3u * (min(wv - 1, r) - (r + 1 > tv ? r + 1 - tv : 0u) + 1u);
+      if (c < 4) {
+        const uint32_t base = (e.x - 1) & ~15u;  // fast runs have P0 >= 1
+        need = base + 16u * c < e.x + len3;
+        if (need) src = a.src + base + 16u * c;
+        if (need) CVE_CHECK(within(src, 16, a.src, a.frame_bytes));
+      } else {
+        const uint64_t kp0 = (uint64_t(e.z) << 32) | e.y;
+        uint64_t kp = (kp0 & ~uint64_t(15)) + 16u * (c - 4);
+        if (kp >= a.ring_bytes) kp -= a.ring_bytes;
+        need = 16u * (c - 4) < (e.y & 15u) + len3;
+        if (need) src = a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes + kp;
+        if (need)
+          CVE_CHECK(within(src, 16, a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes,
+                           a.ring_bytes));
+      }
+    }
+    cp_async16(dst, src, need);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (tid < nruns) {
+    const uint4 e = rinfo[tid];
+    const uint32_t jlo = tid + 1 > tv ? tid + 1 - tv : 0u;
+    const uint32_t len = min(wv - 1, tid) - jlo + 1;
+    if (e.w >> 31) {
+      const uint32_t w = win_base + tid * 128u;
+      uint32_t V[16], R[12], K[12];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
+                     : "r"(w + 16u * (uint32_t(c) ^ (tid & 7u))));
+      realign12(V, (e.x - 1) & 15u, R);  // R byte 0 = c[P0-1], then c[P0..]
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
+                     : "r"(w + 16u * (uint32_t(c + 4) ^ (tid & 7u))));
+      realign12(V, e.y & 15u, K);
+      uint32_t D[12];
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const uint32_t cur = i < 11 ? __funnelshift_r(R[i], R[i + 1], 8) : (R[11] >> 8);
+        D[i] = sub_bytes(K[i] ^ cur ^ R[i], K[i]);
+      }
+#pragma unroll
+      for (int m = 0; m < int(kTileMaxT); ++m) {
+        if (uint32_t(m) >= len) break;
+        const int j = (3 * m) >> 2, sh = ((3 * m) & 3) * 8;
+        put(tid - jlo - uint32_t(m), jlo + uint32_t(m),
+            sh <= 8 ? (D[j] >> sh) : __funnelshift_r(D[j], D[j + 1], sh));
+      }
+    } else {  // band head or wrapping run: deferred (inline if the list is full)
+      const uint32_t i = atomicAdd(&dcount, 1u);
+      if (i < kTileDefer) {
+        dlist[i] = tid;
+      } else {
+        const Run r = run_of(tid);
+        for (uint32_t m = 0; m < len; ++m) put(tid - jlo - m, jlo + m, slow_pixel(r, m));
+      }
+    }
+  }
+  __syncthreads();
+  {  // deferred runs: one thread per pixel
+    const uint32_t nd = min(dcount, kTileDefer);
+    for (uint32_t it = tid; it < nd * kTileMaxT; it += kTileThreads) {
+      const uint32_t s = dlist[it / kTileMaxT], m = it % kTileMaxT;
+      const Run r = run_of(s);
+      if (m < r.len) put(s - r.jlo - m, r.jlo + m, slow_pixel(r, m));
+    }
+  }
+  __syncthreads();
+  // Output: row a0+i, columns o0 .. o0+wv-1 = 3 wv contiguous bytes, 16-byte
+  // aligned (o0, wv multiples of 16): 48-byte granules of 16 slots.
+  const uint32_t gpr = wv >> 4;  // granules per row
+  for (uint32_t q = tid; q < tv * gpr; q += kTileThreads) {
+    const uint32_t i = q / gpr, g = q - i * gpr;
+    const uint32_t u = (i * W >> 4) + g;  // granule index in the slot array
+    const uint4* sl = smem + 4 * u;
+    const uint32_t sw = (u >> 1) & 3u;
+    uint32_t y[12];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 v = sl[c ^ sw];
+      y[3 * c] = __byte_perm(v.x, v.y, 0x4210);
+      y[3 * c + 1] = __byte_perm(v.y, v.z, 0x5421);
+      y[3 * c + 2] = __byte_perm(v.z, v.w, 0x6542);
+    }
+    uint4* out4 = reinterpret_cast<uint4*>(a.dst + (uint64_t(a0 + i) * side + o0 + 16u * g) * 3u);
+    CVE_CHECK(within(out4, 48, a.dst, a.frame_bytes));
+    out4[0] = make_uint4(y[0], y[1], y[2], y[3]);
+    out4[1] = make_uint4(y[4], y[5], y[6], y[7]);
+    out4[2] = make_uint4(y[8], y[9], y[10], y[11]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic forward round for geometries whose band chunks do not fit one
 // cluster's shared memory: gather -> chunk aggregates -> band prefixes ->
 // chunk scans, through global scratch.
@@ -1336,6 +1565,28 @@ uint32_t plan_decrypt_slots(const Geom& g, size_t& smem) {
   return best;
 }
 
+// K3t tile: T = 15 rows (fewer if the side is smaller), W = the largest
+// multiple of 16 dividing the side, <= 128 (the runs tv + wv - 1 <= 142 fit
+// one CTA); shared memory = T*W slots + 128 B of windows per run.
+bool plan_decrypt_tiles(const Geom& g, uint32_t& T, uint32_t& W, size_t& smem) {
+  if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32) || std::getenv("CVE_B200_NO_TILES"))
+    return false;  // experiments only: CVE_B200_NO_TILES selects K3s
+  T = std::min<uint32_t>(kTileMaxT, g.side);
+  if (const char* e = std::getenv("CVE_B200_TILE_T")) T = std::max(1, std::min(atoi(e), int(T)));
+  W = 16;
+  for (uint32_t w = kTileMaxW; w >= 16; w -= 16)
+    if (g.side % w == 0) {
+      W = w;
+      break;
+    }
+  if (const char* e = std::getenv("CVE_B200_TILE_W")) {
+    const uint32_t w = uint32_t(atoi(e));
+    if (w >= 16 && w <= kTileMaxW && w % 16 == 0) W = w;
+  }
+  smem = size_t(T) * W * 4 + size_t(T + W - 1) * 128;
+  return true;
+}
+
 void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
                           KsWindow ks, const int32_t* shift, cudaStream_t s,
                           uint64_t* launches) {
@@ -1343,6 +1594,25 @@ void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
                        ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
                          reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
   size_t smem = 0;
+  uint32_t tT = 0, tW = 0;
+  if (aligned && plan_decrypt_tiles(g, tT, tW, smem)) {
+    TileArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
+               tT, tW, uint32_t(g.region), make_div(g.rows), g.frame_bytes};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((g.side + tW - 1) / tW, (g.side + tT - 1) / tT);
+    cfg.blockDim = dim3(kTileThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 0 : 1;  // experiments only
+    cudaLaunchKernelEx(&cfg, k_decrypt_round_tiles, a);
+    check_launch("decrypt_round_tiles");
+    ++*launches;
+    return;
+  }
   const uint32_t Ts = aligned ? plan_decrypt_slots(g, smem) : 0;
   if (Ts) {
     DecArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows,
