@@ -1066,10 +1066,14 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
 // Unlike K3s (full-width tiles, 184-215 KB of shared memory, one CTA per
 // SM), a tile needs ~25 KB, so ~8 CTAs share an SM and hide each other's
 // staging latency.
-constexpr uint32_t kTileThreads = 256;
+#ifndef TILE_THREADS
+#define TILE_THREADS 160
+#endif
+constexpr uint32_t kTileThreads = TILE_THREADS;  // >= the runs of the largest tile
 constexpr uint32_t kTileMaxT = 15;
 constexpr uint32_t kTileMaxW = 128;
-constexpr uint32_t kTileMaxRuns = kTileMaxT + kTileMaxW - 1;  // <= kTileThreads
+constexpr uint32_t kTileMaxRuns = kTileMaxT + kTileMaxW - 1;
+static_assert(kTileMaxRuns <= kTileThreads, "thread = run");
 constexpr uint32_t kTileDefer = 64;
 
 struct TileArgs {
@@ -1088,7 +1092,6 @@ struct TileArgs {
 __global__ void __launch_bounds__(kTileThreads)
     k_decrypt_round_tiles(const TileArgs a) {
   extern __shared__ uint4 smem[];
-  __shared__ uint4 rinfo[kTileMaxRuns];  // P0, kp0 lo, kp0 hi, band | fast << 31
   __shared__ uint32_t dlist[kTileDefer];
   __shared__ uint32_t dcount;
   const uint32_t tid = threadIdx.x, side = a.side, W = a.W;
@@ -1155,67 +1158,51 @@ __global__ void __launch_bounds__(kTileThreads)
   };
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
   if (tid == 0) dcount = 0;
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
   if (tid < nruns) {
+    // thread = run: its own windows (cp.async), realigned once they land
     const Run r = run_of(tid);
     const uint32_t P0 = (r.al * side + r.be_lo) * 3u;
     uint64_t kp = a.pos + (P0 - r.band * region);
     if (kp >= a.ring_bytes) kp -= a.ring_bytes;
     const bool head = r.al == r.band * a.rows && r.be_lo == 0;
     const bool fast = r.be_lo + r.len <= side && !head;
-    rinfo[tid] = make_uint4(P0, uint32_t(kp), uint32_t(kp >> 32), r.band | (fast ? 0x80000000u : 0u));
-  }
-  __syncthreads();
-  // windows: 8 x 16 B per run (4 cipher from (P0 - 1) & ~15, 4 keystream)
-  for (uint32_t q = tid; q < nruns * 8u; q += kTileThreads) {
-    const uint32_t r = q >> 3, c = q & 7u;
-    const uint4 e = rinfo[r];
-    const uint32_t dst = win_base + r * 128u + 16u * (c ^ (r & 7u));
-    bool need = false;
-    const uint8_t* src = a.src;
-    if (e.w >> 31) {
-      const uint32_t len3 = 3u * (min(wv - 1, r) - (r + 1 > tv ? r + 1 - tv : 0u) + 1u);
-      if (c < 4) {
-        const uint32_t base = (e.x - 1) & ~15u;  // fast runs have P0 >= 1
-        need = base + 16u * c < e.x + len3;
-        if (need) src = a.src + base + 16u * c;
-        if (need) CVE_CHECK(within(src, 16, a.src, a.frame_bytes));
-      } else {
-        const uint64_t kp0 = (uint64_t(e.z) << 32) | e.y;
-        uint64_t kp = (kp0 & ~uint64_t(15)) + 16u * (c - 4);
-        if (kp >= a.ring_bytes) kp -= a.ring_bytes;
-        need = 16u * (c - 4) < (e.y & 15u) + len3;
-        if (need) src = a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes + kp;
-        if (need)
-          CVE_CHECK(within(src, 16, a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes,
-                           a.ring_bytes));
+    const uint32_t w = win_base + tid * 128u;
+    if (fast) {
+      const uint32_t cb = (P0 - 1) & ~15u;  // fast runs have P0 >= 1
+      const uint32_t nc = (P0 + 3u * r.len - cb + 15u) >> 4;  // bytes P0-1 .. P0+3len-1
+      const uint8_t* ks = a.ring + uint64_t(r.band) * a.ring_bytes;
+      const uint64_t kb = kp & ~uint64_t(15);
+      const uint32_t nk = (uint32_t(kp & 15u) + 3u * r.len + 15u) >> 4;
+#pragma unroll
+      for (uint32_t c = 0; c < 4; ++c) {
+        if (c < nc) CVE_CHECK(within(a.src + cb + 16u * c, 16, a.src, a.frame_bytes));
+        cp_async16(w + 16u * (c ^ (tid & 7u)), a.src + cb + 16u * c, c < nc);
       }
-    }
-    cp_async16(dst, src, need);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  if (tid < nruns) {
-    const uint4 e = rinfo[tid];
-    const uint32_t jlo = tid + 1 > tv ? tid + 1 - tv : 0u;
-    const uint32_t len = min(wv - 1, tid) - jlo + 1;
-    if (e.w >> 31) {
-      const uint32_t w = win_base + tid * 128u;
+#pragma unroll
+      for (uint32_t c = 0; c < 4; ++c) {
+        uint64_t q = kb + 16u * c;
+        q -= q >= a.ring_bytes ? a.ring_bytes : 0;
+        if (c < nk) CVE_CHECK(within(ks + q, 16, ks, a.ring_bytes));
+        cp_async16(w + 16u * ((c + 4) ^ (tid & 7u)), ks + q, c < nk);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();  // this thread's own copies: no CTA barrier needed
       uint32_t V[16], R[12], K[12];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
                      : "r"(w + 16u * (uint32_t(c) ^ (tid & 7u))));
-      realign12(V, (e.x - 1) & 15u, R);  // R byte 0 = c[P0-1], then c[P0..]
+      realign12(V, (P0 - 1) & 15u, R);  // R byte 0 = c[P0-1], then c[P0..]
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
                      : "r"(w + 16u * (uint32_t(c + 4) ^ (tid & 7u))));
-      realign12(V, e.y & 15u, K);
+      realign12(V, uint32_t(kp & 15u), K);
       uint32_t D[12];
 #pragma unroll
       for (int i = 0; i < 12; ++i) {
@@ -1224,9 +1211,9 @@ __global__ void __launch_bounds__(kTileThreads)
       }
 #pragma unroll
       for (int m = 0; m < int(kTileMaxT); ++m) {
-        if (uint32_t(m) >= len) break;
+        if (uint32_t(m) >= r.len) break;
         const int j = (3 * m) >> 2, sh = ((3 * m) & 3) * 8;
-        put(tid - jlo - uint32_t(m), jlo + uint32_t(m),
+        put(tid - r.jlo - uint32_t(m), r.jlo + uint32_t(m),
             sh <= 8 ? (D[j] >> sh) : __funnelshift_r(D[j], D[j + 1], sh));
       }
     } else {  // band head or wrapping run: deferred (inline if the list is full)
@@ -1234,8 +1221,7 @@ __global__ void __launch_bounds__(kTileThreads)
       if (i < kTileDefer) {
         dlist[i] = tid;
       } else {
-        const Run r = run_of(tid);
-        for (uint32_t m = 0; m < len; ++m) put(tid - jlo - m, jlo + m, slow_pixel(r, m));
+        for (uint32_t m = 0; m < r.len; ++m) put(tid - r.jlo - m, r.jlo + m, slow_pixel(r, m));
       }
     }
   }
@@ -1393,6 +1379,9 @@ void configure_cipher_kernels() {
   cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_decrypt_round_slots, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(kSlotSmemMax));
+  // K3t: ~26 KB tiles, 8 per SM need the whole carveout as shared memory
+  cudaFuncSetAttribute(k_decrypt_round_tiles, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       int(cudaSharedmemCarveoutMaxShared));
   for (auto k : {k_decrypt_round<true>, k_decrypt_round<false>})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBudget));
 }
