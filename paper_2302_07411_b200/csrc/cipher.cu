@@ -480,23 +480,25 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
     b0 = (sr * side + o0) * 3u;
   };
   const uint32_t nstages = (side + kStageRows - 1) / kStageRows;
-  // Thread tid copies chunk (tid & 3) of rows (tid >> 2) + 128 i of a stage.
-  // b0(sr) = 3 (sr (side - 1) + al0) (+ 3 side once sr > al0).
-  const uint32_t cpc = tid & 3u, cpr = tid >> 2;
-  const uint32_t cp_dst = win_base + cpr * kWinBytes + 16u * (cpc ^ ((cpr >> 1) & 3u));
-  auto issue_stage = [&](uint32_t st) {
-    const uint32_t dst0 = cp_dst + (st & 1u) * kStageBytes;
+  // Thread tid owns source row st * kStageRows + tid of stage st: it copies
+  // the row's aligned 64-byte window (the chunks its run touches) into its
+  // own window slot of buffer st & 1, and repacks it once its copies land --
+  // no CTA barrier between stages.  Stage st + 1 is in flight during st.
+  auto issue_row = [&](uint32_t st) {
+    const uint32_t sr = st * kStageRows + tid;
+    const uint32_t w = win_base + (st & 1u) * kStageBytes + tid * kWinBytes;
+    const uint32_t sw = (tid >> 1) & 3u;
+    uint32_t o0 = 0, b0 = 0;
+    if (sr < side) run_of(sr, o0, b0);
+    // runs that wrap past the row end are read by the deferred pass (their
+    // window could run past the end of the frame: last chunk, row side-1)
+    const bool live = sr < side && o0 + cr <= side;
+    const uint8_t* src = a.src + (b0 & ~15u);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t sr = st * kStageRows + cpr + 128u * i;
-      const bool wraps = sr > al0;  // o0 = al0 - sr (+ side)
-      const uint32_t b0 = 3u * (sr * (side - 1) + al0) + (wraps ? 3u * side : 0u);
-      const uint32_t o0 = al0 - sr + (wraps ? side : 0u);
-      // runs that wrap past the row end are read by the deferred pass; their
-      // window could run past the end of the frame (last chunk, row side-1)
-      const bool need = sr < side && o0 + cr <= side && 16u * cpc < (b0 & 15u) + 3u * cr;
-      if (need) CVE_CHECK(within(a.src + (b0 & ~15u) + 16u * cpc, 16, a.src, a.frame_bytes));
-      cp_async16(dst0 + 128u * kWinBytes * i, a.src + (b0 & ~15u) + 16u * cpc, need);
+    for (uint32_t c = 0; c < 4; ++c) {
+      const bool need = live && 16u * c < (b0 & 15u) + 3u * cr;
+      if (need) CVE_CHECK(within(src + 16u * c, 16, a.src, a.frame_bytes));
+      cp_async16(w + 16u * (c ^ sw), src + 16u * c, need);
     }
     cp_async_commit();
   };
@@ -511,8 +513,7 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
   uint4 kv[3];
   load_ks(tid, kv);  // first super-tile's keystream (independent of the frame)
   asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
-  issue_stage(0);
-  if (nstages > 1) issue_stage(1);
+  issue_row(0);
   for (uint32_t t = tid; t < cr; t += kSlotThreads) {
     uint32_t c = t + uint32_t(a.shift[al0 + t]);
     cks[t] = c >= side ? c - side : c;
@@ -534,11 +535,12 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
       asm volatile("st.shared.u32 [%0], %1;" ::"r"(slots_base + 4u * slot_word(sl)), "r"(pix));
     };
     for (uint32_t st = 0; st < nstages; ++st) {
-      if (st + 1 < nstages)
+      if (st + 1 < nstages) {
+        issue_row(st + 1);
         cp_async_wait<1>();
-      else
+      } else {
         cp_async_wait<0>();
-      __syncthreads();
+      }
       const uint32_t sr = st * kStageRows + tid;
       if (sr < side) {
         uint32_t o0, b0;
@@ -567,10 +569,6 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
             put(k, o0, sh <= 8 ? (A[j] >> sh) : __funnelshift_r(A[j], A[j + 1], sh));
           }
         }  // runs that wrap past the row end: deferred, below
-      }
-      if (st + 2 < nstages) {
-        __syncthreads();  // every thread is done with this stage's windows
-        issue_stage(st + 2);
       }
     }
     // The cr - 1 source rows whose run wraps past the row end are rows
