@@ -311,6 +311,17 @@ CVE_B200_API cve_status cve_set_device(int device);
  * for many concurrent clips). */
 CVE_B200_API cve_status cve_set_streams_per_handle(uint32_t streams);
 
+/* Round fusion for handles created afterwards (process-wide; default 0 or
+ * $CVE_B200_ROUND_FUSION).  1: frames that fit one thread-block cluster
+ * (side % 16 == 0 and two packed copies of a CTA's whole bands in 227 KB: up
+ * to ~768^2) are encrypted with ALL rounds in one cluster kernel -- the frame
+ * is read from and written to HBM once and every round stays in distributed
+ * shared memory, on 8-16 SMs per frame.  0: one kernel per round over the
+ * whole GPU (measured faster on B200, per frame and for many concurrent
+ * clips).  Output is identical in both modes.  Other values ->
+ * INVALID_ARGUMENT. */
+CVE_B200_API cve_status cve_set_round_fusion(uint32_t mode);
+
 /* Copies the next `len` keystream bytes of subframe generator `worker` to
  * host memory WITHOUT consuming them from the cipher's stream (diagnostics /
  * parity; the reference's per-worker Prbg output, chaos.cpp:143-153). */

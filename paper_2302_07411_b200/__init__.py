@@ -108,6 +108,7 @@ def _load() -> C.CDLL:
         "cve_cipher_synchronize": (C.c_int, [vp]),
         "cve_set_device": (C.c_int, [C.c_int]),
         "cve_set_streams_per_handle": (C.c_int, [C.c_uint32]),
+        "cve_set_round_fusion": (C.c_int, [C.c_uint32]),
         "cve_cipher_peek_keystream": (C.c_int, [vp, C.c_uint32, vp, C.c_size_t]),
         "cve_cipher_prefetch_keystream": (C.c_int, [vp, C.c_uint64]),
         "cve_cipher_get_stats": (C.c_int, [vp, C.POINTER(Stats)]),
@@ -464,6 +465,13 @@ class Cipher:
 
 def set_device(device: int) -> None:
     _check(lib.cve_set_device(device))
+
+
+def set_round_fusion(mode: int) -> None:
+    """1 = all rounds of a frame in one thread-block cluster kernel wherever the
+    frame fits (<= ~768^2); 0 (default) = one kernel per round.  Output is
+    identical in both modes."""
+    _check(lib.cve_set_round_fusion(mode))
 
 
 def set_streams_per_handle(streams: int) -> None:

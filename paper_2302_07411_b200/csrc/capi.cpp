@@ -413,6 +413,10 @@ cve_status cve_set_streams_per_handle(uint32_t streams) {
   return guarded([&] { cveb::set_streams_per_handle(int(streams)); });
 }
 
+cve_status cve_set_round_fusion(uint32_t mode) {
+  return guarded([&] { cveb::set_round_fusion(int(mode)); });
+}
+
 cve_status cve_cipher_peek_keystream(cve_cipher* cipher, uint32_t worker,
                                      uint8_t* out, size_t len) {
   return guarded([&] {

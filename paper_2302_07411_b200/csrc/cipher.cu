@@ -1258,6 +1258,280 @@ __global__ void __launch_bounds__(kTileThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K6: ALL rounds of one frame in one thread-block cluster (frames up to
+// ~768^2).  CTA q of the CL-CTA cluster owns the R = side/CL
+// destination rows al0 = qR .. qR+R-1 -- whole bands (R % rows == 0), so the
+// diffusion scan never crosses a CTA -- as a packed slab of R*side*3 bytes
+// in each of two shared-memory buffers.
+//   load:  one TMA bulk copy (cp.async.bulk, mbarrier completion) of the
+//          CTA's slab of the plaintext into buffer 0;
+//   round: gather y = confuse(x) from the cluster's source buffers through
+//          distributed shared memory (every source row sr holds the CTA's
+//          run of R pixels at columns (al0 - sr) mod side ...: 16-pixel
+//          pieces, a 64-byte window each) into the local other buffer; then
+//          the XOR-prefix diffusion of each local band in place, with the
+//          keystream of round k from the ring and s_d gathered from the
+//          round's source buffers (engine.cpp:237); one cluster barrier;
+//   store: one TMA bulk copy of the final slab to the frame.
+// The frame is read from and written to HBM once, with no kernel boundary
+// between rounds (reference: the r-round loop of engine.cpp:207-250).
+#ifndef CL_THREADS
+#define CL_THREADS 512
+#endif
+constexpr uint32_t kClThreads = CL_THREADS;
+constexpr int kClBatch = 4;  // gather pieces per thread with loads in flight together
+constexpr uint32_t kClMax = 16;  // CTAs per cluster (non-portable above 8)
+constexpr size_t kClSmemMax = 227 * 1024;
+
+struct ClusterArgs {
+  const uint8_t* src;  // plaintext (global)
+  uint8_t* dst;        // ciphertext (global; may alias src)
+  const uint8_t* ring;
+  uint64_t ring_bytes;
+  uint64_t pos;  // stream position of round 0 (round k: pos + k * region)
+  const int32_t* shift;
+  uint32_t side, n, rows, R, rounds;
+  uint32_t region, slab;  // slab = R * side * 3
+  uint32_t cks_off;       // shared-memory offset of the c_k table (after 2 slabs)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(kClThreads, 1)
+    k_encrypt_frame_cluster(const ClusterArgs a) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t q = cluster.block_rank();
+  const uint32_t tid = threadIdx.x, side = a.side, R = a.R;
+  const uint32_t al0 = q * R;
+  uint8_t* const buf0 = sm;
+  uint32_t* const cks = reinterpret_cast<uint32_t*>(sm + a.cks_off);  // R entries
+  uint32_t* const wsum = cks + ((R + 3u) & ~3u);                       // 64 words
+  uint32_t* const bseed = wsum + 64;                                   // 8 words
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(bseed + 8);
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // shift table and frame ready
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                 "r"(a.slab)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(buf0)),
+        "l"(a.src + uint64_t(q) * a.slab), "r"(a.slab), "r"(smem_u32(mbar))
+        : "memory");
+  }
+  for (uint32_t k = tid; k < R; k += kClThreads) {
+    uint32_t c = k + uint32_t(a.shift[al0 + k]);
+    cks[k] = c >= side ? c - side : c;
+  }
+  {  // wait for the slab (phase 0)
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(smem_u32(mbar))
+          : "memory");
+  }
+  cluster.sync();  // every slab is loaded before any CTA gathers from it
+
+  const uint32_t np = (R + 15u) >> 4;  // 16-pixel pieces of a run
+  const uint32_t nbl = R / a.rows;     // local bands
+  const uint32_t ngr = a.region / 48u; // 48-byte granules per band
+  uint32_t phase = 0;                  // block_xor_scan calls (alternating workspace)
+  for (uint32_t rk = 0; rk < a.rounds; ++rk) {
+    const uint8_t* S = sm + (rk & 1u) * a.slab;  // this round's source (every CTA)
+    uint8_t* Y = sm + ((rk & 1u) ^ 1u) * a.slab;  // local destination
+    // 1. Gather: piece (sr, p) = pixels k in [16p, 16p+16) of source row sr's
+    //    run, source columns o0 + k, o0 = (al0 - sr) mod side; pixel k goes to
+    //    local row k, column (o0 + c_k) mod side.
+    // The windows of up to kClBatch pieces of the thread are loaded (remote
+    // DSMEM, long latency) before any is used, then realigned and stored.
+    struct Piece {
+      uint32_t o0, k0, len, b0;
+      bool fast, live;
+      const uint8_t* rs;
+      uint32_t rowb;
+    };
+    auto piece_of = [&](uint32_t w) {
+      Piece pc;
+      pc.live = w < side * np;
+      const uint32_t sr = pc.live ? w / np : 0u, p = pc.live ? w - sr * np : 0u;
+      int oi = int(al0) - int(sr);
+      oi += oi < 0 ? int(side) : 0;
+      pc.o0 = uint32_t(oi);
+      pc.k0 = 16u * p;
+      pc.len = min(16u, R - pc.k0);
+      const uint32_t qs = sr / R;  // owner of source row sr
+      pc.rs = cluster.map_shared_rank(S, qs);
+      pc.rowb = (sr - qs * R) * side * 3u;
+      pc.fast = pc.live && pc.o0 + pc.k0 + pc.len <= side;
+      pc.b0 = pc.rowb + (pc.o0 + pc.k0) * 3u;
+      return pc;
+    };
+    const uint32_t npieces = side * np;
+    for (uint32_t w0 = 0; w0 < npieces; w0 += kClBatch * kClThreads) {
+      Piece pc[kClBatch];
+      uint4 V4[kClBatch][4];
+#pragma unroll
+      for (int b = 0; b < kClBatch; ++b) {
+        pc[b] = piece_of(w0 + uint32_t(b) * kClThreads + tid);
+        const uint4* win = reinterpret_cast<const uint4*>(pc[b].rs + (pc[b].b0 & ~15u));
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          V4[b][c] = (pc[b].fast && 16u * c < (pc[b].b0 & 15u) + 3u * pc[b].len)
+                         ? win[c] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int b = 0; b < kClBatch; ++b) {
+        const Piece& q = pc[b];
+        if (q.fast) {
+          uint32_t V[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            V[4 * c] = V4[b][c].x;
+            V[4 * c + 1] = V4[b][c].y;
+            V[4 * c + 2] = V4[b][c].z;
+            V[4 * c + 3] = V4[b][c].w;
+          }
+          uint32_t A[12];
+          realign12(V, q.b0 & 15u, A);
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            if (uint32_t(m) >= q.len) break;
+            const int j = (3 * m) >> 2, sh = ((3 * m) & 3) * 8;
+            const uint32_t pix = sh <= 8 ? (A[j] >> sh) : __funnelshift_r(A[j], A[j + 1], sh);
+            const uint32_t k = q.k0 + uint32_t(m);
+            uint32_t col = q.o0 + cks[k];
+            col -= col >= side ? side : 0u;
+            uint8_t* d = Y + (k * side + col) * 3u;
+            d[0] = uint8_t(pix);
+            d[1] = uint8_t(pix >> 8);
+            d[2] = uint8_t(pix >> 16);
+          }
+        } else if (q.live) {  // the run wraps past the row end: pixel by pixel
+          for (uint32_t m = 0; m < q.len; ++m) {
+            const uint32_t k = q.k0 + m;
+            uint32_t o = q.o0 + k;
+            o -= o >= side ? side : 0u;
+            const uint8_t* sp = q.rs + q.rowb + o * 3u;
+            uint32_t col = q.o0 + cks[k];
+            col -= col >= side ? side : 0u;
+            uint8_t* d = Y + (k * side + col) * 3u;
+            d[0] = sp[0];
+            d[1] = sp[1];
+            d[2] = sp[2];
+          }
+        }
+      }
+    }
+    // s_d of each local band: the post-confusion byte ((band+1) mod n + 1) *
+    // region - 1 = pixel (last row of the next band, column side-1), channel
+    // 2, gathered straight from this round's source buffers.
+    if (tid < nbl) {
+      const uint32_t band = al0 / a.rows + tid;
+      const uint32_t nb = band + 1 == a.n ? 0 : band + 1;
+      const uint32_t al = nb * a.rows + a.rows - 1;
+      int o = int(side - 1) - a.shift[al];
+      o += o < 0 ? int(side) : 0;
+      int sr = int(al) - o;
+      sr += sr < 0 ? int(side) : 0;
+      const uint32_t qs = uint32_t(sr) / R;
+      const uint8_t* rs = cluster.map_shared_rank(S, qs);
+      bseed[tid] = rs[((uint32_t(sr) - qs * R) * side + uint32_t(o)) * 3u + 2u];
+    }
+    __syncthreads();  // Y complete, seeds set
+    // 2. Diffusion of each local band, in place on Y (one granule of 48 bytes
+    //    per thread per super-tile, one CTA-wide XOR scan per super-tile).
+    uint64_t kbase = a.pos + uint64_t(rk) * a.region;
+    kbase %= a.ring_bytes;
+    // keystream granule g of local band lb (48-byte granules never straddle
+    // the ring end: positions and ring size are multiples of 48)
+    auto load_kw = [&](uint32_t lb, uint32_t g, uint4 (&kv)[3]) {
+      const uint8_t* ks = a.ring + uint64_t(al0 / a.rows + lb) * a.ring_bytes;
+      uint64_t kp = kbase + 48ull * g;
+      kp -= kp >= a.ring_bytes ? a.ring_bytes : 0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        kv[i] = g < ngr ? ld_stream(ks + kp + 16 * i) : make_uint4(0, 0, 0, 0);
+    };
+    uint4 kv[3];
+    load_kw(0, tid, kv);
+    for (uint32_t lb = 0; lb < nbl; ++lb) {
+      uint32_t carry = bseed[lb];
+      uint8_t* yb = Y + lb * a.region;
+      for (uint32_t st = 0; st * kClThreads < ngr; ++st) {
+        const uint32_t g = st * kClThreads + tid;
+        // next super-tile's keystream (or the next band's first) in flight
+        uint4 kn[3];
+        const bool last = (st + 1) * kClThreads >= ngr;
+        if (!last)
+          load_kw(lb, g + kClThreads, kn);
+        else if (lb + 1 < nbl)
+          load_kw(lb + 1, tid, kn);
+        uint32_t yv[12];
+        const uint32_t kw[12] = {kv[0].x, kv[0].y, kv[0].z, kv[0].w, kv[1].x, kv[1].y,
+                                 kv[1].z, kv[1].w, kv[2].x, kv[2].y, kv[2].z, kv[2].w};
+        if (g < ngr) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const uint4 v = reinterpret_cast<const uint4*>(yb + 48u * g)[i];
+            yv[4 * i] = v.x;
+            yv[4 * i + 1] = v.y;
+            yv[4 * i + 2] = v.z;
+            yv[4 * i + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 12; ++i) yv[i] = 0;
+        }
+        uint32_t res[12], E = 0;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const uint32_t t = t_prefix4(yv[i], kw[i]);
+          res[i] = t ^ E;
+          E ^= __byte_perm(t, 0, 0x3333);
+        }
+        uint32_t total;
+        const uint32_t excl = block_xor_scan(E & 0xFFu, wsum, phase++, total) ^ carry;
+        if (g < ngr) {
+          const uint32_t m = excl * 0x01010101u;
+          uint4* o4 = reinterpret_cast<uint4*>(yb + 48u * g);
+          o4[0] = make_uint4(res[0] ^ m, res[1] ^ m, res[2] ^ m, res[3] ^ m);
+          o4[1] = make_uint4(res[4] ^ m, res[5] ^ m, res[6] ^ m, res[7] ^ m);
+          o4[2] = make_uint4(res[8] ^ m, res[9] ^ m, res[10] ^ m, res[11] ^ m);
+        }
+        carry ^= total;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) kv[i] = kn[i];
+      }
+    }
+    cluster.sync();  // Y complete everywhere; every read of this round's S done
+  }
+  // 3. Store the final slab with one TMA bulk copy.
+  const uint8_t* fin = sm + (a.rounds & 1u) * a.slab;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                     a.dst + uint64_t(q) * a.slab),
+                 "r"(smem_u32(fin)), "r"(a.slab)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic forward round for geometries whose band chunks do not fit one
 // cluster's shared memory: gather -> chunk aggregates -> band prefixes ->
 // chunk scans, through global scratch.
@@ -1377,6 +1651,9 @@ void configure_cipher_kernels() {
   cudaFuncSetAttribute(k_encrypt_round_slots, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_decrypt_round_slots, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(kSlotSmemMax));
+  cudaFuncSetAttribute(k_encrypt_frame_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(kClSmemMax));
+  cudaFuncSetAttribute(k_encrypt_frame_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   // K3t: ~26 KB tiles, 8 per SM need the whole carveout as shared memory
   cudaFuncSetAttribute(k_decrypt_round_tiles, cudaFuncAttributePreferredSharedMemoryCarveout,
                        int(cudaSharedmemCarveoutMaxShared));
@@ -1445,6 +1722,54 @@ EncPlan plan_encrypt(const Geom& g) {
   }
   if (!std::getenv("CVE_B200_NO_SLOTS")) plan_slots(g, out);  // experiments only
   return out;
+}
+
+// K6 plan: the largest cluster (<= 16 CTAs) whose CTAs own whole bands
+// (R = side / CL rows, R % rows == 0) and fit two packed slabs of R rows plus
+// the c_k table in shared memory.  0: the frame does not fit one cluster.
+uint32_t plan_cluster(const Geom& g, size_t& smem) {
+  if (g.side % 16 || std::getenv("CVE_B200_NO_CLUSTER")) return 0;  // experiments only
+  for (uint32_t cl = kClMax; cl >= 1; --cl) {
+    if (g.side % cl) continue;
+    const uint32_t R = g.side / cl;
+    if (R % g.rows) continue;
+    const size_t slab = size_t(R) * g.side * 3;
+    const size_t need = 2 * slab + 4 * ((R + 3) & ~3u) + 4 * 64 + 4 * 8 + 16;
+    if (need > kClSmemMax || R / g.rows > 8) continue;
+    smem = need;
+    return cl;
+  }
+  return 0;
+}
+
+bool launch_encrypt_frame(const Geom& g, uint8_t* buf, KsWindow ks, const int32_t* shift,
+                          uint32_t rounds, cudaStream_t s, uint64_t* launches) {
+  size_t smem = 0;
+  const uint32_t cl = plan_cluster(g, smem);
+  const bool aligned = ks.pos % 48 == 0 && ks.ring_bytes % 48 == 0 && g.region % 48 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring)) % 16 == 0);
+  if (!cl || !aligned) return false;
+  const uint32_t R = g.side / cl;
+  ClusterArgs a{buf, buf, ks.ring, ks.ring_bytes, ks.pos, shift, g.side, g.n, g.rows, R,
+                rounds, uint32_t(g.region), R * g.side * 3, 2 * R * g.side * 3};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kClThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 1 : 2;  // experiments only
+  cudaLaunchKernelEx(&cfg, k_encrypt_frame_cluster, a);
+  check_launch("encrypt_frame_cluster");
+  ++*launches;
+  return true;
 }
 
 void launch_encrypt_round(const EncPlan& plan, const Geom& g,

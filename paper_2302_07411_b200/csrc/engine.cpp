@@ -369,6 +369,7 @@ uint64_t Generator::replays() {
 
 namespace {
 std::atomic<int> g_streams{0};  // 0: not yet read from the environment
+std::atomic<int> g_fusion{-1};  // -1: not yet read from the environment
 }
 
 NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -386,6 +387,23 @@ int streams_per_handle() {
     v = (e && std::atoi(e) == 1) ? 1 : 2;
     int expected = 0;
     if (!g_streams.compare_exchange_strong(expected, v)) v = expected;
+  }
+  return v;
+}
+
+void set_round_fusion(int mode) {
+  if (mode < 0 || mode > 1) raise(Errc::invalid_argument, "round fusion mode must be 0 or 1");
+  g_fusion.store(mode);
+}
+
+int round_fusion() {
+  int v = g_fusion.load();
+  if (v < 0) {
+    const char* e = std::getenv("CVE_B200_ROUND_FUSION");
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 1) v = 0;
+    int expected = -1;
+    if (!g_fusion.compare_exchange_strong(expected, v)) v = expected;
   }
   return v;
 }
@@ -593,6 +611,7 @@ Engine::Engine(const Key& key, uint32_t workers, uint32_t rounds,
     if (v) gen_chunk_cap_ = v;
   }
   one_stream_ = streams_per_handle() == 1;
+  fuse_rounds_ = round_fusion() == 1;
   try {
     for (int d : devices) configure_kernels_once(d);
     DeviceScope scope(dev_);  // the caller's device is restored on return
@@ -886,8 +905,16 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
   timed_begin(c.events, c.s_work, false, false);
   launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
   ++st_.kernel_launches;
-  const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
   const uint64_t base = ks.pos;
+  if (!decrypt && fuse_rounds_ &&
+      launch_encrypt_frame(g, buf, ks, c.d_shift, r_, c.s_work, &st_.kernel_launches)) {
+    timed_end(c.s_work);  // K6: every round in one cluster kernel
+    cudaEvent_t done = c.events.get();
+    ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
+    ++st_.frames;
+    return done;
+  }
+  const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
   const uint8_t* src = buf;
   for (uint32_t step = 0; step < r_; ++step) {
     const uint32_t k = decrypt ? r_ - 1 - step : step;

@@ -73,6 +73,17 @@ struct EngineStats {
 void set_streams_per_handle(int n);
 int streams_per_handle();
 
+// Round fusion (process-wide, read when a handle is created): whether the
+// forward rounds of frames that fit one thread-block cluster (<= ~768^2) run
+// as ONE cluster kernel (K6: the frame is read and written once, every round
+// on-chip in distributed shared memory, 8-16 SMs per frame) or as one
+// grid-wide kernel per round (K2s, all SMs).  0 (default) = one kernel per
+// round: measured faster per frame (C1 37 vs 112-120 us) and in aggregate for
+// 16-32 concurrent clips (C1 4.4k vs 4.2k, C3 6.5k vs 5.8k frames/s);
+// 1 = K6 wherever the frame fits.  Initial value: $CVE_B200_ROUND_FUSION.
+void set_round_fusion(int mode);
+int round_fusion();
+
 // Runs on `dev` until the scope ends, then restores the caller's device.  If
 // no device can be queried (no driver), does nothing and lets the first CUDA
 // call report INTERNAL, after the host-side checks ran (reference order).
@@ -277,6 +288,7 @@ class Engine {
   uint64_t launches_ = 0;  // generator launches (slot = launches_ & 1)
   uint64_t gen_chunk_cap_ = 0;  // optional cap on iterations per generator launch
   bool one_stream_ = false;     // generator shares the rounds stream
+  bool fuse_rounds_ = false;    // K6 cluster kernel for frames that fit
   Generator gen_;
   uint32_t bpi_ = 6;  // keystream bytes per generator iteration (6 PLCM, 12 LASM)
 

@@ -127,6 +127,12 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
                           const int32_t* shift, uint8_t* scratch,
                           cudaStream_t s, uint64_t* launches);
 
+// K6: all `rounds` forward rounds of one frame (in place in `buf`) in one
+// thread-block cluster, when the frame fits one (side % 16 == 0, up to
+// ~768^2); false: not applicable, nothing launched.
+bool launch_encrypt_frame(const Geom& g, uint8_t* buf, KsWindow ks, const int32_t* shift,
+                          uint32_t rounds, cudaStream_t s, uint64_t* launches);
+
 // One inverse round (elementwise inverse diffusion fused with the inverse
 // confusion gather).
 void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,

@@ -388,6 +388,52 @@ def test_sharded_clip_vs_reference(name, devices, mode, frames):
                     frames=frames) == (frames or g["frames"])
 
 
+@pytest.mark.parametrize("side,n", [(16, 1), (16, 2), (48, 3), (64, 4), (96, 8), (128, 16),
+                                    (160, 5), (192, 12), (256, 8), (480, 8), (512, 8)])
+def test_round_fusion_vs_oracle(side, n):
+    # K6 (every forward round of a frame in one thread-block cluster) against
+    # the oracle on consecutive frames of a handle, PLCM and LASM keys, r in
+    # {1, 2, 5} (the final buffer's parity changes with r), then a round trip
+    # through a decrypt handle.
+    cve.set_round_fusion(1)
+    try:
+        for key, r in ((synth.det_key(70 + side + n), 5), (synth.det_key_lasm(71 + side), 2),
+                       (synth.det_key(72 + n), 1)):
+            frames = rand_frames(side, 3, side * 7 + n + r)
+            want = frames.copy()
+            o = Oracle(key, n, r)
+            for t in range(3):
+                assert o.encrypt(want[t]) == 0
+            got = frames.copy()
+            h = cve.Cipher(key, n, r)
+            for t in range(3):
+                h.encrypt_frame(got[t])
+            assert np.array_equal(got, want), (side, n, r)
+            cve.Cipher(key, n, r).decrypt_frames(got)
+            assert np.array_equal(got, frames)
+    finally:
+        cve.set_round_fusion(0)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_round_fusion_clips_vs_reference(name):
+    # The fused path on the config clips: every frame (C1/C2) or a 96-frame
+    # prefix (C3) against the reference's digests, plus the round trip.
+    from _clips import run_clip
+    g = load("clips.json")[name] if name == "C3" else None
+    if g is None:
+        fr = load("frames.json")[name]
+        g = {"key": fr["key"], "workers": fr["workers"], "rounds": fr["rounds"],
+             "frames": len(fr["cipher_sha256"]), "cipher_sha256": fr["cipher_sha256"],
+             "plain_sha256": fr["plain_sha256"]}
+    cve.set_round_fusion(1)
+    try:
+        n = run_clip(name, g, g["plain_sha256"], frames=96 if name == "C3" else 0)
+    finally:
+        cve.set_round_fusion(0)
+    assert n == (96 if name == "C3" else g["frames"])
+
+
 def test_sharded_per_frame_calls_and_lasm_vs_oracle():
     # Per-frame drop-in calls on a sharded handle are dealt round-robin over
     # the shards; sides change between calls; a LASM key shards the same way.

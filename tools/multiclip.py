@@ -1,19 +1,22 @@
-"""M independent C4 clips on one GPU through the device-resident API, each
-on its own stream: aggregate frames/s.  Tool (bench.py reports a labelled
-multi-clip line from the same code)."""
+"""M independent clips (config $CONFIG, default C4) on one GPU through the
+device-resident API, each on its own stream, one hardware queue per handle
+(cve_set_streams_per_handle(1)): aggregate frames/s.  Tool (bench.py reports
+a labelled multi-clip line from the same code)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2302_07411_b200 as cve
 from workloads import synth
 
-name = "C4"; c = synth.CONFIGS[name]; side = synth.config_side(name); n = c["workers"]
+name = os.environ.get("CONFIG", "C4"); c = synth.CONFIGS[name]; side = synth.config_side(name); n = c["workers"]
 F = 8
 pool = np.stack([synth.config_frame(name, 2 + t) for t in range(F)])
 for M in [int(a) for a in sys.argv[1:]] or [1, 4, 16, 32, 64]:
     bufs = [torch.from_numpy(pool).cuda() for _ in range(M)]
     streams = [torch.cuda.Stream() for _ in range(M)]
+    cve.set_streams_per_handle(1)
     hs = [cve.Cipher(synth.det_key(500 + k), n, 5) for k in range(M)]
+    cve.set_streams_per_handle(2)
     for h, b, s in zip(hs, bufs, streams):   # warm-up step
         h.encrypt_frames_device(b.data_ptr(), side, F, s.cuda_stream)
     torch.cuda.synchronize()
