@@ -92,11 +92,33 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
   return f.d == 1 ? n : uint32_t(__umul64hi(uint64_t(n), f.m));
 }
 
-__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+// Keystream bytes are read exactly once per frame: they are loaded with an
+// L2 evict-first policy (KS_HINT, default on), so the stream of keystream
+// does not push the round's frame buffers (re-read by the next round) out
+// of L2.
+#ifndef KS_HINT
+#define KS_HINT 1
+#endif
+__device__ __forceinline__ uint64_t ks_policy() {
+  uint64_t pol = 0;
+#if KS_HINT
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p, uint64_t pol = ks_policy()) {
   uint4 v;
+#if KS_HINT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+#else
+  (void)pol;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
+#endif
   return v;
 }
 
@@ -432,6 +454,18 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool p
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "r"(pred ? 16 : 0)
                : "memory");
+}
+// keystream windows: with the evict-first L2 policy (see ld_stream)
+__device__ __forceinline__ void cp_async16_ks(uint32_t dst, const void* src, bool pred,
+                                              uint64_t pol) {
+#if KS_HINT
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+               "l"(src), "r"(pred ? 16 : 0), "l"(pol)
+               : "memory");
+#else
+  (void)pol;
+  cp_async16(dst, src, pred);
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -899,7 +933,10 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
       if (need && cps >= 4)
         CVE_CHECK(within(src, 16, a.ring + uint64_t(e.w & 0x7FFFFFFFu) * a.ring_bytes,
                          a.ring_bytes));
-      cp_async16(dst, src, need);
+      if (cps >= 4)
+        cp_async16_ks(dst, src, need, ks_policy());
+      else
+        cp_async16(dst, src, need);
     }
     cp_async_commit();
   };
@@ -1174,6 +1211,7 @@ __global__ void __launch_bounds__(kTileThreads)
       const uint8_t* ks = a.ring + uint64_t(r.band) * a.ring_bytes;
       const uint64_t kb = kp & ~uint64_t(15);
       const uint32_t nk = (uint32_t(kp & 15u) + 3u * r.len + 15u) >> 4;
+      const uint64_t kpol = ks_policy();
 #pragma unroll
       for (uint32_t c = 0; c < 4; ++c) {
         if (c < nc) CVE_CHECK(within(a.src + cb + 16u * c, 16, a.src, a.frame_bytes));
@@ -1184,7 +1222,7 @@ __global__ void __launch_bounds__(kTileThreads)
         uint64_t q = kb + 16u * c;
         q -= q >= a.ring_bytes ? a.ring_bytes : 0;
         if (c < nk) CVE_CHECK(within(ks + q, 16, ks, a.ring_bytes));
-        cp_async16(w + 16u * ((c + 4) ^ (tid & 7u)), ks + q, c < nk);
+        cp_async16_ks(w + 16u * ((c + 4) ^ (tid & 7u)), ks + q, c < nk, kpol);
       }
       cp_async_commit();
       cp_async_wait<0>();  // this thread's own copies: no CTA barrier needed
