@@ -513,7 +513,13 @@ def lasm_row(stream, have_ref: bool) -> dict:
         row["few_subframes"] = {"workload": "LASM key, C1 geometry (480^2, n=8), 10 frames "
                                             "through the host API after 2",
                                 "value": ours1, "reference": ref1, "unit": "frames/s",
-                                "identical": bool(np.array_equal(a, b))}
+                                "identical": bool(np.array_equal(a, b)),
+                                "crossover": "a LASM clip is 2n sequential glibc-sin orbits at "
+                                             "~256 ns per iteration on the GPU: the GPU is ahead "
+                                             "of the reference's host threads from n >= 32 "
+                                             "subframes (C3 n=32: 167 vs 122 frames/s, C4 n=64: "
+                                             "54 vs 24); at n = 8-16 (C1, C2) the host cores "
+                                             "are faster (tools/lasm_small_probe.py, DESIGN §10)"}
     return row
 
 
@@ -843,12 +849,29 @@ def run_b200(args) -> None:
     alg_per_launch = alg_bytes * launch_iters / iters_per_frame
     chain_gbs = (alg_per_launch / (float(np.mean(chain_times)) / 1e3) / 1e9
                  if len(chain_times) else None)
-    traffic_per_launch = None
-    try:  # DRAM bytes of the chain kernel from the committed ncu --set full capture
+    traffic_per_launch = ckpt_per_launch = None
+    frame_traffic = None
+    try:  # DRAM bytes per launch from the committed ncu --set full captures
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh)["k_prbg_chain"]
-        traffic_per_launch = tr["dram_bytes"] / tr["iterations"] * launch_iters
-    except (OSError, KeyError, ValueError, ZeroDivisionError):
+            tr = json.load(fh)
+        ch = tr["k_prbg_chain"]
+        traffic_per_launch = ch["dram_bytes"] / ch["iterations"] * launch_iters
+        ckpt_per_launch = ch["checkpoint_bytes_written"] / ch["iterations"] * launch_iters
+        # per-frame device DRAM traffic, cold-cache upper bound: the sum of
+        # every kernel's per-launch DRAM bytes (ncu replays each launch with a
+        # flushed L2, so reuse of the frame buffers across rounds is not seen)
+        ver = tr["k_prbg_verify_emit"]
+        rnd = tr["k_encrypt_round_slots"]["dram_bytes"] if side == 1920 else None
+        if rnd is not None:
+            per_frame = (ch["dram_bytes"] + ver["dram_bytes"]) / ch["iterations"] * iters_per_frame \
+                + synth.ROUNDS * rnd
+            frame_traffic = {"device_dram_bytes": per_frame, "algorithmic_bytes": alg_bytes,
+                             "ratio": per_frame / alg_bytes,
+                             "note": "cold-cache upper bound from profiles/traffic.json "
+                                     "(chain + verify per frame's iterations + 5 rounds); "
+                                     "keystream traffic (5F per frame) is implementation "
+                                     "overhead by SURVEY 8(d) and is included here"}
+    except (OSError, KeyError, ValueError, ZeroDivisionError, TypeError):
         pass
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s",
@@ -870,6 +893,12 @@ def run_b200(args) -> None:
             "achieved": chain_gbs, "peak": hbm, "unit": "GB/s",
             "frac": chain_gbs / hbm if chain_gbs else None, "peak_source": hbm_src,
             "traffic": traffic_per_launch,
+            "traffic_note": "ncu dram__bytes_read+write of one k_prbg_chain launch (cold), per "
+                            "launch of this run; the chain writes one 8-byte checkpoint per lane "
+                            "per 8 iterations (checkpoint_bytes_per_launch), which the verifier "
+                            "reads back from L2",
+            "checkpoint_bytes_per_launch": ckpt_per_launch,
+            "frame_traffic": frame_traffic,
             "algorithmic_bytes_per_launch": alg_per_launch,
             "baseline_roofline_us_per_frame": baseline_roofline(side, hbm),
             "note": "BASELINE.json roofline: 2*side^2*3 B per frame (SURVEY 8(d)) at peak "
