@@ -1424,6 +1424,8 @@ __global__ void __launch_bounds__(kClThreads, 1)
       for (int b = 0; b < kClBatch; ++b) {
         pc[b] = piece_of(w0 + uint32_t(b) * kClThreads + tid);
         const uint4* win = reinterpret_cast<const uint4*>(pc[b].rs + (pc[b].b0 & ~15u));
+        CVE_CHECK(!pc[b].fast ||
+                  (pc[b].b0 & ~15u) + 16u * (((pc[b].b0 & 15u) + 3u * pc[b].len + 15u) / 16u) <= a.slab);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           V4[b][c] = (pc[b].fast && 16u * c < (pc[b].b0 & 15u) + 3u * pc[b].len)
@@ -1452,6 +1454,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             uint32_t col = q.o0 + cks[k];
             col -= col >= side ? side : 0u;
             uint8_t* d = Y + (k * side + col) * 3u;
+            CVE_CHECK(k < R && col < side);
             d[0] = uint8_t(pix);
             d[1] = uint8_t(pix >> 8);
             d[2] = uint8_t(pix >> 16);
@@ -1462,6 +1465,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             uint32_t o = q.o0 + k;
             o -= o >= side ? side : 0u;
             const uint8_t* sp = q.rs + q.rowb + o * 3u;
+            CVE_CHECK(k < R && q.rowb + o * 3u + 3u <= a.slab);
             uint32_t col = q.o0 + cks[k];
             col -= col >= side ? side : 0u;
             uint8_t* d = Y + (k * side + col) * 3u;
@@ -1498,6 +1502,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
       const uint8_t* ks = a.ring + uint64_t(al0 / a.rows + lb) * a.ring_bytes;
       uint64_t kp = kbase + 48ull * g;
       kp -= kp >= a.ring_bytes ? a.ring_bytes : 0;
+      if (g < ngr) CVE_CHECK(within(ks + kp, 48, ks, a.ring_bytes));
 #pragma unroll
       for (int i = 0; i < 3; ++i)
         kv[i] = g < ngr ? ld_stream(ks + kp + 16 * i) : make_uint4(0, 0, 0, 0);
