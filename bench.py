@@ -908,10 +908,10 @@ def run_b200(args) -> None:
             "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
             "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
             "cycles_per_iteration": ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3,
-            # ptxas stall counts of the unrolled loop body (SASS control
-            # bits, tools/iter_cycles.py): 326 cycles per 8 iterations
-            "static_schedule_cycles": 40.75,
-            "frac_of_static_schedule": 40.75 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
+            # ptxas stall counts of the unrolled 32-iteration loop body (SASS
+            # control bits, tools/iter_cycles.py): 7 x 41 + 38 per 8 steps
+            "static_schedule_cycles": 40.6,
+            "frac_of_static_schedule": 40.6 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
             "launches": int(len(chain_times)),
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,
