@@ -1,6 +1,9 @@
 """Multi-rank host logic of bench.py on CPU (gloo, world size 2): the
-barrier, the max-over-ranks reduction of timings, and per-rank clip keys
-(one independent clip per rank -- "replicas only")."""
+barrier, the max-over-ranks reduction of timings, per-rank clip keys of the
+labelled multi-clip line, and the reference arm's contract (same config as
+the B200 arm, only the reference's own library mapped).  The headline at
+N > 1 is ONE clip sharded over the GPUs; its device path is
+covered by the sharded-handle GPU tests."""
 import os
 import socket
 import sys
@@ -58,3 +61,31 @@ def test_reference_arm_other_ranks_exit_quietly(monkeypatch, capsys):
     args = type("A", (), dict(config="C4", gpus=2, steps=1, warmup=0))()
     bench.run_reference(args)
     assert capsys.readouterr().out == ""
+
+
+def test_reference_arm_config_matches_b200_arm():
+    # both arms build the SAME config dict (frames per step rounded to the
+    # GPU count, the L2 note, the sharding description)
+    import bench
+    for gpus in (1, 2, 8):
+        args = type("A", (), dict(config="C4", gpus=gpus, frames=24, shard_devices=""))()
+        F = bench.frames_per_step(args)
+        assert F % gpus == 0 and F >= 24
+        a = bench.config_dict("C4", F, gpus)
+        b = bench.config_dict("C4", bench.frames_per_step(args), gpus)
+        assert a == b and a["frames_per_step"] == F
+        assert ("sharded" in a["parallelism"]) == (gpus > 1)
+    assert bench.scaling_of(1) == bench.scaling_of(8) == "strong"
+
+
+def test_harness_import_does_not_map_the_product_library():
+    # the reference arm imports workloads.synth and tests/_oracle: neither may
+    # load libcve_b200.so (the driver checks which .so files the arm mapped)
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = [%r, %r]; import bench; from workloads import synth; "
+            "import _oracle; print(bench.mapped_libraries())" % (root, os.path.join(root, "tests")))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr
+    assert "libcve_b200" not in out.stdout, out.stdout
