@@ -361,6 +361,17 @@ CVE_B200_API cve_status cve_cipher_get_stats(cve_cipher* cipher,
 CVE_B200_API cve_status cve_keystream_generate(const double lanes[4],
                                                uint8_t* out, size_t len);
 
+/* Diagnostics: cve_keystream_generate with at most `launch_iters` generator
+ * iterations per launch (0: no cap; the generator is pipelined as in a
+ * cipher handle: the chain of launch L+1 runs while launch L is verified)
+ * and, if guard_replays is not NULL, the number of worker launches the
+ * exact fix-up recomputed (guard-set hits on the speculative chain,
+ * chaos.cpp:18-24, and the launch after each, whose start it repairs).
+ * Output is identical to cve_keystream_generate. */
+CVE_B200_API cve_status cve_keystream_generate_ex(const double lanes[4], uint8_t* out,
+                                                  size_t len, uint32_t launch_iters,
+                                                  uint64_t* guard_replays);
+
 /* LASM counterpart (row f2): lanes {x0_a, y0_a, mu_a, x0_b, y0_b, mu_b}, the
  * reference's Prbg(LasmParams, LasmParams).take(len) (chaos.cpp:93-107,
  * 119-153: 12 bytes per iteration).  Out-of-domain lanes -> BAD_KEY. */

@@ -463,6 +463,17 @@ cve_status cve_keystream_generate(const double lanes[4], uint8_t* out,
   });
 }
 
+cve_status cve_keystream_generate_ex(const double lanes[4], uint8_t* out, size_t len,
+                                     uint32_t launch_iters, uint64_t* guard_replays) {
+  return guarded([&] {
+    require(lanes != nullptr, "lanes is null");
+    require(out != nullptr || len == 0, "out is null");
+    DeviceScope scope(current_device());
+    cveb::standalone_stream(cveb::Lane{lanes[0], lanes[1]}, cveb::Lane{lanes[2], lanes[3]}, out,
+                            len, launch_iters, guard_replays);
+  });
+}
+
 cve_status cve_keystream_generate_lasm(const double lanes[6], uint8_t* out,
                                        size_t len) {
   return guarded([&] {

@@ -188,6 +188,7 @@ void free_prbg(PrbgBuffers& b, cudaStream_t s = nullptr) {
   }
   dfree(b.bad, s);
   dfree(b.replays, s);
+  dfree(b.resync, s);
   b = PrbgBuffers{};
 }
 
@@ -211,8 +212,10 @@ PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
     b.max_iters = orbit_iters;
     dmalloc(&b.bad, (nlanes / 2) * sizeof(unsigned), "cudaMalloc flags");
     dmalloc(&b.replays, sizeof(unsigned long long), "cudaMalloc");
+    dmalloc(&b.resync, nlanes * sizeof(unsigned long long), "cudaMalloc");
     ck(cudaMemsetAsync(b.bad, 0, (nlanes / 2) * sizeof(unsigned), s), "memset");
     ck(cudaMemsetAsync(b.replays, 0, sizeof(unsigned long long), s), "memset");
+    ck(cudaMemsetAsync(b.resync, 0xFF, nlanes * sizeof(unsigned long long), s), "memset");
   } catch (...) {
     free_prbg(b);
     throw;
@@ -267,6 +270,8 @@ void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaSt
                      uint32_t orbit_iters) {
   release();
   kind_ = kind;
+  chains_ = 0;
+  last_iters_ = 0;
   nl_ = uint32_t(2 * lanes.size());
   if (kind_ == MapKind::Plcm) {
     std::vector<LaneConst> lc(nl_);
@@ -345,16 +350,20 @@ void Generator::resize(uint32_t iters) {
 
 void Generator::chain(int slot, uint32_t iters, cudaStream_t s) {
   if (kind_ == MapKind::Plcm)
-    launch_prbg_chain(pb_, slot, d_lc_, iters, nl_, s);
+    launch_prbg_chain(pb_, slot, d_lc_, iters, nl_, chains_, last_iters_, s);
   else
     launch_lasm_chain(lb_, slot, iters, nl_, s);
   ck(cudaGetLastError(), "generator chain launch");
+  launch_of_[slot & 1] = chains_;
+  ++chains_;
+  last_iters_ = iters;
 }
 
 void Generator::emit(int slot, uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
                      uint32_t iters, cudaStream_t s) {
   if (kind_ == MapKind::Plcm)
-    launch_prbg_verify(pb_, slot, d_lc_, ring, ring_bytes, it0, iters, nl_, s);
+    launch_prbg_verify(pb_, slot, d_lc_, ring, ring_bytes, it0, iters, nl_, launch_of_[slot & 1],
+                       s);
   else
     launch_lasm_emit(lb_, slot, ring, ring_bytes, it0, iters, nl_, s);
   ck(cudaGetLastError(), "generator emit launch");
@@ -1192,36 +1201,58 @@ std::vector<float> Engine::take_prbg_times() {
 
 namespace {
 // The reference's Prbg{lane_a, lane_b}.take(len) (chaos.cpp:79-107, 143-153)
-// on the GPU: explicit lanes, one worker.
-void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len) {
-  cudaStream_t s = nullptr;
+// on the GPU: explicit lanes, one worker.  The generator is pipelined like an
+// Engine's: chain L+1 runs on one stream while launch L is verified and
+// emitted on another.  launch_iters (0: as large as the orbit budget allows)
+// caps the iterations per generator launch.
+void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len,
+                uint32_t launch_iters, uint64_t* replays) {
+  cudaStream_t sg = nullptr, sw = nullptr;
+  cudaEvent_t chain_done[2] = {nullptr, nullptr}, ver_done[2] = {nullptr, nullptr};
   uint8_t* d_out = nullptr;
   Generator gen;
   auto cleanup = [&] {
-    if (s) cudaStreamSynchronize(s);
+    for (cudaStream_t s : {sg, sw})
+      if (s) cudaStreamSynchronize(s);
     gen.release();
     dfree(d_out);
-    stream_put(s);
+    for (auto* evs : {chain_done, ver_done})
+      for (int k = 0; k < 2; ++k)
+        if (evs[k]) cudaEventDestroy(evs[k]);
+    stream_put(sg);
+    stream_put(sw);
   };
   try {
     int dev = 0;
     ck(cudaGetDevice(&dev), "cudaGetDevice");
     configure_kernels_once(dev);
-    s = stream_get();
-    gen.init({w}, kind, s, 0);
+    sg = stream_get();
+    sw = stream_get();
+    for (auto* evs : {chain_done, ver_done})
+      for (int k = 0; k < 2; ++k)
+        ck(cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming), "cudaEventCreate");
+    gen.init({w}, kind, sg, 0);
     const uint32_t bpi = gen.bytes_per_iter();
     const uint64_t iters = round_up((len + bpi - 1) / bpi, 8);
-    gen.resize(uint32_t(std::min<uint64_t>(gen.orbit_cap_iters(), iters)));
+    uint64_t chunk = std::min<uint64_t>(gen.orbit_cap_iters(), iters);
+    if (launch_iters) chunk = std::min<uint64_t>(chunk, std::max<uint32_t>(8, launch_iters / 8 * 8));
+    gen.resize(uint32_t(chunk));
     const uint64_t ring = iters * bpi;  // multiple of 48
     dmalloc(&d_out, ring, "cudaMalloc");
-    int slot = 0;
-    for (uint64_t it = 0; it < iters; it += gen.max_iters(), slot ^= 1) {
-      const uint32_t n = uint32_t(std::min<uint64_t>(gen.max_iters(), iters - it));
-      gen.chain(slot, n, s);
-      gen.emit(slot, d_out, ring, it, n, s);
+    uint64_t L = 0;
+    for (uint64_t it = 0; it < iters; it += chunk, ++L) {
+      const int slot = int(L & 1);
+      const uint32_t n = uint32_t(std::min<uint64_t>(chunk, iters - it));
+      if (L >= 2) ck(cudaStreamWaitEvent(sg, ver_done[slot], 0), "wait slot");
+      gen.chain(slot, n, sg);
+      ck(cudaEventRecord(chain_done[slot], sg), "record");
+      ck(cudaStreamWaitEvent(sw, chain_done[slot], 0), "wait chain");
+      gen.emit(slot, d_out, ring, it, n, sw);
+      ck(cudaEventRecord(ver_done[slot], sw), "record");
     }
-    ck(cudaStreamSynchronize(s), "keystream");
+    ck(cudaStreamSynchronize(sw), "keystream");
     ck(cudaMemcpy(out, d_out, len, cudaMemcpyDeviceToHost), "download");
+    if (replays) *replays = gen.replays();
   } catch (...) {
     cleanup();
     throw;
@@ -1230,14 +1261,16 @@ void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len) {
 }
 }  // namespace
 
-void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len) {
+void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len,
+                       uint32_t launch_iters, uint64_t* replays) {
+  if (replays) *replays = 0;
   if (len == 0) return;
   HostPrbg validate(a, b);  // domain checks (bad_key), cheap
   (void)validate;
   WorkerLanes w;
   w.a = a;
   w.b = b;
-  standalone(w, MapKind::Plcm, out, len);
+  standalone(w, MapKind::Plcm, out, len, launch_iters, replays);
 }
 
 void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len) {
@@ -1247,7 +1280,7 @@ void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_
   WorkerLanes w;
   w.la = a;
   w.lb = b;
-  standalone(w, MapKind::Lasm, out, len);
+  standalone(w, MapKind::Lasm, out, len, 0, nullptr);
 }
 
 KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind,

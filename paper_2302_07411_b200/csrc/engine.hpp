@@ -187,6 +187,9 @@ class Generator {
  private:
   MapKind kind_ = MapKind::Plcm;
   uint32_t nl_ = 0;
+  uint64_t chains_ = 0;          // chain launches so far (resync bookkeeping)
+  uint32_t last_iters_ = 0;      // iterations of the latest chain launch
+  uint64_t launch_of_[2] = {0, 0};  // launch index that wrote orbit slot k
   PrbgBuffers pb_{};
   LaneConst* d_lc_ = nullptr;
   LasmBuffers lb_{};
@@ -311,7 +314,10 @@ class Engine {
 };
 
 // Reference Prbg with explicit lanes, generated on the current device.
-void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len);
+// launch_iters: cap on iterations per generator launch (0: none); replays
+// (may be null): workers the fix-up recomputed exactly.
+void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len,
+                       uint32_t launch_iters = 0, uint64_t* replays = nullptr);
 void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len);
 
 // Fresh generators for a set of workers (reference WorkerParams::make_prbg,

@@ -49,13 +49,21 @@ struct PrbgBuffers {
   double* verified_end;   // nlanes: verified end point of the last launch
   unsigned* bad;          // nworkers: verification failure flags
   unsigned long long* replays;  // workers recomputed exactly (cumulative)
+  unsigned long long* resync;   // nlanes: index of the launch last replayed (~0: none)
   uint32_t max_iters;           // per launch, multiple of 8
 };
 
 // (1) Chain: advances every lane by `iters` (multiple of 8, <= max_iters)
 // iterations, group checkpoints into orbit[slot], start point into ckpt[slot].
+// `launch` counts the generator's chain launches (0, 1, ...); `prev_iters`
+// is the previous launch's iteration count.  A lane whose launch R was
+// replayed exactly by the fix-up restarts from the verified end point in
+// launch R + 1 (same-stream pipelines) or R + 2 (the chain of R + 1 already
+// ran: its iterations are recomputed first), instead of continuing from its
+// diverged speculative state forever.
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
-                       uint32_t iters, uint32_t nlanes, cudaStream_t s);
+                       uint32_t iters, uint32_t nlanes, uint64_t launch, uint32_t prev_iters,
+                       cudaStream_t s);
 // (2) Verify every step of launch `slot` against the reference's exact step
 // (and that it starts where the previous launch verifiably ended), emit the
 // keystream bytes of iterations [it0, it0+iters) into the ring at stream
@@ -63,7 +71,7 @@ void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
 // failed worker exactly from the verified end point.
 void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
                         uint8_t* ring, uint64_t ring_bytes, uint64_t it0,
-                        uint32_t iters, uint32_t nlanes, cudaStream_t s);
+                        uint32_t iters, uint32_t nlanes, uint64_t launch, cudaStream_t s);
 
 // LASM generator (lasm.cu, row f2).  Lane layout as above; per lane the
 // chain position (x, y) and mu.  Orbit values are lane-major:

@@ -70,3 +70,25 @@ def test_guard_hits_in_both_lanes_across_launches():
     n = 6 * 2_500_000
     got = cve.keystream_generate([xa, pa, xb, pb], n)
     assert np.array_equal(got, plcm_stream(xa, pa, xb, pb, n))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,at,s", [("half", 30, 3), ("p", 9, 3), ("p", 7, 2)])
+def test_guard_hit_resync_limits_replays(kind, at, s):
+    # After an exact replay of launch R the chain restarts from the verified
+    # end point (launch R+1 in a same-stream pipeline, R+2 here, where chain
+    # R+1 already ran from the diverged state): a single guard hit costs a
+    # couple of replayed launches, not every later one.  32 launches of 8,192
+    # iterations, against the oracle byte for byte.  p = 1/4 lanes re-hit the
+    # guard every 25 iterations, so there every launch is replayed.
+    import paper_2302_07411_b200 as cve
+    x0, p = g.seed(kind, at, s)
+    n = 6 * 8192 * 32
+    for lanes in ([x0, p, *OTHER], [*OTHER, x0, p]):
+        got, rep = cve.keystream_generate_ex(lanes, n, launch_iters=8192)
+        assert np.array_equal(got, plcm_stream(*lanes, n)), lanes
+        hits = g.stream_hits(x0, p, 8192 * 32)
+        if len(hits) == 1:
+            assert 1 <= rep <= 3, rep
+        else:
+            assert rep >= 30, rep
