@@ -367,10 +367,14 @@ CVE_B200_API cve_status cve_keystream_generate(const double lanes[4],
  * and, if guard_replays is not NULL, the number of worker launches the
  * exact fix-up recomputed (guard-set hits on the speculative chain,
  * chaos.cpp:18-24, and the launch after each, whose start it repairs).
- * Output is identical to cve_keystream_generate. */
+ * flags: CVE_KEYSTREAM_DENSE_ORBIT selects the generator variant that
+ * handles created with one stream per handle use (the chain stores every
+ * orbit value; default: one checkpoint per 8 iterations).  Output is
+ * identical to cve_keystream_generate either way. */
+#define CVE_KEYSTREAM_DENSE_ORBIT 1u
 CVE_B200_API cve_status cve_keystream_generate_ex(const double lanes[4], uint8_t* out,
                                                   size_t len, uint32_t launch_iters,
-                                                  uint64_t* guard_replays);
+                                                  uint32_t flags, uint64_t* guard_replays);
 
 /* LASM counterpart (row f2): lanes {x0_a, y0_a, mu_a, x0_b, y0_b, mu_b}, the
  * reference's Prbg(LasmParams, LasmParams).take(len) (chaos.cpp:93-107,

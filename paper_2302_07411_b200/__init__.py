@@ -129,7 +129,7 @@ def _load() -> C.CDLL:
         "cve_keystream_generate": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
         "cve_keystream_generate_lasm": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t]),
         "cve_keystream_generate_ex": (C.c_int, [C.POINTER(C.c_double), vp, C.c_size_t,
-                                                C.c_uint32, C.POINTER(C.c_uint64)]),
+                                                C.c_uint32, C.c_uint32, C.POINTER(C.c_uint64)]),
         "cve_glibc_sin": (C.c_int, [vp, vp, C.c_size_t]),
         "cve_derive_worker_lanes": (C.c_int, [C.c_char_p, C.c_uint32,
                                               C.POINTER(C.c_double),
@@ -191,15 +191,16 @@ def keystream_generate(lanes, length: int) -> np.ndarray:
     return out
 
 
-def keystream_generate_ex(lanes, length: int, launch_iters: int = 0):
-    """keystream_generate with a cap on iterations per generator launch;
-    returns (bytes, guard_replays) -- the worker launches the exact fix-up
-    recomputed."""
+def keystream_generate_ex(lanes, length: int, launch_iters: int = 0, dense: bool = False):
+    """keystream_generate with a cap on iterations per generator launch and
+    the generator variant (dense: every orbit value stored, as for handles
+    with one stream per handle); returns (bytes, guard_replays) -- the worker
+    launches the exact fix-up recomputed."""
     lan = (C.c_double * 4)(*[float(v) for v in lanes])
     out = np.zeros(length, dtype=np.uint8)
     rep = C.c_uint64()
     _check(lib.cve_keystream_generate_ex(lan, out.ctypes.data, length, launch_iters,
-                                         C.byref(rep)))
+                                         1 if dense else 0, C.byref(rep)))
     return out, rep.value
 
 

@@ -464,13 +464,16 @@ cve_status cve_keystream_generate(const double lanes[4], uint8_t* out,
 }
 
 cve_status cve_keystream_generate_ex(const double lanes[4], uint8_t* out, size_t len,
-                                     uint32_t launch_iters, uint64_t* guard_replays) {
+                                     uint32_t launch_iters, uint32_t flags,
+                                     uint64_t* guard_replays) {
   return guarded([&] {
     require(lanes != nullptr, "lanes is null");
     require(out != nullptr || len == 0, "out is null");
+    require((flags & ~uint32_t(CVE_KEYSTREAM_DENSE_ORBIT)) == 0, "unknown flags");
     DeviceScope scope(current_device());
     cveb::standalone_stream(cveb::Lane{lanes[0], lanes[1]}, cveb::Lane{lanes[2], lanes[3]}, out,
-                            len, launch_iters, guard_replays);
+                            len, launch_iters, guard_replays,
+                            (flags & CVE_KEYSTREAM_DENSE_ORBIT) != 0);
   });
 }
 

@@ -198,16 +198,18 @@ void free_prbg(PrbgBuffers& b, cudaStream_t s = nullptr) {
 // may even return before its DMA lands).
 // orbit_iters = 0: no orbit buffers yet (an Engine sizes them from its ring,
 // resize_orbit); otherwise capacity for launches of orbit_iters iterations.
-PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters) {
+PrbgBuffers alloc_prbg(uint32_t nlanes, cudaStream_t s, uint32_t orbit_iters, bool dense) {
   PrbgBuffers b{};
+  b.dense = dense;
   try {
     const size_t lanes_bytes = nlanes * sizeof(double);
     dmalloc(&b.state, lanes_bytes, "cudaMalloc state");
     dmalloc(&b.verified_end, lanes_bytes, "cudaMalloc state");
     for (int k = 0; k < 2; ++k) {
       dmalloc(&b.ckpt[k], lanes_bytes, "cudaMalloc ckpt");
-      if (orbit_iters)  // one checkpoint per 8 iterations
-        dmalloc(&b.orbit[k], uint64_t(orbit_iters / 8) * lanes_bytes, "cudaMalloc orbit");
+      if (orbit_iters)  // one checkpoint per 8 iterations, or every value
+        dmalloc(&b.orbit[k], uint64_t(dense ? orbit_iters : orbit_iters / 8) * lanes_bytes,
+                "cudaMalloc orbit");
     }
     b.max_iters = orbit_iters;
     dmalloc(&b.bad, (nlanes / 2) * sizeof(unsigned), "cudaMalloc flags");
@@ -231,8 +233,9 @@ void resize_orbit(PrbgBuffers& b, uint32_t nlanes, uint32_t iters) {
     b.orbit[k] = nullptr;
   }
   b.max_iters = 0;
-  for (int k = 0; k < 2; ++k)  // one checkpoint per 8 iterations
-    dmalloc(&b.orbit[k], uint64_t(iters / 8) * nlanes * sizeof(double), "cudaMalloc orbit");
+  for (int k = 0; k < 2; ++k)  // one checkpoint per 8 iterations, or every value
+    dmalloc(&b.orbit[k], uint64_t(b.dense ? iters : iters / 8) * nlanes * sizeof(double),
+            "cudaMalloc orbit");
   b.max_iters = iters;
 }
 
@@ -267,7 +270,7 @@ void free_lasm(LasmBuffers& b, cudaStream_t s = nullptr) {
 }  // namespace
 
 void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaStream_t s,
-                     uint32_t orbit_iters) {
+                     uint32_t orbit_iters, bool dense) {
   release();
   kind_ = kind;
   chains_ = 0;
@@ -282,7 +285,7 @@ void Generator::init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaSt
       x0[2 * i] = lanes[i].a.x0;
       x0[2 * i + 1] = lanes[i].b.x0;
     }
-    pb_ = alloc_prbg(nl_, s, orbit_iters);
+    pb_ = alloc_prbg(nl_, s, orbit_iters, dense);
     dmalloc(&d_lc_, nl_ * sizeof(LaneConst), "cudaMalloc lanes");
     ck(cudaMemcpyAsync(d_lc_, lc.data(), nl_ * sizeof(LaneConst), cudaMemcpyHostToDevice, s),
        "upload lanes");
@@ -327,8 +330,8 @@ void Generator::release(cudaStream_t after) noexcept {
 
 uint32_t Generator::orbit_cap_iters() const {
   // orbit bytes per iteration: LASM keeps every (x, y); PLCM one 8-byte
-  // checkpoint per 8 iterations
-  const uint64_t per = (kind_ == MapKind::Lasm ? 16ull : 1ull) * nl_;
+  // checkpoint per 8 iterations (or every value, dense)
+  const uint64_t per = (kind_ == MapKind::Lasm ? 16ull : pb_.dense ? 8ull : 1ull) * nl_;
   const uint64_t iters = std::min<uint64_t>(kOrbitBytes / per, 1u << 20) / 8 * 8;
   return uint32_t(std::max<uint64_t>(iters, 8));
 }
@@ -647,7 +650,10 @@ void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
     s_gen_ = s_work_;
   }
 
-  gen_.init(lanes, key_.kind, s_gen_, 0);  // orbit buffers sized by ensure_ring
+  // dense orbit in the many-clips configuration (one stream per handle):
+  // the verifier then streams the orbit instead of regenerating it, which
+  // leaves SM issue slots to the other clips' kernels
+  gen_.init(lanes, key_.kind, s_gen_, 0, one_stream_);  // orbit buffers sized by ensure_ring
   bpi_ = gen_.bytes_per_iter();
   ++st_.kernel_launches;
 }
@@ -1206,7 +1212,7 @@ namespace {
 // emitted on another.  launch_iters (0: as large as the orbit budget allows)
 // caps the iterations per generator launch.
 void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len,
-                uint32_t launch_iters, uint64_t* replays) {
+                uint32_t launch_iters, uint64_t* replays, bool dense) {
   cudaStream_t sg = nullptr, sw = nullptr;
   cudaEvent_t chain_done[2] = {nullptr, nullptr}, ver_done[2] = {nullptr, nullptr};
   uint8_t* d_out = nullptr;
@@ -1231,7 +1237,7 @@ void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len,
     for (auto* evs : {chain_done, ver_done})
       for (int k = 0; k < 2; ++k)
         ck(cudaEventCreateWithFlags(&evs[k], cudaEventDisableTiming), "cudaEventCreate");
-    gen.init({w}, kind, sg, 0);
+    gen.init({w}, kind, sg, 0, dense);
     const uint32_t bpi = gen.bytes_per_iter();
     const uint64_t iters = round_up((len + bpi - 1) / bpi, 8);
     uint64_t chunk = std::min<uint64_t>(gen.orbit_cap_iters(), iters);
@@ -1262,7 +1268,7 @@ void standalone(const WorkerLanes& w, MapKind kind, uint8_t* out, size_t len,
 }  // namespace
 
 void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len,
-                       uint32_t launch_iters, uint64_t* replays) {
+                       uint32_t launch_iters, uint64_t* replays, bool dense) {
   if (replays) *replays = 0;
   if (len == 0) return;
   HostPrbg validate(a, b);  // domain checks (bad_key), cheap
@@ -1270,7 +1276,7 @@ void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len,
   WorkerLanes w;
   w.a = a;
   w.b = b;
-  standalone(w, MapKind::Plcm, out, len, launch_iters, replays);
+  standalone(w, MapKind::Plcm, out, len, launch_iters, replays, dense);
 }
 
 void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len) {
@@ -1280,7 +1286,7 @@ void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_
   WorkerLanes w;
   w.la = a;
   w.lb = b;
-  standalone(w, MapKind::Lasm, out, len, 0, nullptr);
+  standalone(w, MapKind::Lasm, out, len, 0, nullptr, false);
 }
 
 KeystreamSource::KeystreamSource(const std::vector<WorkerLanes>& lanes, MapKind kind,

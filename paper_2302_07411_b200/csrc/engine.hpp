@@ -165,8 +165,9 @@ class Generator {
 
   // Uploads the lanes and runs the warm-up on `s` (synchronously).
   // orbit_iters = 0: no orbit buffers yet (see resize).
+  // dense: PLCM chain stores every orbit value (see PrbgBuffers::dense).
   void init(const std::vector<WorkerLanes>& lanes, MapKind kind, cudaStream_t s,
-            uint32_t orbit_iters);
+            uint32_t orbit_iters, bool dense = false);
   // after == nullptr: nothing may still use the buffers; otherwise they are
   // released in the stream order of `after`, behind every user of them.
   void release(cudaStream_t after = nullptr) noexcept;
@@ -317,7 +318,8 @@ class Engine {
 // launch_iters: cap on iterations per generator launch (0: none); replays
 // (may be null): workers the fix-up recomputed exactly.
 void standalone_stream(const Lane& a, const Lane& b, uint8_t* out, size_t len,
-                       uint32_t launch_iters = 0, uint64_t* replays = nullptr);
+                       uint32_t launch_iters = 0, uint64_t* replays = nullptr,
+                       bool dense = false);
 void standalone_stream(const LasmLane& a, const LasmLane& b, uint8_t* out, size_t len);
 
 // Fresh generators for a set of workers (reference WorkerParams::make_prbg,

@@ -44,13 +44,18 @@ void launch_prbg_init(double* state, const LaneConst* lc, const double* x0,
 struct PrbgBuffers {
   double* state;          // nlanes: chain position (written by the chain)
   double* ckpt[2];        // nlanes: start point of launch L (slot L&1)
-  double* orbit[2];       // (max_iters / 8) * nlanes: checkpoints of launch L, the
-                          // orbit value ending each 8-iteration group
+  double* orbit[2];       // launch L's orbit: the value ending each 8-iteration group
+                          // ((max_iters / 8) * nlanes), or every value if dense
   double* verified_end;   // nlanes: verified end point of the last launch
   unsigned* bad;          // nworkers: verification failure flags
   unsigned long long* replays;  // workers recomputed exactly (cumulative)
   unsigned long long* resync;   // nlanes: index of the launch last replayed (~0: none)
   uint32_t max_iters;           // per launch, multiple of 8
+  // Dense orbit: the chain stores every value and the verifier streams them
+  // (DRAM-bound, leaves SM issue slots to other clips' kernels: the
+  // many-clips configuration); otherwise one checkpoint per 8 iterations and
+  // the verifier regenerates the rest (the fastest chain: one clip).
+  bool dense;
 };
 
 // (1) Chain: advances every lane by `iters` (multiple of 8, <= max_iters)

@@ -210,6 +210,7 @@ __device__ __noinline__ double chain_resync(uint32_t l, const LaneConst& c,
 // _rn intrinsics, integer compares, selects), so the verifier regenerates the
 // 7 values in between bit for bit from the previous checkpoint instead of
 // reading them: 1/8 of the stores on the chain and 1/8 of the orbit traffic.
+template <bool DENSE>
 __global__ void __launch_bounds__(128, 1)
     k_prbg_chain(double* __restrict__ state, double* __restrict__ ckpt,
                  const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
@@ -232,6 +233,18 @@ __global__ void __launch_bounds__(128, 1)
     x = chain_resync(l, c, verified_end, resync, launch - R == 2 ? prev_iters : 0u);
   ckpt[l] = x;
   double* o = orbit + l;
+  if (DENSE) {  // every orbit value stored: the verifier streams them from memory
+    for (uint32_t i = 0; i < iters; i += 8) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        x = plcm_fast(x, c);
+        o[size_t(t) * nlanes] = x;
+      }
+      o += size_t(8) * nlanes;
+    }
+    state[l] = x;
+    return;
+  }
 #ifndef CHAIN_GROUPS
 #define CHAIN_GROUPS 4
 #endif
@@ -275,6 +288,7 @@ constexpr int kVerifyIlp = VERIFY_ILP;
 #define VERIFY_MIN_BLOCKS 1
 #endif
 
+template <bool DENSE>
 __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
                        const double* __restrict__ verified_end,
@@ -314,24 +328,40 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
       live[j] = live_thread && gr < groups;
       g[j] = live[j] ? gr : groups - 1;
       cont[j] = true;  // continuity with the previous launch (group 0 only)
+      const size_t prev = DENSE ? size_t(g[j]) * 8 - 1 : size_t(g[j]) - 1;
       if (g[j]) {
-        x[j] = orbit[size_t(g[j] - 1) * nlanes + l];
+        x[j] = orbit[prev * nlanes + l];
       } else {
         x[j] = ckpt[l];
         cont[j] = x[j] == verified_end[l];
       }
-      end[j] = __ldg(orbit + size_t(g[j]) * nlanes + l);
+      if (DENSE) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)  // all in flight
+          y[j][t] = __ldg(orbit + (size_t(g[j]) * 8 + t) * nlanes + l);
+      } else {
+        end[j] = __ldg(orbit + size_t(g[j]) * nlanes + l);
+      }
       ok[j] = true;
       suspect[j] = false;
     }
+    if (DENSE) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t)
+      for (int j = 0; j < kVerifyIlp; ++j) {
+        ok[j] = plcm_verify_fast(x[j], y[j][0], c, suspect[j]);
 #pragma unroll
-      for (int j = 0; j < kVerifyIlp; ++j)
-        y[j][t] = plcm_regen_verify(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
+        for (int t = 1; t < 8; ++t) ok[j] &= plcm_verify_fast(y[j][t - 1], y[j][t], c, suspect[j]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int j = 0; j < kVerifyIlp; ++j)
+          y[j][t] = plcm_regen_verify(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
+    }
 #pragma unroll
     for (int j = 0; j < kVerifyIlp; ++j) {
-      cont[j] &= y[j][7] == end[j];  // the chain walked exactly these values
+      if (!DENSE) cont[j] &= y[j][7] == end[j];  // the chain walked exactly these values
       if (suspect[j]) {  // rare: decide this group exactly
         ok[j] = true;
         for (int t = 0; t < 8; ++t) ok[j] &= plcm_verify_exact(t ? y[j][t - 1] : x[j], y[j][t], c);
@@ -385,13 +415,15 @@ __global__ void k_prbg_fixup(const double* __restrict__ orbit,
                              uint64_t ring_bytes, uint64_t it0,
                              unsigned* __restrict__ bad,
                              unsigned long long* __restrict__ replays,
-                             unsigned long long* __restrict__ resync, uint64_t launch) {
+                             unsigned long long* __restrict__ resync, uint64_t launch,
+                             bool dense) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nworkers) return;
   const uint32_t nl = 2 * nworkers;
-  if (!bad[w]) {  // the launch's last checkpoint is its last orbit value
-    verified_end[2 * w] = orbit[size_t(iters / 8 - 1) * nl + 2 * w];
-    verified_end[2 * w + 1] = orbit[size_t(iters / 8 - 1) * nl + 2 * w + 1];
+  if (!bad[w]) {  // the launch's last orbit value (its last checkpoint)
+    const size_t last = dense ? size_t(iters) - 1 : size_t(iters / 8) - 1;
+    verified_end[2 * w] = orbit[last * nl + 2 * w];
+    verified_end[2 * w + 1] = orbit[last * nl + 2 * w + 1];
     return;
   }
   bad[w] = 0;
@@ -443,8 +475,8 @@ int chain_reserve() {
 }
 
 void configure_prbg_kernels() {
-  cudaFuncSetAttribute(k_prbg_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       chain_reserve());
+  for (auto k : {k_prbg_chain<false>, k_prbg_chain<true>})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, chain_reserve());
 }
 
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
@@ -452,7 +484,8 @@ void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
                        cudaStream_t s) {
   // 128 threads/CTA, one CTA per SM; the dynamic shared memory request only
   // enforces SM exclusivity (chain_reserve).
-  k_prbg_chain<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
+  auto kern = b.dense ? k_prbg_chain<true> : k_prbg_chain<false>;
+  kern<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
       b.state, b.ckpt[slot], lc, b.orbit[slot], iters, nlanes, b.verified_end, b.resync, launch,
       prev_iters);
 }
@@ -475,12 +508,14 @@ void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
   const uint32_t gs = uint32_t(std::max<uint64_t>(
       1, std::min<uint64_t>(groups, (target + nlanes - 1) / nlanes)));
   const uint64_t threads = uint64_t(gs) * nlanes;
-  k_prbg_verify_emit<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
+  auto vk = b.dense ? k_prbg_verify_emit<true> : k_prbg_verify_emit<false>;
+  vk<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
       b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nlanes, gs, ring, ring_bytes,
       it0, b.bad);
   k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.orbit[slot], b.verified_end, lc,
                                                 iters, nw, ring, ring_bytes, it0,
-                                                b.bad, b.replays, b.resync, launch);
+                                                b.bad, b.replays, b.resync, launch,
+                                                b.dense);
 }
 
 }  // namespace cveb

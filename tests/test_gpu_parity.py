@@ -434,6 +434,21 @@ def test_round_fusion_clips_vs_reference(name):
     assert n == (96 if name == "C3" else g["frames"])
 
 
+@pytest.mark.parametrize("name,frames", [("C3", 0), ("C4", 30)])
+def test_one_stream_handles_vs_reference(name, frames):
+    # handles created with one stream per handle (the many-clips
+    # configuration) use the dense-orbit generator: every frame of C3 and a
+    # C4 prefix against the reference digests, plus the round trip
+    from _clips import run_clip
+    g = load("clips.json")[name]
+    cve.set_streams_per_handle(1)
+    try:
+        n = run_clip(name, g, g["plain_sha256"], frames=frames)
+    finally:
+        cve.set_streams_per_handle(2)
+    assert n == (frames or g["frames"])
+
+
 def test_sharded_per_frame_calls_and_lasm_vs_oracle():
     # Per-frame drop-in calls on a sharded handle are dealt round-robin over
     # the shards; sides change between calls; a LASM key shards the same way.

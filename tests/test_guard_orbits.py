@@ -73,8 +73,9 @@ def test_guard_hits_in_both_lanes_across_launches():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("dense", [False, True])
 @pytest.mark.parametrize("kind,at,s", [("half", 30, 3), ("p", 9, 3), ("p", 7, 2)])
-def test_guard_hit_resync_limits_replays(kind, at, s):
+def test_guard_hit_resync_limits_replays(kind, at, s, dense):
     # After an exact replay of launch R the chain restarts from the verified
     # end point (launch R+1 in a same-stream pipeline, R+2 here, where chain
     # R+1 already ran from the diverged state): a single guard hit costs a
@@ -85,10 +86,23 @@ def test_guard_hit_resync_limits_replays(kind, at, s):
     x0, p = g.seed(kind, at, s)
     n = 6 * 8192 * 32
     for lanes in ([x0, p, *OTHER], [*OTHER, x0, p]):
-        got, rep = cve.keystream_generate_ex(lanes, n, launch_iters=8192)
+        got, rep = cve.keystream_generate_ex(lanes, n, launch_iters=8192, dense=dense)
         assert np.array_equal(got, plcm_stream(*lanes, n)), lanes
         hits = g.stream_hits(x0, p, 8192 * 32)
         if len(hits) == 1:
             assert 1 <= rep <= 3, rep
         else:
             assert rep >= 30, rep
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,at,s", g.CASES)
+def test_guard_hits_dense_orbit_generator(kind, at, s):
+    # the generator variant of one-stream (many-clips) handles: every orbit
+    # value stored, the verifier reads them back
+    import paper_2302_07411_b200 as cve
+    x0, p = g.seed(kind, at, s)
+    n = 6 * 40000
+    for lanes in ([x0, p, *OTHER], [*OTHER, x0, p]):
+        got, _ = cve.keystream_generate_ex(lanes, n, launch_iters=4096, dense=True)
+        assert np.array_equal(got, plcm_stream(*lanes, n)), lanes
