@@ -37,18 +37,22 @@ def main(tag):
             k = next((k for k in KERNELS if k in name), None)
             if not k:
                 continue
+            if "ILb1" in name:  # the dense-orbit / many-clips variants
+                k += "<dense>"
+            elif "ILb0" in name:
+                k += "<checkpointed>"
             ins = [re.sub(r"\s*/\*.*?\*/\s*", " ", ln).strip().rstrip(";") for ln in body
                    if re.match(r"\s+/\*[0-9a-f]{4}\*/", ln)]
             ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", i).split()[0] for i in ins if i)
             lines.append(f"== {k}  ({name})  {len(ins)} instructions")
             lines.append("   " + ", ".join(f"{op} {c}" for op, c in ops.most_common()))
-            if k == "k_prbg_chain":
-                # the unrolled 8-iteration loop: from the first DADD after the
-                # loop head to the backward branch
+            if k == "k_prbg_chain<checkpointed>":
+                # the main loop: 32 unrolled iterations (4 checkpoint stores),
+                # from its first DADD to its backward branch
                 start = next(i for i, s in enumerate(ins) if s.startswith("DADD"))
-                end = next(i for i in range(len(ins) - 1, 0, -1) if "BRA" in ins[i] and i > start)
-                lines.append("   loop body (8 iterations, one checkpoint store):")
-                lines.extend("     " + s for s in ins[start - 4:end + 1])
+                end = next(i for i in range(start, len(ins)) if "BRA" in ins[i])
+                lines.append("   main loop body (32 iterations, 4 checkpoint stores):")
+                lines.extend("     " + s for s in ins[start:end + 1])
             lines.append("")
     path = os.path.join(ROOT, "profiles", f"{tag}_sass.txt")
     with open(path, "w") as fh:
