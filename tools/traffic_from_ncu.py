@@ -7,6 +7,7 @@ Usage: python tools/traffic_from_ncu.py profiles/r02b_ncu_full_raw.csv ..."""
 import csv
 import json
 import os
+import re
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -31,7 +32,7 @@ out = {"source": [os.path.relpath(p, ROOT) for p in sys.argv[1:]],
                  "writes still dirty in L2 at kernel end are not in dram__bytes_write"}
 for p in sys.argv[1:]:
     for r in rows(p):
-        name = r["Kernel Name"][0].split("(")[0].split("::")[-1]
+        name = re.sub(r"<.*>", "", r["Kernel Name"][0].split("(")[0].split("::")[-1]).strip()
         rec = {"dram_bytes": num(r["dram__bytes_read.sum"]) + num(r["dram__bytes_write.sum"]),
                "dram_read": num(r["dram__bytes_read.sum"]),
                "dram_write": num(r["dram__bytes_write.sum"]),
