@@ -77,11 +77,18 @@ def parse():
 # ---- distributed plumbing ----------------------------------------------------
 
 class Dist:
+    """One process per GPU (torchrun).  The default process group is NCCL on
+    GPU ranks, but the bench's own collectives -- the barrier around timed
+    regions and the max of timings -- go through a gloo group on the host: an
+    NCCL barrier is a kernel that spins on the rank's GPU while it waits, and
+    on GPUs 1..N-1 it would time-slice with rank 0's shards of the clip."""
+
     def __init__(self, use_cuda: bool):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.host = None
         if self.world > 1:
             import torch.distributed as td
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -91,18 +98,18 @@ class Dist:
                 torch.cuda.set_device(self.local)
             td.init_process_group(backend=backend)
             self.pg = td
+            self.host = td.new_group(backend="gloo") if backend != "gloo" else None
 
     def barrier(self):
         if self.pg:
-            self.pg.barrier()
+            self.pg.barrier(group=self.host)
 
     def max(self, v: float) -> float:
         if not self.pg:
             return v
         import torch
-        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        t = torch.tensor([v], dtype=torch.float64)  # host tensor, gloo
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX, group=self.host)
         return float(t.item())
 
     def close(self):
