@@ -455,13 +455,31 @@ def test_sharded_per_frame_calls_and_lasm_vs_oracle():
     for key in (synth.det_key(61), synth.det_key_lasm(61)):
         o = Oracle(key, 4, 5)
         h = cve.Cipher(key, 4, 5, devices=[0, 0, 0])
-        for t, side in enumerate([64, 64, 96, 64, 128, 96, 64]):
+        for t, side in enumerate([64, 64, 96, 60, 128, 100, 64, 44]):
             f = rand_frames(side, 1, 500 + t)[0]
             want = f.copy()
             assert o.encrypt(want) == 0
             h.encrypt_frame(f)
             assert np.array_equal(f, want), (key[:2], t, side)
-        assert h.seeds_drawn == 7
+        assert h.seeds_drawn == 8
+
+
+def test_sharded_generic_geometries_vs_oracle():
+    # shards running the byte-staged and the generic multi-kernel forward
+    # rounds (band too large for one cluster: n = 1 at side 720) and their
+    # inverses, from keystream windows of any length
+    for side, n in ((720, 1), (90, 3), (52, 2)):
+        key = synth.det_key(64 + side)
+        frames = rand_frames(side, 3, side)
+        want = frames.copy()
+        o = Oracle(key, n, 5)
+        for t in range(3):
+            assert o.encrypt(want[t]) == 0
+        got = frames.copy()
+        cve.Cipher(key, n, 5, devices=[0, 0]).encrypt_frames(got)
+        assert np.array_equal(got, want), (side, n)
+        cve.Cipher(key, n, 5, devices=[0, 0, 0]).decrypt_frames(got)
+        assert np.array_equal(got, frames), (side, n)
 
 
 def test_sharded_errors():
