@@ -916,7 +916,7 @@ cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
 // scratch and a copy).  The generic encrypt path stages y in a third
 // scratch frame.
 cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
-                                   bool decrypt, KsWindow ks, uint64_t lo) {
+                                   bool decrypt, KsWindow ks) {
   timed_begin(c.events, c.s_work, false, false);
   launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
   ++st_.kernel_launches;
@@ -947,7 +947,6 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
   if (r_ == 1)
     ck(cudaMemcpyAsync(buf, src, g.frame_bytes, cudaMemcpyDeviceToDevice, c.s_work), "d2d");
   timed_end(c.s_work);
-  (void)lo;
   cudaEvent_t done = c.events.get();
   ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
   ++st_.frames;
@@ -973,7 +972,7 @@ cudaEvent_t Engine::enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed, bo
   if (cudaEvent_t ge = gen_event_covering(lo + need))
     ck(cudaStreamWaitEvent(s_work_, ge, 0), "wait keystream");
   cudaEvent_t done =
-      enqueue_rounds(*local_, buf, g, seed, decrypt, KsWindow{ring_, ring_bytes_, lo % ring_bytes_}, lo);
+      enqueue_rounds(*local_, buf, g, seed, decrypt, KsWindow{ring_, ring_bytes_, lo % ring_bytes_});
   // the rounds read the ring: they are its consumer
   consumers_.push_back(Consumer{lo, lo + need, done, &local_->events});
   after_frame(need);
@@ -1021,7 +1020,7 @@ cudaEvent_t Engine::enqueue_shard_frame(CipherCtx& c, uint8_t* buf, const Geom& 
   cudaEvent_t copied = c.events.get();
   ck(cudaEventRecord(copied, c.s_work), "cudaEventRecord");
   consumers_.push_back(Consumer{lo, lo + need, copied, &c.events});
-  cudaEvent_t done = enqueue_rounds(c, buf, g, seed, decrypt, KsWindow{c.win[w], need, 0}, lo);
+  cudaEvent_t done = enqueue_rounds(c, buf, g, seed, decrypt, KsWindow{c.win[w], need, 0});
   ck(cudaEventRecord(c.win_free[w], c.s_work), "cudaEventRecord");
   return done;
 }

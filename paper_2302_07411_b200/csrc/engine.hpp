@@ -12,8 +12,8 @@
 //   s_work: K1 verification + keystream emission (+ exact fix-up) of each
 //           chain launch, then K4 shift table and K2/K3 rounds of the frames
 //           whose keystream it verified (waits on s_gen and s_h2d events)
-//   s_h2d : host->device frame copies  } created on the first host-API call
-//   s_d2h : device->host copies        } (waits on s_work)
+//   s_h2d : host->device frame copies  } CipherCtx streams, created on the
+//   s_d2h : device->host copies        } first host-API call (wait on s_work)
 //
 // The keystream lives in one ring per worker (ring_bytes each).  Stream byte
 // s of worker i sits at ring[i*ring_bytes + s % ring_bytes]; the generator
@@ -268,7 +268,7 @@ class Engine {
   // Rounds of one frame on ctx (the keystream is read from `ks`); returns
   // the event recorded on ctx.s_work behind them.
   cudaEvent_t enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
-                             bool decrypt, KsWindow ks, uint64_t lo);
+                             bool decrypt, KsWindow ks);
   // Single-device handle: rounds read the ring directly.
   cudaEvent_t enqueue_frame(uint8_t* buf, const Geom& g, uint32_t seed, bool decrypt);
   // Sharded handle: pull the window into the shard, then the rounds there.
