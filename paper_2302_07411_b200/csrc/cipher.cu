@@ -1104,6 +1104,9 @@ __global__ void __launch_bounds__(kSlotThreads, 1)
 #ifndef TILE_THREADS
 #define TILE_THREADS 160
 #endif
+#ifndef TILE_TMA
+#define TILE_TMA 0  // experiment: 1-D TMA bulk copies for K3t's windows
+#endif
 constexpr uint32_t kTileThreads = TILE_THREADS;  // >= the runs of the largest tile
 constexpr uint32_t kTileMaxT = 15;
 constexpr uint32_t kTileMaxW = 128;
@@ -1193,9 +1196,20 @@ __global__ void __launch_bounds__(kTileThreads)
   };
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#if TILE_TMA
+  __shared__ uint64_t tbar;
+  const uint32_t mbar = uint32_t(__cvta_generic_to_shared(&tbar));
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(kTileThreads));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#endif
   if (tid == 0) dcount = 0;
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // previous round / shift table done
+#if TILE_TMA
+  bool arrived = false;
+#endif
   if (tid < nruns) {
     // thread = run: its own windows (cp.async), realigned once they land
     const Run r = run_of(tid);
@@ -1204,7 +1218,7 @@ __global__ void __launch_bounds__(kTileThreads)
     if (kp >= a.ring_bytes) kp -= a.ring_bytes;
     const bool head = r.al == r.band * a.rows && r.be_lo == 0;
     const bool fast = r.be_lo + r.len <= side && !head;
-    const uint32_t w = win_base + tid * 128u;
+    const uint32_t w = win_base + tid * (TILE_TMA ? 144u : 128u);
     if (fast) {
       const uint32_t cb = (P0 - 1) & ~15u;  // fast runs have P0 >= 1
       const uint32_t nc = (P0 + 3u * r.len - cb + 15u) >> 4;  // bytes P0-1 .. P0+3len-1
@@ -1212,6 +1226,29 @@ __global__ void __launch_bounds__(kTileThreads)
       const uint64_t kb = kp & ~uint64_t(15);
       const uint32_t nk = (uint32_t(kp & 15u) + 3u * r.len + 15u) >> 4;
       const uint64_t kpol = ks_policy();
+#if TILE_TMA
+      // experiment: 1-D TMA bulk copies of the needed chunks (windows
+      // unswizzled, 144-byte stride), completion on the CTA's mbarrier
+      {
+        const uint64_t kroom = a.ring_bytes - kb;
+        const uint32_t kfirst = kroom < 16u * nk ? uint32_t(kroom) : 16u * nk;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                     "r"(16u * nc + 16u * nk) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(w), "l"(a.src + cb), "r"(16u * nc), "r"(mbar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(w + 64u), "l"(ks + kb), "r"(kfirst), "r"(mbar) : "memory");
+        if (kfirst < 16u * nk)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(w + 64u + kfirst), "l"(ks), "r"(16u * nk - kfirst), "r"(mbar) : "memory");
+        arrived = true;
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0; selp.u32 %0, 1, 0, q; }"
+              : "=r"(done) : "r"(mbar) : "memory");
+      }
+#else
 #pragma unroll
       for (uint32_t c = 0; c < 4; ++c) {
         if (c < nc) CVE_CHECK(within(a.src + cb + 16u * c, 16, a.src, a.frame_bytes));
@@ -1226,18 +1263,19 @@ __global__ void __launch_bounds__(kTileThreads)
       }
       cp_async_commit();
       cp_async_wait<0>();  // this thread's own copies: no CTA barrier needed
+#endif
       uint32_t V[16], R[12], K[12];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
-                     : "r"(w + 16u * (uint32_t(c) ^ (tid & 7u))));
+                     : "r"(w + 16u * (uint32_t(c) ^ (TILE_TMA ? 0u : tid & 7u))));
       realign12(V, (P0 - 1) & 15u, R);  // R byte 0 = c[P0-1], then c[P0..]
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(V[4 * c]), "=r"(V[4 * c + 1]), "=r"(V[4 * c + 2]), "=r"(V[4 * c + 3])
-                     : "r"(w + 16u * (uint32_t(c + 4) ^ (tid & 7u))));
+                     : "r"(w + 16u * (uint32_t(c + 4) ^ (TILE_TMA ? 0u : tid & 7u))));
       realign12(V, uint32_t(kp & 15u), K);
       uint32_t D[12];
 #pragma unroll
@@ -1261,6 +1299,9 @@ __global__ void __launch_bounds__(kTileThreads)
       }
     }
   }
+#if TILE_TMA
+  if (!arrived) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+#endif
   __syncthreads();
   {  // deferred runs: one thread per pixel
     const uint32_t nd = min(dcount, kTileDefer);
@@ -1938,7 +1979,7 @@ bool plan_decrypt_tiles(const Geom& g, uint32_t& T, uint32_t& W, size_t& smem) {
     const uint32_t w = uint32_t(atoi(e));
     if (w >= 16 && w <= kTileMaxW && w % 16 == 0) W = w;
   }
-  smem = size_t(T) * W * 4 + size_t(T + W - 1) * 128;
+  smem = size_t(T) * W * 4 + size_t(T + W - 1) * (TILE_TMA ? 144 : 128);
   return true;
 }
 
