@@ -485,15 +485,17 @@ void CipherCtx::ensure_buffers(const Geom& g, uint32_t nslots) {
   const bool generic = !plan_encrypt(g).fused;
   if (scratch_bytes < scratch_need || (generic && !scratch[2])) {
     sync();
-    for (auto& p : scratch) {
-      dfree(p);
-      p = nullptr;
-    }
+    dfree(scratch[0]);  // scratch[1] lives in the same allocation
+    dfree(scratch[2]);
+    for (auto& p : scratch) p = nullptr;
     scratch_bytes = 0;
-    dmalloc(&scratch[0], scratch_need, "cudaMalloc scratch");
-    dmalloc(&scratch[1], scratch_need, "cudaMalloc scratch");
+    // the two ping-pong frames of the middle rounds in one allocation, so one
+    // L2 access-policy window can cover both
+    dmalloc(&scratch[0], 2 * scratch_need, "cudaMalloc scratch");
+    scratch[1] = scratch[0] + scratch_need;
     if (generic) dmalloc(&scratch[2], scratch_need, "cudaMalloc scratch");
     scratch_bytes = scratch_need;
+    set_l2_window();
   }
   if (shift_cap < g.side) {
     sync();
@@ -517,6 +519,35 @@ void CipherCtx::ensure_buffers(const Geom& g, uint32_t nslots) {
       slot_free.push_back(e);
     }
   }
+}
+
+// Experiment ($CVE_B200_L2_WINDOW=1): an L2 access-policy window marking the
+// two scratch frames persisting on the rounds stream (the middle rounds
+// read and write them; the keystream streams through evict-first).
+void CipherCtx::set_l2_window() {
+  static const bool on = [] {
+    const char* e = std::getenv("CVE_B200_L2_WINDOW");
+    return e && std::atoi(e) == 1;
+  }();
+  if (!on || !s_work || !scratch[0]) return;
+  int max_win = 0, max_persist = 0;
+  if (cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+      max_win <= 0 || max_persist <= 0) {
+    cudaGetLastError();
+    return;
+  }
+  const uint64_t bytes = std::min<uint64_t>(2 * scratch_bytes, uint64_t(max_win));
+  const uint64_t persist = std::min<uint64_t>(bytes, uint64_t(max_persist));
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = scratch[0];
+  v.accessPolicyWindow.num_bytes = bytes;
+  v.accessPolicyWindow.hitRatio = float(double(persist) / double(bytes));
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(s_work, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();
 }
 
 void CipherCtx::ensure_windows(uint64_t bytes_per_worker, uint32_t workers) {
@@ -580,10 +611,9 @@ void CipherCtx::release() noexcept {
   }
   for (auto& kv : sines) dfree(kv.second, fin);
   sines.clear();
-  for (uint8_t*& p : scratch) {
-    dfree(p, fin);
-    p = nullptr;
-  }
+  dfree(scratch[0], fin);  // scratch[1] lives in the same allocation
+  dfree(scratch[2], fin);
+  for (uint8_t*& p : scratch) p = nullptr;
   dfree(d_shift, fin);
   d_shift = nullptr;
   events.release();

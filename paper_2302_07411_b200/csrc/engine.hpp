@@ -145,6 +145,7 @@ struct CipherCtx {
   void ensure_copy_streams();
   void ensure_buffers(const Geom& g, uint32_t nslots);
   void ensure_windows(uint64_t bytes_per_worker, uint32_t workers);
+  void set_l2_window();
   const double* sine_for(uint32_t side);
   void sync();
   // Frees everything in the stream order of s_work (after all queued work).
