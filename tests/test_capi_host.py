@@ -160,6 +160,45 @@ def test_streams_per_handle_setting():
     assert L.cve_set_streams_per_handle(2) == cve.CVE_OK
 
 
+def test_r02_entry_point_argument_checks():
+    # argument errors of the additive r02 calls come before any device work
+    L = cve.lib
+    h = C.c_void_p()
+    devs = (C.c_int * 2)(0, 0)
+    assert L.cve_cipher_create_devices(None, 2, 3, devs, 2, C.byref(h)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create_devices(PLCM.encode(), 2, 3, None, 2, C.byref(h)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create_devices(PLCM.encode(), 2, 3, devs, 0, C.byref(h)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_create_devices(b"00ff", 2, 3, devs, 2, C.byref(h)) == cve.CVE_ERROR_BAD_KEY
+    assert L.cve_cipher_create_devices(PLCM.encode(), 2, 3, devs, 2, None) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    n = C.c_uint32()
+    assert L.cve_cipher_shards(None, C.byref(n), None, 0) == cve.CVE_ERROR_INVALID_ARGUMENT
+    ptrs = (C.c_void_p * 1)()
+    assert L.cve_cipher_encrypt_frames_sharded_async(None, ptrs, 8, 1, None) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_cipher_decrypt_frames_sharded_async(None, ptrs, 8, 1, None) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    for bad in (2, 7):
+        assert L.cve_set_round_fusion(bad) == cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_set_round_fusion(1) == cve.CVE_OK
+    assert L.cve_set_round_fusion(0) == cve.CVE_OK
+    lanes = (C.c_double * 4)(0.1, 0.2, 0.3, 0.4)
+    rep = C.c_uint64()
+    assert L.cve_keystream_generate_ex(None, None, 0, 0, 0, C.byref(rep)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    assert L.cve_keystream_generate_ex(lanes, None, 16, 0, 0, C.byref(rep)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT
+    out = np.zeros(16, dtype=np.uint8)
+    assert L.cve_keystream_generate_ex(lanes, out.ctypes.data, 16, 0, 2, C.byref(rep)) == \
+        cve.CVE_ERROR_INVALID_ARGUMENT  # unknown flag
+    bad = (C.c_double * 4)(0.1, 0.7, 0.3, 0.4)  # p outside (0, 0.5)
+    assert L.cve_keystream_generate_ex(bad, out.ctypes.data, 16, 0, 0, C.byref(rep)) == \
+        cve.CVE_ERROR_BAD_KEY
+
+
 def test_analysis_and_tool_argument_checks():
     # reference capi.cpp:335-383: null options / paths / blocks
     L = cve.lib
