@@ -428,6 +428,7 @@ void configure_kernels_once(int device) {
   DeviceScope scope(device);
   configure_prbg_kernels();
   configure_cipher_kernels();
+  configure_rows_kernels();
   ck(cudaGetLastError(), "kernel attributes");
   done.insert(device);
 }
@@ -960,6 +961,15 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
     return done;
   }
   const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
+  // K2r (rows.cu) for the forward rounds where it applies: 16-byte aligned
+  // frames and keystream, side % 16 == 0 (every benchmark config)
+  RowPlan rplan{};
+  const bool rows = !decrypt && plan_rows_encrypt(g, rplan) && ks.pos % 16 == 0 &&
+                    ks.ring_bytes % 16 == 0 &&
+                    ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
+                      reinterpret_cast<uintptr_t>(c.scratch[0]) |
+                      reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
+  const double* sine = c.sine_for(g.side);
   const uint8_t* src = buf;
   for (uint32_t step = 0; step < r_; ++step) {
     const uint32_t k = decrypt ? r_ - 1 - step : step;
@@ -967,11 +977,15 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
                        ? buf
                        : (src == c.scratch[0] ? c.scratch[1] : c.scratch[0]);
     ks.pos = (base + uint64_t(k) * g.region) % ks.ring_bytes;
-    if (decrypt)
+    if (decrypt) {
       launch_decrypt_round(g, src, dst, ks, c.d_shift, c.s_work, &st_.kernel_launches);
-    else
+    } else if (rows) {
+      launch_encrypt_round_rows(rplan, g, src, dst, ks, sine, seed, c.d_shift, c.s_work);
+      ++st_.kernel_launches;
+    } else {
       launch_encrypt_round(plan, g, src, dst, ks, c.d_shift, c.scratch[2], c.s_work,
                            &st_.kernel_launches);
+    }
     src = dst;
   }
   if (r_ == 1)

@@ -152,6 +152,29 @@ void launch_decrypt_round(const Geom& g, const uint8_t* src, uint8_t* dst,
                           KsWindow ks, const int32_t* shift, cudaStream_t s,
                           uint64_t* launches);
 
+// K2r / K3r (rows.cu): rounds with one lane per destination row; a warp holds
+// bpw = 32/cr blocks of cr lanes, block j of the nb blocks walks L = side/nb
+// source rows.  plan_rows_* returns false when the geometry does not allow
+// them (side % 16, 4-pixel groups, shared memory).
+struct RowPlan {
+  uint32_t cr, h;     // destination rows per CTA; CTAs (one cluster) per band
+  uint32_t bpw, nb, L;
+  uint32_t rs;        // shared-memory row stride
+  size_t smem;
+  uint32_t threads;   // per CTA
+};
+bool plan_rows_encrypt(const Geom& g, RowPlan& p);
+bool plan_rows_decrypt(const Geom& g, RowPlan& p);
+void configure_rows_kernels();
+// K4 is folded in for the row rotations (shift from sine and seed), so the
+// keystream copies start before the previous round ends; `shift` (the K4
+// table of the same frame) gives s_d.
+void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
+                               uint8_t* dst, KsWindow ks, const double* sine, uint32_t seed,
+                               const int32_t* shift, cudaStream_t s);
+void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
+                               uint8_t* dst, KsWindow ks, const int32_t* shift, cudaStream_t s);
+
 // Copies stream bytes [lo, hi) of every worker from one ring to another
 // (ring growth).
 void launch_ring_move(const uint8_t* src, uint64_t src_bytes, uint8_t* dst,
