@@ -969,6 +969,16 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
                     ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
                       reinterpret_cast<uintptr_t>(c.scratch[0]) |
                       reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
+  // K3r (rows.cu) for the inverse rounds: opt-in (CVE_B200_ROWS_DECRYPT=1).
+  // Alone it matches K3t (1920^2: 14.8 vs 14.1 us per round, 768^2: 7.4 vs
+  // 8.5), chained in a frame it is slower (768^2: 46 vs 36 us per frame).
+  RowPlan dplan{};
+  const bool drows = decrypt && std::getenv("CVE_B200_ROWS_DECRYPT") && plan_rows_decrypt(g, dplan) &&
+                     ks.pos % 16 == 0 && ks.ring_bytes % 48 == 0 &&
+                     ks.ring_bytes < (uint64_t(1) << 31) &&
+                     ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
+                       reinterpret_cast<uintptr_t>(c.scratch[0]) |
+                       reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
   const double* sine = c.sine_for(g.side);
   const uint8_t* src = buf;
   for (uint32_t step = 0; step < r_; ++step) {
@@ -977,7 +987,10 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
                        ? buf
                        : (src == c.scratch[0] ? c.scratch[1] : c.scratch[0]);
     ks.pos = (base + uint64_t(k) * g.region) % ks.ring_bytes;
-    if (decrypt) {
+    if (drows) {
+      launch_decrypt_round_rows(dplan, g, src, dst, ks, c.d_shift, c.s_work);
+      ++st_.kernel_launches;
+    } else if (decrypt) {
       launch_decrypt_round(g, src, dst, ks, c.d_shift, c.s_work, &st_.kernel_launches);
     } else if (rows) {
       launch_encrypt_round_rows(rplan, g, src, dst, ks, sine, seed, c.d_shift, c.s_work);

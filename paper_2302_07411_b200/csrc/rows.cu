@@ -63,7 +63,8 @@ __device__ unsigned long long g_rows_prof[8192][8];
 #else
 #define ROWS_STAMP(i) ((void)0)
 #endif
-constexpr uint32_t kRowThreads = 512;  // maximum; the plan picks 256 or 512
+constexpr uint32_t kRowThreads = 1024;  // K2r maximum (the plan picks the count)
+constexpr uint32_t kDecRowThreads = 512;  // K3r maximum
 constexpr uint32_t kRowMaxCr = 16;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -262,8 +263,10 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     };
     // Group g = source rows sr_g .. sr_g-3, sr_g = hi-1-4g.  Its pixel loads
     // are issued two groups ahead.  A lane's column wraps between rows
-    // al0+k+1 and al0+k: groups that have (or follow) such a step, and the
-    // group holding the frame's last pixel, take exact per-pixel addresses.
+    // al0+k+1 and al0+k: groups that have (or follow) such a step take exact
+    // per-pixel addresses, and never read the word after a pixel that ends
+    // on a word boundary (the frame's last pixel, row side-1 / column side-1,
+    // is read by lane side-2-al0 of the last chunk, whose wrap zone it is in).
     struct Grp {
       uint32_t w0[4], w1[4], sh[4];
     };
@@ -271,8 +274,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     uint32_t fa = addr_of(hi - 1u);  // address of the next group to load (fast path)
     auto load = [&](Grp& G, uint32_t g) {
       const uint32_t sr = hi - 1u - 4u * g;
-      const bool slow = __any_sync(amask, (sr >= al0 && sr - 3u <= al0 + cr) ||
-                                              (al0 == 0 && sr == side - 1u));
+      const bool slow = __any_sync(amask, sr >= al0 && sr - 3u <= al0 + cr);
       if (!slow) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -373,11 +375,11 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   //    s_t = segment (jz - t) mod nb (t = 1 .. nb-1), s_nb = jz before column
   //    0.  rowc[t] = the XOR to apply to s_t's stored bytes (relative to the
   //    row start; broadcast), s_x1 = byte offset of s_1 in the row.
-  uint32_t* rowc_all = kfin;  // cr * (nb + 1) words
+  uint32_t* rowc_all = kfin;  // cr * (nb + 2) words (entry nb + 1 unused)
   for (uint32_t kk = warp; kk < cr; kk += blockDim.x >> 5) {
     const uint32_t jz = s_jz[kk], a1 = s_a1[kk];
     const uint8_t* ag = aggb + kk * nb;
-    uint32_t* rowc = rowc_all + kk * (nb + 1);
+    uint32_t* rowc = rowc_all + kk * (nb + 2);
     uint32_t carry = 0;
     for (uint32_t t0 = 0; t0 < nb; t0 += 32) {
       const uint32_t t = t0 + lane;
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   const uint32_t L3 = 3u * a.L;
   for (uint32_t kk = warp; kk < cr; kk += blockDim.x >> 5) {
     const uint32_t D = s_d[kk], rho3 = 3u * s_rho[kk], x1 = s_x1[kk];
-    const uint32_t* rowc = rowc_all + kk * (nb + 1);
+    const uint32_t* rowc = rowc_all + kk * (nb + 2);
     uint32_t e = s_prefix;
     for (uint32_t r = 0; r < kk; ++r) e ^= s_tot[r];
     e = (e & 0xFFu) * 0x01010101u;
@@ -459,16 +461,15 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       t = t > nb ? nb : t;
       const uint32_t xb = t == 0 ? x1 : (t == nb ? RB : x1 + L3 * t);  // next boundary
       const uint32_t bo = xb - x;
-      const uint32_t c0 = rowc[t] ^ e;
-      uint32_t cw[4] = {c0, c0, c0, c0};
-      if (bo < 16u) {
-        const uint32_t c1 = rowc[t + 1] ^ e;
+      const uint32_t c0 = rowc[t] ^ e, c1 = rowc[t + 1] ^ e;
+      // branch-free: word w keeps c0 on its bytes before the boundary
+      // (funnel shift with clamp: 0 -> no byte, >= 32 -> all four)
+      const int sb = int(min(bo, 16u) * 8u);
+      uint32_t cw[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int sh = int(bo) - 4 * w;  // bytes of word w before the boundary
-          const uint32_t keep = sh <= 0 ? 0u : sh >= 4 ? ~0u : (~0u >> (32 - 8 * sh));
-          cw[w] = (c0 & keep) | (c1 & ~keep);
-        }
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t keep = __funnelshift_lc(~0u, 0u, uint32_t(max(sb - 32 * w, 0)));
+        cw[w] = (c0 & keep) | (c1 & ~keep);
       }
       if (su + 16u > RB) {  // the rotation seam: bytes past the row wrap to D
         uint32_t vw[4] = {v.x, v.y, v.z, v.w};
@@ -548,7 +549,7 @@ __device__ __forceinline__ uint32_t inv_pixel(uint32_t cv, uint32_t kv) {
   return ((x | 0x80808080u) - (kv & 0x7F7F7F7Fu)) ^ ((x ^ ~kv) & 0x80808080u);
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_decrypt_round_rows(const RowDecArgs a) {
+__global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const RowDecArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint32_t s_d[kRowMaxCr], s_rho[kRowMaxCr];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -700,8 +701,10 @@ bool plan_rows_encrypt(const Geom& g, RowPlan& p) {
     return false;
   uint32_t forced = 0;
   if (const char* e = std::getenv("CVE_B200_ROWS_CR")) forced = uint32_t(std::atoi(e));
-  uint32_t threads = 512;
+  // 1024 threads for 3840^2 (41 vs 48 us per round), 512 below (C4: 11.4 vs 12.1)
+  uint32_t threads = g.side >= 3072 ? 1024 : 512;
   if (const char* e = std::getenv("CVE_B200_ROWS_THREADS")) threads = uint32_t(std::atoi(e));
+  threads = std::min(threads, kRowThreads);
   const uint32_t nw = threads / 32;
   bool found = false;
   for (uint32_t cr = std::min(g.rows, kRowMaxCr - 1); cr >= 1; --cr) {
@@ -714,7 +717,7 @@ bool plan_rows_encrypt(const Geom& g, RowPlan& p) {
     while (nb > 1 && ((g.side / 4) % nb || g.side / nb < 8)) --nb;
     if ((g.side / 4) % nb || g.side / nb < 8) continue;
     const uint32_t rs = row_stride(g.side);
-    const size_t smem = size_t(cr) * rs + ((cr * nb + 15) & ~15u) + 4 * cr * (nb + 1);
+    const size_t smem = size_t(cr) * rs + ((cr * nb + 15) & ~15u) + 4 * cr * (nb + 2);
     if (smem > 200 * 1024) continue;
     p = RowPlan{cr, g.rows / cr, bpw, nb, g.side / nb, rs, smem, threads};
     found = true;
@@ -732,6 +735,7 @@ bool plan_rows_decrypt(const Geom& g, RowPlan& p) {
   cr = std::max(1u, std::min(cr, std::min(g.side, kRowMaxCr)));
   uint32_t threads = 512;
   if (const char* e = std::getenv("CVE_B200_ROWS_THREADS")) threads = uint32_t(std::atoi(e));
+  threads = std::min(threads, kDecRowThreads);
   const uint32_t bpw = 32 / cr, nw = threads / 32;
   uint32_t nb = nw * bpw;
   while (nb > 1 && (g.side / 4) % nb) --nb;
