@@ -868,7 +868,8 @@ def run_b200(args) -> None:
         # every kernel's per-launch DRAM bytes (ncu replays each launch with a
         # flushed L2, so reuse of the frame buffers across rounds is not seen)
         ver = tr["k_prbg_verify_emit"]
-        rnd = tr["k_encrypt_round_slots"]["dram_bytes"] if side == 1920 else None
+        rk = "k_encrypt_round_rows" if "k_encrypt_round_rows" in tr else "k_encrypt_round_slots"
+        rnd = tr[rk]["dram_bytes"] if side == 1920 else None
         if rnd is not None:
             per_frame = (ch["dram_bytes"] + ver["dram_bytes"]) / ch["iterations"] * iters_per_frame \
                 + synth.ROUNDS * rnd
@@ -923,7 +924,7 @@ def run_b200(args) -> None:
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,
             "verify_emit_fixup_ms": prbg_ms - chain_ms},
-        "cipher": {"kernel": "k_encrypt_round_slots x5 + k_shift per frame",
+        "cipher": {"kernel": "k_encrypt_round_rows (K2r) x5 + k_shift per frame",
                    "ms_per_frame": cipher_ms / frames_timed,
                    "achieved_gbs_2F": cipher_gbs,
                    "frac_of_hbm_2F": (cipher_gbs / hbm) if cipher_gbs else None},

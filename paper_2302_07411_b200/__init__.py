@@ -36,7 +36,9 @@ CVE_MAP_PLCM = 0
 CVE_MAP_LASM = 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libcve_b200.so")
+# CVE_B200_LIBRARY: a variant build of the same library (tools/ experiments,
+# e.g. `make OUT=... BUILD=... EXTRA=-D...`); the product loads the in-tree one.
+lib_path = os.environ.get("CVE_B200_LIBRARY") or os.path.join(_HERE, "libcve_b200.so")
 
 
 class CveError(RuntimeError):

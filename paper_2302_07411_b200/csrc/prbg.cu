@@ -171,6 +171,62 @@ __device__ __forceinline__ double plcm_regen_verify(double x, const LaneConst& c
   return y;
 }
 
+// The verifier's step (r02): the exact next orbit value, computed with the
+// reference's own case logic (chaos.cpp:28-32: f = x > 0.5 ? 1 - x : x;
+// f < p ? f/p : (f - p)/q -- fold tests x >= 0.5, and at x == 0.5, 1 - x ==
+// x), the quotient num/den from the selected operands as fma(num, yh,
+// num*yl), proven correctly rounded by the residual test (same suspect flags
+// as plcm_verify_fast).  It need not reproduce the chain's speculative
+// formula bit for bit: the regenerated orbit is exact step by step, the
+// bytes are emitted from it, and it must end on the chain's checkpoint.  Two
+// operand selects fewer than the chain-exact form (no fold/case offset
+// terms): the verifier is bound by the ALU pipe's selects.
+__device__ __forceinline__ double plcm_check_step(double x, const LaneConst& c, bool& ok,
+                                                  bool& suspect) {
+  const bool fold = x >= 0.5;
+  const double f = fold ? __dsub_rn(1.0, x) : x;  // exact when folded (Sterbenz)
+  const bool low = f < c.p;
+  const double num = low ? f : __dsub_rn(f, c.p);
+  const double yh = low ? c.yh_p : c.yh_q;
+  const double yl = low ? c.yl_p : c.yl_q;
+  const double y = __fma_rn(num, yh, __dmul_rn(num, yl));
+  const unsigned hi = unsigned(__double2hiint(y));
+  const unsigned lo = unsigned(__double2loint(y));
+  const unsigned ex = hi & 0x7FF00000u;
+  const double r = __fma_rn(-y, low ? c.p : c.q, num);
+  const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
+  const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
+  suspect |= (lo == 0u) | (lo == c.plo) | (ex < (53u << 20));
+  ok &= fabs(r) < thr;
+  return y;
+}
+
+// Same decision with fewer operand selects (the verifier is bound by the ALU
+// pipe): the quotient from yh and den alone -- y0 = num*yh, one exact
+// residual correction y = y0 + (num - den*y0)*yh (Markstein's correction
+// of a correctly rounded reciprocal) -- and the threshold den*ulp(y)/2
+// formed from den (p/2 and q/2 are exact halves), so yl, hp/hq need no
+// select.  Still proven by the residual test.
+__device__ __forceinline__ double plcm_check_step_m(double x, const LaneConst& c, bool& ok,
+                                                    bool& suspect) {
+  const bool fold = x >= 0.5;
+  const double f = fold ? __dsub_rn(1.0, x) : x;
+  const bool low = f < c.p;
+  const double num = low ? f : __dsub_rn(f, c.p);
+  const double yh = low ? c.yh_p : c.yh_q;
+  const double den = low ? c.p : c.q;
+  const double y0 = __dmul_rn(num, yh);
+  const double y = __fma_rn(__fma_rn(-y0, den, num), yh, y0);
+  const unsigned hi = unsigned(__double2hiint(y));
+  const unsigned lo = unsigned(__double2loint(y));
+  const unsigned ex = hi & 0x7FF00000u;
+  const double r = __fma_rn(-y, den, num);
+  const double hulp = __hiloint2double(int(ex - (53u << 20)), 0);  // ulp(y) / 2
+  suspect |= (lo == 0u) | (lo == c.plo) | (ex < (54u << 20));
+  ok &= fabs(r) < __dmul_rn(den, hulp);
+  return y;
+}
+
 // Exact decision: the reference step itself (IEEE division + guard).
 __device__ __noinline__ bool plcm_verify_exact(double x, double y, const LaneConst& c) {
   return y == plcm_exact(x, c.p, c.q);
@@ -274,14 +330,21 @@ __global__ void __launch_bounds__(128, 1)
 // emit the keystream: 6 bytes per iteration per worker = the little-endian
 // low 48 mantissa bits of x_a ^ x_b (extract_bytes, chaos.cpp:46-56).
 // Thread = (lane, 8-iteration group), lanes fastest (coalesced checkpoint
-// loads); the group's 8 orbit values are regenerated from the previous
-// group's checkpoint with the chain's own plcm_fast and must end on the
-// group's checkpoint (so they are the values the chain walked).  Lanes a/b of
+// loads); the group's 8 orbit values are regenerated exactly from the
+// previous group's checkpoint (every step proven correctly rounded) and must
+// end on the group's checkpoint, so the chain walked exactly the reference's
+// orbit and the bytes emitted from the regenerated values are the
+// reference's; a group starting from a wrong checkpoint belongs to a flagged
+// worker, whose launch the fix-up replays.  Lanes a/b of
 // a worker are shuffle partners: the even one emits iterations 0-3 of the
 // group, the odd one 4-7.  Group 0 also checks continuity: the launch must
 // start where the previous launch verifiably ended.
 #ifndef VERIFY_ILP
 #define VERIFY_ILP 1
+#endif
+// plcm_check_step (r02, default) or plcm_regen_verify (the chain's formula)
+#ifndef VERIFY_STEP
+#define VERIFY_STEP plcm_check_step
 #endif
 constexpr int kVerifyIlp = VERIFY_ILP;
 #ifndef VERIFY_MIN_BLOCKS
@@ -318,6 +381,18 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
   uint64_t off0 = ((it0 + uint64_t(g0) * 8) * 6u) % ring_bytes;
   const uint64_t off_step = (uint64_t(gs) * 48u) % ring_bytes;
   bool flagged = false;
+  // checkpointed: the next trip's start and end values are loaded one trip
+  // ahead (the loads otherwise stall every trip: register-limited occupancy)
+  auto group_of = [&](uint32_t kk) {
+    const uint32_t gr = g0 + kk * gs;
+    return (live_thread && gr < groups) ? gr : groups - 1;
+  };
+  double nx = 0.0, nend = 0.0;
+  if (!DENSE) {
+    const uint32_t gn = group_of(0);
+    nx = gn ? orbit[size_t(gn - 1) * nlanes + l] : ckpt[l];
+    nend = __ldg(orbit + size_t(gn) * nlanes + l);
+  }
   for (uint32_t k = 0; k < trips; k += kVerifyIlp) {
     uint32_t g[kVerifyIlp];
     bool live[kVerifyIlp], cont[kVerifyIlp], ok[kVerifyIlp], suspect[kVerifyIlp];
@@ -328,19 +403,26 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
       live[j] = live_thread && gr < groups;
       g[j] = live[j] ? gr : groups - 1;
       cont[j] = true;  // continuity with the previous launch (group 0 only)
-      const size_t prev = DENSE ? size_t(g[j]) * 8 - 1 : size_t(g[j]) - 1;
-      if (g[j]) {
-        x[j] = orbit[prev * nlanes + l];
-      } else {
-        x[j] = ckpt[l];
-        cont[j] = x[j] == verified_end[l];
-      }
       if (DENSE) {
+        const size_t prev = size_t(g[j]) * 8 - 1;
+        if (g[j]) {
+          x[j] = orbit[prev * nlanes + l];
+        } else {
+          x[j] = ckpt[l];
+          cont[j] = x[j] == verified_end[l];
+        }
 #pragma unroll
         for (int t = 0; t < 8; ++t)  // all in flight
           y[j][t] = __ldg(orbit + (size_t(g[j]) * 8 + t) * nlanes + l);
       } else {
-        end[j] = __ldg(orbit + size_t(g[j]) * nlanes + l);
+        x[j] = nx;
+        end[j] = nend;
+        if (!g[j]) cont[j] = x[j] == verified_end[l];
+        if (k + j + 1 < trips) {
+          const uint32_t gn = group_of(k + j + 1);
+          nx = gn ? orbit[size_t(gn - 1) * nlanes + l] : ckpt[l];
+          nend = __ldg(orbit + size_t(gn) * nlanes + l);
+        }
       }
       ok[j] = true;
       suspect[j] = false;
@@ -357,7 +439,7 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
       for (int t = 0; t < 8; ++t)
 #pragma unroll
         for (int j = 0; j < kVerifyIlp; ++j)
-          y[j][t] = plcm_regen_verify(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
+          y[j][t] = VERIFY_STEP(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
     }
 #pragma unroll
     for (int j = 0; j < kVerifyIlp; ++j) {

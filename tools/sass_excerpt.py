@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_prbg_chain", "k_prbg_verify_emit", "k_encrypt_round_slots",
+KERNELS = ["k_prbg_chain", "k_prbg_verify_emit", "k_encrypt_round_rows", "k_encrypt_round_slots",
            "k_decrypt_round_tiles", "k_encrypt_frame_cluster", "k_lasm_chain"]
 
 
