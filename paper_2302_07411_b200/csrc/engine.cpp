@@ -684,7 +684,9 @@ void Engine::acquire(const std::vector<WorkerLanes>& lanes) {
   // dense orbit in the many-clips configuration (one stream per handle):
   // the verifier then streams the orbit instead of regenerating it, which
   // leaves SM issue slots to the other clips' kernels
-  gen_.init(lanes, key_.kind, s_gen_, 0, one_stream_);  // orbit buffers sized by ensure_ring
+  bool dense = one_stream_;
+  if (const char* e = std::getenv("CVE_B200_DENSE")) dense = std::atoi(e) != 0;  // experiments only
+  gen_.init(lanes, key_.kind, s_gen_, 0, dense);  // orbit buffers sized by ensure_ring
   bpi_ = gen_.bytes_per_iter();
   ++st_.kernel_launches;
 }
