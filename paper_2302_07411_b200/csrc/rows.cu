@@ -63,6 +63,21 @@ __device__ unsigned long long g_rows_prof[8192][8];
 #else
 #define ROWS_STAMP(i) ((void)0)
 #endif
+// Device-side bounds checks (make BOUNDS=1): global frame / ring addresses
+// and shared-memory row-slot addresses the row kernels form are checked
+// against their buffers; a failure prints and traps.  Compiled out otherwise.
+#ifdef CVE_B200_BOUNDS
+#define RCHECK(cond)                                                                  \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      printf("cve rows bounds check failed: %s (%s:%d) block %d thread %d\n", #cond,  \
+             __FILE__, __LINE__, blockIdx.x, threadIdx.x);                            \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define RCHECK(cond) ((void)0)
+#endif
 constexpr uint32_t kRowThreads = 1024;  // K2r maximum (the plan picks the count)
 constexpr uint32_t kDecRowThreads = 512;  // K3r maximum
 constexpr uint32_t kRowMaxCr = 16;
@@ -108,6 +123,8 @@ __device__ __forceinline__ void bulk_stream(uint32_t dst, const uint8_t* ring,
   while (len) {
     const uint64_t room = ring_bytes - off;
     const uint32_t n = room < len ? uint32_t(room) : len;
+    RCHECK(off < ring_bytes && off + n <= ring_bytes && (off & 15) == 0 && (n & 15) == 0 &&
+           (dst & 15) == 0);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
         "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
@@ -280,6 +297,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
         for (int t = 0; t < 4; ++t) {
           const uint32_t at = fa - uint32_t(t) * (RB - 3u);
           const uint32_t* w = reinterpret_cast<const uint32_t*>(a.src + (at & ~3u));
+          RCHECK(at == addr_of(sr - uint32_t(t)) && uint64_t(at & ~3u) + 8 <= uint64_t(side) * RB);
           G.w0[t] = __ldg(w);
           G.w1[t] = __ldg(w + 1);
           G.sh[t] = at << 3;
@@ -289,6 +307,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
         for (int t = 0; t < 4; ++t) {
           const uint32_t at = addr_of(sr - uint32_t(t));
           const uint32_t* w = reinterpret_cast<const uint32_t*>(a.src + (at & ~3u));
+          RCHECK(uint64_t(at & ~3u) + ((at & 3u) >= 2u ? 8 : 4) <= uint64_t(side) * RB);
           G.w0[t] = __ldg(w);
           G.w1[t] = __ldg(w + ((at & 3u) >= 2u ? 1 : 0));
           G.sh[t] = at << 3;
@@ -316,6 +335,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       if (g + 2u < ngroups) load(G, g + 2u);
       // keystream words of the group (12 bytes at q0 + 12 g)
       uint32_t W1, W2, W3;
+      RCHECK(qw >= su32(sm) + k * a.rs && qw + 16u <= su32(sm) + (k + 1u) * a.rs);
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W1) : "r"(qw + 4u));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W2) : "r"(qw + 8u));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W3) : "r"(qw + 12u));
@@ -456,6 +476,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       int sgn = int(x) - int(rho3);
       sgn += sgn < 0 ? int(RB) : 0;
       const uint32_t su = uint32_t(sgn);
+      RCHECK(D + su >= kk * a.rs && D + su + 16u <= (kk + 1u) * a.rs);
       uint4 v = *reinterpret_cast<const uint4*>(sm + D + su);
       uint32_t t = x < x1 ? 0u : 1u + __umulhi(x - x1, a.magic_3L);
       t = t > nb ? nb : t;
@@ -609,12 +630,15 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
         const uint32_t ca = c * RB + 3u * be;  // the pixel's cipher byte offset
         const uint32_t cm = ca ? ca - 1u : 0u;
         const uint8_t* cw = a.src + (cm & ~3u);
+        RCHECK(uint64_t(cm & ~3u) + ((cm & 3u) ? 8 : 4) <= uint64_t(side) * RB);
         G.c0[t] = __ldg(reinterpret_cast<const uint32_t*>(cw));
         G.c1[t] = __ldg(reinterpret_cast<const uint32_t*>(cw + ((cm & 3u) ? 4 : 0)));
         G.csh[t] = cm << 3;
         uint32_t kp = ko + 3u * be;
         kp -= kp >= a.ring32 ? a.ring32 : 0u;
         const uint8_t* kw = a.ring + uint64_t(__umulhi(c, a.magic_rows)) * a.ring_bytes + (kp & ~3u);
+        RCHECK(kp + 3u <= a.ring32 && uint64_t(kp & ~3u) + ((kp & 3u) >= 2u ? 8 : 4) <= a.ring_bytes &&
+               __umulhi(c, a.magic_rows) < a.n);
         G.k0[t] = __ldg(reinterpret_cast<const uint32_t*>(kw));
         G.k1[t] = __ldg(reinterpret_cast<const uint32_t*>(kw + ((kp & 3u) >= 2u ? 4 : 0)));
         G.ksh[t] = kp << 3;

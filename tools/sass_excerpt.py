@@ -11,7 +11,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_prbg_chain", "k_prbg_verify_emit", "k_encrypt_round_rows", "k_encrypt_round_slots",
+KERNELS = ["k_prbg_chain", "k_prbg_verify_emit", "k_encrypt_round_rows", "k_decrypt_round_rows",
+           "k_encrypt_round_slots",
            "k_decrypt_round_tiles", "k_encrypt_frame_cluster", "k_lasm_chain"]
 
 
@@ -32,7 +33,7 @@ def functions(obj):
 
 def main(tag):
     lines = []
-    for obj in ("prbg.o", "cipher.o", "lasm.o"):
+    for obj in ("prbg.o", "cipher.o", "rows.o", "lasm.o"):
         for name, body in functions(os.path.join(ROOT, "build", "csrc", obj)):
             k = next((k for k in KERNELS if k in name), None)
             if not k:
