@@ -602,7 +602,6 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
     t_ko[c] = ko;
   }
   __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const uint32_t bw = lane / cr, k = lane - bw * cr;
   const uint32_t j = warp * a.bpw + bw;
@@ -701,6 +700,9 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
     for (uint32_t bb = 0; bb < (m8 >> 3); ++bb)
       asm volatile("st.shared.u8 [%0], %1;" ::"r"(qw + bb), "r"(prev >> (8u * (4u - (m8 >> 3) + bb))));
   }
+  // the next round is released only now: triggered at entry, its CTAs were
+  // co-scheduled two per SM with this round's
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   if (tid < cr && a0 + tid < side)
