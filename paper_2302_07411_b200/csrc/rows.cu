@@ -321,12 +321,15 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     if (ngroups > 1) load(GB, 1);
     // smem byte of the segment's first pixel; alignment m is the same for
     // every 4-pixel group (12 bytes)
-    const uint32_t q0 = su32(sm) + D + 3u * i0;
+    // (shared-memory byte offsets; plain C++ accesses, so the compiler may
+    // overlap one group's keystream loads with the previous group's stores:
+    // they never touch the same word)
+    const uint32_t q0 = D + 3u * i0;
     const uint32_t m8 = (q0 & 3u) * 8u;
     uint32_t qw = q0 & ~3u;  // aligned word of the current group's first byte
     mbar_wait(mb, 0);        // keystream in shared memory
-    uint32_t W0;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W0) : "r"(qw));
+    auto smw = [&](uint32_t off) -> uint32_t& { return *reinterpret_cast<uint32_t*>(sm + off); };
+    uint32_t W0 = smw(qw);
     uint32_t prev = 0;  // previous group's out2 (its top bytes precede this group)
     auto step = [&](Grp& G, uint32_t g) {
       uint32_t p[4];
@@ -335,10 +338,10 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       if (g + 2u < ngroups) load(G, g + 2u);
       // keystream words of the group (12 bytes at q0 + 12 g)
       uint32_t W1, W2, W3;
-      RCHECK(qw >= su32(sm) + k * a.rs && qw + 16u <= su32(sm) + (k + 1u) * a.rs);
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W1) : "r"(qw + 4u));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W2) : "r"(qw + 8u));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(W3) : "r"(qw + 12u));
+      RCHECK(qw >= k * a.rs && qw + 16u <= (k + 1u) * a.rs);
+      W1 = smw(qw + 4u);
+      W2 = smw(qw + 8u);
+      W3 = smw(qw + 12u);
       const uint32_t b0 = __funnelshift_r(W0, W1, m8), b1 = __funnelshift_r(W1, W2, m8),
                      b2 = __funnelshift_r(W2, W3, m8);
       const uint32_t y0 = __byte_perm(p[0], p[1], 0x4210), y1 = __byte_perm(p[1], p[2], 0x5421),
@@ -364,13 +367,12 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       const uint32_t A1 = m8 ? __funnelshift_l(o0, o1, m8) : o1;
       const uint32_t A2 = m8 ? __funnelshift_l(o1, o2, m8) : o2;
       if (g == 0 && m8) {
-        for (uint32_t bb = m8 >> 3; bb < 4u; ++bb)
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(qw + bb), "r"(A0 >> (8u * bb)));
+        for (uint32_t bb = m8 >> 3; bb < 4u; ++bb) sm[qw + bb] = uint8_t(A0 >> (8u * bb));
       } else {
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw), "r"(A0));
+        smw(qw) = A0;
       }
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw + 4u), "r"(A1));
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw + 8u), "r"(A2));
+      smw(qw + 4u) = A1;
+      smw(qw + 8u) = A2;
       prev = o2;
       W0 = W3;
       qw += 12u;
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     // tail: the top m bytes of the last group go into the low bytes of the
     // next word (shared with the next segment: bytes only)
     for (uint32_t bb = 0; bb < (m8 >> 3); ++bb)
-      asm volatile("st.shared.u8 [%0], %1;" ::"r"(qw + bb), "r"(prev >> (8u * (4u - (m8 >> 3) + bb))));
+      sm[qw + bb] = uint8_t(prev >> (8u * (4u - (m8 >> 3) + bb)));
     aggb[k * nb + j] = uint8_t(R);
   }
   ROWS_STAMP(2);
