@@ -951,8 +951,20 @@ cudaEvent_t Engine::gen_event_covering(uint64_t end_byte) {
 cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, uint32_t seed,
                                    bool decrypt, KsWindow ks) {
   timed_begin(c.events, c.s_work, false, false);
-  launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
-  ++st_.kernel_launches;
+  // K2r (rows.cu) for the forward rounds where it applies: 16-byte aligned
+  // frames and keystream, side % 16 == 0 (every benchmark config).  It forms
+  // the frame's shifts itself (sine table and seed), so K4 runs only for the
+  // other round kernels.
+  RowPlan rplan{};
+  const bool rows = !decrypt && !fuse_rounds_ && plan_rows_encrypt(g, rplan) &&
+                    ks.pos % 16 == 0 && ks.ring_bytes % 16 == 0 &&
+                    ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
+                      reinterpret_cast<uintptr_t>(c.scratch[0]) |
+                      reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
+  if (!rows) {
+    launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
+    ++st_.kernel_launches;
+  }
   const uint64_t base = ks.pos;
   if (!decrypt && fuse_rounds_ &&
       launch_encrypt_frame(g, buf, ks, c.d_shift, r_, c.s_work, &st_.kernel_launches)) {
@@ -963,14 +975,6 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
     return done;
   }
   const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
-  // K2r (rows.cu) for the forward rounds where it applies: 16-byte aligned
-  // frames and keystream, side % 16 == 0 (every benchmark config)
-  RowPlan rplan{};
-  const bool rows = !decrypt && plan_rows_encrypt(g, rplan) && ks.pos % 16 == 0 &&
-                    ks.ring_bytes % 16 == 0 &&
-                    ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
-                      reinterpret_cast<uintptr_t>(c.scratch[0]) |
-                      reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
   // K3r (rows.cu) for the inverse rounds: opt-in (CVE_B200_ROWS_DECRYPT=1).
   // Alone it matches K3t (1920^2: 14.8 vs 14.1 us per round, 768^2: 7.4 vs
   // 8.5), chained in a frame it is slower (768^2: 46 vs 36 us per frame).
@@ -995,7 +999,7 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
     } else if (decrypt) {
       launch_decrypt_round(g, src, dst, ks, c.d_shift, c.s_work, &st_.kernel_launches);
     } else if (rows) {
-      launch_encrypt_round_rows(rplan, g, src, dst, ks, sine, seed, c.d_shift, c.s_work);
+      launch_encrypt_round_rows(rplan, g, src, dst, ks, sine, seed, c.s_work, step > 0);
       ++st_.kernel_launches;
     } else {
       launch_encrypt_round(plan, g, src, dst, ks, c.d_shift, c.scratch[2], c.s_work,

@@ -166,12 +166,15 @@ struct RowPlan {
 bool plan_rows_encrypt(const Geom& g, RowPlan& p);
 bool plan_rows_decrypt(const Geom& g, RowPlan& p);
 void configure_rows_kernels();
-// K4 is folded in for the row rotations (shift from sine and seed), so the
-// keystream copies start before the previous round ends; `shift` (the K4
-// table of the same frame) gives s_d.
+// K4 is folded in (the row rotations and s_d's row shift from the sine table
+// and the seed), so no shift-table kernel precedes the first round.  pdl:
+// launched as a programmatic dependent of the previous kernel in the stream
+// (rounds 2..r: its keystream copies start before that round ends); the
+// first round of a frame is launched plainly, behind every earlier stream
+// operation (the waits for its keystream and input).
 void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const double* sine, uint32_t seed,
-                               const int32_t* shift, cudaStream_t s);
+                               cudaStream_t s, bool pdl = true);
 void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const int32_t* shift, cudaStream_t s);
 

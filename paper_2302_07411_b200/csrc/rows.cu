@@ -166,8 +166,7 @@ struct RowEncArgs {
   const uint8_t* ring;
   uint64_t ring_bytes;
   uint64_t pos;
-  const double* sine;
-  const int32_t* shift;
+  const double* sine;  // sin(2 pi a / side) (K4's table input): shifts from it and the seed
   uint32_t seed;
   uint32_t side, n, rows, cr, h;
   uint32_t bpw;     // blocks (of cr lanes) per warp = 32 / cr
@@ -794,8 +793,8 @@ static void rows_check(const char* what) {
 
 void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const double* sine, uint32_t seed,
-                               const int32_t* shift, cudaStream_t s) {
-  RowEncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, sine, shift, seed, g.side, g.n,
+                               cudaStream_t s, bool pdl) {
+  RowEncArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, sine, seed, g.side, g.n,
                g.rows, p.cr, p.h, p.bpw, p.nb, p.L, p.rs,
                uint32_t((uint64_t(1) << 32) / p.L + ((uint64_t(1) << 32) % p.L ? 1 : 0)),
                g.region, 0,
@@ -814,7 +813,7 @@ void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* s
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 1 : 2;
+  cfg.numAttrs = (pdl && !std::getenv("CVE_B200_NO_PDL")) ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k_encrypt_round_rows, a);
   rows_check("encrypt_round_rows");
 }

@@ -191,14 +191,14 @@ int main(int argc, char** argv) {
     std::printf("K2r plan: cr %u h %u bpw %u nb %u L %u smem %zu\n", rp.cr, rp.h, rp.bpw, rp.nb,
                 rp.L, rp.smem);
     CK(cudaMemset(dO, 0, F));
-    launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, dShift, s);
+    launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, s);
     CK(cudaGetLastError());
     check("K2r encrypt", C);
-    timeit("K2r", [&] { launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, dShift, s); });
+    timeit("K2r", [&] { launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, s); });
 #ifdef ROWS_PROF
     {
       CK(cudaDeviceSynchronize());
-      launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, dShift, s);
+      launch_encrypt_round_rows(rp, g, dX, dO, w, dSine, seed, s);
       CK(cudaDeviceSynchronize());
       const size_t nc = g.n * rp.h;
       std::vector<unsigned long long> pr(nc * 8);
