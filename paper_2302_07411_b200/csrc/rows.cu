@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   const uint32_t side = a.side, cr = a.cr, nb = a.nb;
   const uint32_t RB = 3u * side;
   const uint32_t al0 = band * a.rows + chunk * cr;
-  uint8_t* aggb = sm + cr * a.rs;                                   // cr * nb bytes
-  uint32_t* kfin = reinterpret_cast<uint32_t*>(aggb + ((cr * nb + 15u) & ~15u));  // cr * nb
+  uint8_t* aggb = sm + cr * a.rs;  // cr * nb bytes: segment aggregates
+  // cr * (nb + 2) words: per row, the segments' constants in row order
+  uint32_t* rowc_all = reinterpret_cast<uint32_t*>(aggb + ((cr * nb + 15u) & ~15u));
   const uint32_t mb = su32(&mbar), pmb = su32(&pmbar);
   ROWS_STAMP(0);
 
@@ -210,6 +211,9 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     s_iz[tid] = rho == 0 ? 0u : side - rho;  // pixel index of column 0
     s_jz[tid] = ~0u;
     s_a1[tid] = 0;
+    // row k's data starts at D_k = k*rs + 16 + (3 rho_k mod 16): the TMA
+    // copies keep the stream's alignment mod 16
+    s_d[tid] = tid * a.rs + 16u + ((3u * rho) & 15u);
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(cr));
@@ -220,10 +224,6 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pmb), "r"(4u * chunk)
                    : "memory");
   }
-  __syncthreads();
-  // Row k's data starts at D_k = k*rs + 16 + (3 rho_k mod 16): the TMA copy
-  // keeps the stream's alignment mod 16.
-  if (tid < cr) s_d[tid] = tid * a.rs + 16u + ((3u * s_rho[tid]) & 15u);
   __syncthreads();
   // 1. Keystream of every destination row into shared memory, rotated.
   if (tid < cr) {
@@ -396,7 +396,6 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   //    s_t = segment (jz - t) mod nb (t = 1 .. nb-1), s_nb = jz before column
   //    0.  rowc[t] = the XOR to apply to s_t's stored bytes (relative to the
   //    row start; broadcast), s_x1 = byte offset of s_1 in the row.
-  uint32_t* rowc_all = kfin;  // cr * (nb + 2) words (entry nb + 1 unused)
   for (uint32_t kk = warp; kk < cr; kk += blockDim.x >> 5) {
     const uint32_t jz = s_jz[kk], a1 = s_a1[kk];
     const uint8_t* ag = aggb + kk * nb;
