@@ -525,7 +525,7 @@ struct RowDecArgs {
   uint32_t side, n, rows, cr;
   uint32_t bpw, nb, L, rs;
   uint64_t region;
-  uint32_t magic_rows;    // ceil(2^32 / rows)
+  uint32_t magic_rows;    // ceil(2^32 / rows) (unused when rows == 1)
   uint32_t pos32, ring32; // pos, ring_bytes (< 2^32: checked by the plan)
 };
 
@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t side = a.side, cr = a.cr, RB = 3u * side;
   const uint32_t a0 = blockIdx.x * cr;
+  // band of cipher row c: c / rows (magic_rows = ceil(2^32 / rows) is 0 for
+  // rows == 1, which does not fit 32 bits)
+  auto band_of = [&](uint32_t c) { return a.rows == 1 ? c : __umulhi(c, a.magic_rows); };
   // per cipher row c: be0[c] = column of output row a0's pixel in row c,
   // ko[c] = stream offset (mod ring) of row c's first byte in its worker's
   // round window
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
     uint32_t be = c + side - a0 + uint32_t(a.shift[c]);
     be -= be >= side ? side : 0u;
     be -= be >= side ? side : 0u;
-    const uint32_t bandc = __umulhi(c, a.magic_rows);
+    const uint32_t bandc = band_of(c);
     uint32_t ko = a.pos32 + (c - bandc * a.rows) * RB;
     ko -= ko >= a.ring32 ? a.ring32 : 0u;
     t_be0[c] = be;
@@ -635,9 +638,9 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
         G.csh[t] = cm << 3;
         uint32_t kp = ko + 3u * be;
         kp -= kp >= a.ring32 ? a.ring32 : 0u;
-        const uint8_t* kw = a.ring + uint64_t(__umulhi(c, a.magic_rows)) * a.ring_bytes + (kp & ~3u);
+        const uint8_t* kw = a.ring + uint64_t(band_of(c)) * a.ring_bytes + (kp & ~3u);
         RCHECK(kp + 3u <= a.ring32 && uint64_t(kp & ~3u) + ((kp & 3u) >= 2u ? 8 : 4) <= a.ring_bytes &&
-               __umulhi(c, a.magic_rows) < a.n);
+               band_of(c) < a.n);
         G.k0[t] = __ldg(reinterpret_cast<const uint32_t*>(kw));
         G.k1[t] = __ldg(reinterpret_cast<const uint32_t*>(kw + ((kp & 3u) >= 2u ? 4 : 0)));
         G.ksh[t] = kp << 3;
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
         for (int t = 0; t < 4; ++t) {
           if (!((G.head >> t) & 1u)) continue;
           const uint32_t c = lo + 4u * g + uint32_t(t);
-          const uint32_t bandc = __umulhi(c, a.magic_rows);
+          const uint32_t bandc = band_of(c);
           const uint32_t nbd = bandc + 1 == a.n ? 0 : bandc + 1;
           const uint64_t last = (uint64_t(nbd) + 1) * a.region - 1;
           uint64_t kq = a.pos + a.region - 1;

@@ -21,7 +21,9 @@ pytestmark = pytest.mark.gpu
 # (side, n, r): K2r chunk heights 3..15, clusters of 1..16 chunks, segment
 # counts that are not powers of two, rows that K2r cannot split (K2s)
 GEOMS = [(48, 16, 5), (64, 1, 3), (96, 2, 5), (144, 3, 2), (160, 10, 5), (240, 8, 5),
-         (256, 16, 1), (320, 20, 3), (480, 8, 5), (512, 32, 2), (576, 16, 5), (32, 16, 5)]
+         (256, 16, 1), (320, 20, 3), (480, 8, 5), (512, 32, 2), (576, 16, 5), (32, 16, 5),
+         # one row per band (K3r once divided by rows with a magic that overflowed)
+         (48, 48, 5), (16, 16, 3)]
 
 
 def rand_frames(side, count, seed):
