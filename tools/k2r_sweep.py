@@ -12,9 +12,24 @@ from _oracle import Oracle
 
 rng = random.Random(int(sys.argv[1]) if len(sys.argv) > 1 else 7)
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 60
+maxside = int(sys.argv[3]) if len(sys.argv) > 3 else 640
 bad = 0
+# one handle across sides: the stream continues through frames of different
+# geometries (ring growth), per-frame calls against one oracle handle
+key = synth.det_key(4321)
+for n in (1, 2, 4, 8, 16):
+    o, h = Oracle(key, n, 5), cve.Cipher(key, n, 5)
+    for t in range(6):
+        side = 16 * n * rng.randint(1, max(1, maxside // (16 * n)))
+        f = np.random.default_rng(t + 50 * n).integers(0, 256, size=(side, side, 3), dtype=np.uint8)
+        a, b = f.copy(), f.copy()
+        assert o.encrypt(a) == 0
+        h.encrypt_frame(b)
+        if not np.array_equal(a, b):
+            bad += 1
+            print(f"FAIL mixed-side handle n={n} frame {t} side={side}", flush=True)
 for it in range(cases):
-    side = 16 * rng.randint(1, 40)
+    side = 16 * rng.randint(1, maxside // 16)
     divs = [d for d in range(1, side + 1) if side % d == 0 and d <= 128]
     n = rng.choice(divs)
     r = rng.choice([1, 2, 3, 5, 5, 5, 7])
