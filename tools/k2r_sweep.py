@@ -41,7 +41,8 @@ for it in range(cases):
     for t in range(2):
         assert o.encrypt(want[t]) == 0
     got = frames.copy()
-    h = cve.Cipher(key, n, r)
+    devs = os.environ.get("SWEEP_DEVICES")  # e.g. "0,0,0": the sharded path on one GPU
+    h = cve.Cipher(key, n, r, devices=[int(d) for d in devs.split(",")] if devs else None)
     for t in range(2):
         h.encrypt_frame(got[t])
     ok = np.array_equal(got, want)
