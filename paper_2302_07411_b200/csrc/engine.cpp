@@ -506,6 +506,7 @@ void CipherCtx::ensure_buffers(const Geom& g, uint32_t nslots) {
     dmalloc(&d_shift, sizeof(int32_t) * g.side, "cudaMalloc shift");
     shift_cap = g.side;
   }
+  if (!d_gbar) dmalloc(&d_gbar, 256, "cudaMalloc grid barrier");
   if (nslots && (slots.size() < nslots || slot_bytes < fb)) {
     sync();
     for (uint8_t* p : slots) dfree(p);
@@ -617,6 +618,8 @@ void CipherCtx::release() noexcept {
   for (uint8_t*& p : scratch) p = nullptr;
   dfree(d_shift, fin);
   d_shift = nullptr;
+  dfree(d_gbar, fin);
+  d_gbar = nullptr;
   events.release();
   for (cudaStream_t s : {owns_work ? s_work : nullptr, s_h2d, s_d2h}) stream_put(s);
   s_work = s_h2d = s_d2h = nullptr;
@@ -966,6 +969,20 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
     ++st_.kernel_launches;
   }
   const uint64_t base = ks.pos;
+  // K2r with every round in one cooperative launch, opt-in
+  // (CVE_B200_ROWS_PERSIST=1): a grid barrier per round costs more than the
+  // programmatic-dependent launches it replaces (C1 34 -> 40, C4 72 -> 74 us
+  // per frame; DESIGN 6a)
+  if (rows && c.d_gbar && std::getenv("CVE_B200_ROWS_PERSIST") &&
+      launch_encrypt_frame_rows(rplan, g, buf, c.scratch[0], c.scratch[1], ks, c.sine_for(g.side),
+                                seed, r_, c.d_gbar, c.s_work)) {
+    ++st_.kernel_launches;
+    timed_end(c.s_work);
+    cudaEvent_t done = c.events.get();
+    ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
+    ++st_.frames;
+    return done;
+  }
   if (!decrypt && fuse_rounds_ &&
       launch_encrypt_frame(g, buf, ks, c.d_shift, r_, c.s_work, &st_.kernel_launches)) {
     timed_end(c.s_work);  // K6: every round in one cluster kernel

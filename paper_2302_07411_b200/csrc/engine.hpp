@@ -129,6 +129,7 @@ struct CipherCtx {
   uint8_t* scratch[3] = {nullptr, nullptr, nullptr};
   uint64_t scratch_bytes = 0;
   int32_t* d_shift = nullptr;
+  unsigned* d_gbar = nullptr;  // grid-barrier counter of the all-rounds K2r launch
   uint32_t shift_cap = 0;
   std::map<uint32_t, double*> sines;
   std::vector<uint8_t*> slots;  // host-API frame slots

@@ -175,6 +175,14 @@ void configure_rows_kernels();
 void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const double* sine, uint32_t seed,
                                cudaStream_t s, bool pdl = true);
+// Every round of one frame in one cooperative launch (K2r with a grid
+// barrier between rounds; the next round's keystream rows load during the
+// current one): buf -> sc0 -> sc1 -> ... -> buf.  gbar: one device counter.
+// false: not applicable or not launchable (e.g. the grid cannot be
+// co-resident); nothing was launched and the caller runs the rounds one by one.
+bool launch_encrypt_frame_rows(const RowPlan& p, const Geom& g, uint8_t* buf, uint8_t* sc0,
+                               uint8_t* sc1, KsWindow ks, const double* sine, uint32_t seed,
+                               uint32_t rounds, unsigned* gbar, cudaStream_t s);
 void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const int32_t* shift, cudaStream_t s);
 

@@ -177,11 +177,22 @@ struct RowEncArgs {
   uint64_t region;
   uint32_t pdl_early;  // trigger the next round at entry (else after the band prefix)
   uint32_t magic_3L;   // ceil(2^32 / 3L)
+  // all rounds in one launch (k_encrypt_round_rows<true>): round k reads
+  // k == 0 ? src : sc[(k-1) & 1] and writes k == rounds-1 ? dst : sc[k & 1];
+  // gbar counts CTAs through the grid barrier between rounds (zeroed per launch)
+  uint32_t rounds;
+  uint8_t* sc[2];
+  unsigned* gbar;
 };
 
+// PERSIST: every round of the frame in one cooperative launch (co-resident
+// grid, a grid barrier after each round's copy-out); the next round's
+// keystream rows land in the other of two shared-memory row buffers while
+// this round runs.  Otherwise one round per launch.
+template <bool PERSIST>
 __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEncArgs a) {
   extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t s_rho[kRowMaxCr], s_d[kRowMaxCr], s_iz[kRowMaxCr], s_jz[kRowMaxCr];
   __shared__ uint32_t s_a1[kRowMaxCr], s_x1[kRowMaxCr], s_tot[kRowMaxCr];
   __shared__ __align__(8) uint64_t pmbar;  // chunk prefixes from the earlier chunks
@@ -193,10 +204,11 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   const uint32_t side = a.side, cr = a.cr, nb = a.nb;
   const uint32_t RB = 3u * side;
   const uint32_t al0 = band * a.rows + chunk * cr;
-  uint8_t* aggb = sm + cr * a.rs;  // cr * nb bytes: segment aggregates
+  const uint32_t bufb = cr * a.rs;  // bytes of one row buffer
+  uint8_t* aggb = sm + (PERSIST ? 2u : 1u) * bufb;  // cr * nb bytes: segment aggregates
   // cr * (nb + 2) words: per row, the segments' constants in row order
   uint32_t* rowc_all = reinterpret_cast<uint32_t*>(aggb + ((cr * nb + 15u) & ~15u));
-  const uint32_t mb = su32(&mbar), pmb = su32(&pmbar);
+  const uint32_t pmb = su32(&pmbar);
   ROWS_STAMP(0);
 
   // 0. Rotation of each destination row (from the sine table and the seed,
@@ -216,7 +228,8 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     s_d[tid] = tid * a.rs + 16u + ((3u * rho) & 15u);
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(cr));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[0])), "r"(cr));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mbar[1])), "r"(cr));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pmb));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // the earlier chunks' totals: 4 bytes each
@@ -225,27 +238,49 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
                    : "memory");
   }
   __syncthreads();
-  // 1. Keystream of every destination row into shared memory, rotated.
-  if (tid < cr) {
-    const uint32_t k = tid, rho = s_rho[k];
-    uint64_t r0 = a.pos + uint64_t(chunk) * cr * RB + uint64_t(k) * RB;
-    r0 %= a.ring_bytes;
-    const uint8_t* ring = a.ring + uint64_t(band) * a.ring_bytes;
-    const uint32_t cut = (3u * rho) & ~15u;  // part 1: [cut, RB) of the row
-    const uint32_t len1 = RB - cut, len2 = (3u * rho + 15u) & ~15u;
-    const uint32_t base = su32(sm) + s_d[k] - ((3u * rho) & 15u);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                 "r"(len1 + len2)
-                 : "memory");
-    const uint64_t pol = evict_first_policy();
-    uint64_t o1 = r0 + cut;
-    o1 -= o1 >= a.ring_bytes ? a.ring_bytes : 0;
-    bulk_stream(base, ring, a.ring_bytes, o1, len1, mb, pol);
-    if (len2) bulk_stream(base + len1, ring, a.ring_bytes, r0, len2, mb, pol);
-  }
-  if (a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // 1. Keystream of every destination row into shared memory, rotated:
+  //    round kk's rows into row buffer bi (its mbarrier mbar[bi]).
+  auto issue_keystream = [&](uint32_t kk, uint32_t bi) {
+    if (tid < cr) {
+      const uint32_t k = tid, rho = s_rho[k];
+      uint64_t r0 = (a.pos + uint64_t(kk) * a.region) % a.ring_bytes + uint64_t(chunk) * cr * RB +
+                    uint64_t(k) * RB;
+      r0 %= a.ring_bytes;
+      const uint8_t* ring = a.ring + uint64_t(band) * a.ring_bytes;
+      const uint32_t cut = (3u * rho) & ~15u;  // part 1: [cut, RB) of the row
+      const uint32_t len1 = RB - cut, len2 = (3u * rho + 15u) & ~15u;
+      const uint32_t base = su32(sm) + bi * bufb + s_d[k] - ((3u * rho) & 15u);
+      const uint32_t mb = su32(&mbar[bi]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                   "r"(len1 + len2)
+                   : "memory");
+      const uint64_t pol = evict_first_policy();
+      uint64_t o1 = r0 + cut;
+      o1 -= o1 >= a.ring_bytes ? a.ring_bytes : 0;
+      bulk_stream(base, ring, a.ring_bytes, o1, len1, mb, pol);
+      if (len2) bulk_stream(base + len1, ring, a.ring_bytes, r0, len2, mb, pol);
+    }
+  };
+  issue_keystream(0, 0);
+  if (!PERSIST && a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.h > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous round wrote src
+  if (!PERSIST) asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous round wrote src
+
+  const uint32_t nrounds = PERSIST ? a.rounds : 1u;
+  for (uint32_t kr = 0; kr < nrounds; ++kr) {
+  const uint32_t bi = PERSIST ? (kr & 1u) : 0u;  // this round's row buffer
+  const uint8_t* __restrict__ src = !PERSIST || kr == 0 ? a.src : a.sc[(kr - 1u) & 1u];
+  uint8_t* __restrict__ dst = !PERSIST || kr + 1u == nrounds ? a.dst : a.sc[kr & 1u];
+  // frames written by this launch (rounds >= 1 of PERSIST) are read through
+  // L2 only: L1 lines cached in an earlier round would be stale
+  const bool coherent = PERSIST && kr > 0;
+  auto ldf = [&](const uint32_t* p) { return coherent ? __ldcg(p) : __ldg(p); };
+  if (PERSIST && kr + 1u < nrounds) {
+    // the next round's rows into the other buffer (its last reader, the
+    // copy-out of round kr-1, finished before the grid barrier)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue_keystream(kr + 1u, bi ^ 1u);
+  }
 
   ROWS_STAMP(1);
   // s_d (engine.cpp:237): the post-confusion byte ((band+1) mod n + 1)*region
@@ -259,7 +294,8 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     if (o < 0) o += side;
     int sr = int(al) - o;
     if (sr < 0) sr += side;
-    sd_val = a.src[(uint64_t(sr) * side + uint32_t(o)) * 3 + 2];
+    const uint64_t ba = (uint64_t(sr) * side + uint32_t(o)) * 3 + 2;
+    sd_val = coherent ? __ldcg(src + ba) : src[ba];
   }
   // 2. Lanes.  Block j = warp * bpw + lane / cr, lane row k = lane % cr.
   const uint32_t bw = lane / cr, k = lane - bw * cr;
@@ -269,7 +305,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   uint32_t R = 0;   // running XOR byte, broadcast to the 4 bytes of a word
   if (active) {
     const uint32_t L = a.L, hi = (j + 1u) * L;
-    const uint32_t D = s_d[k], iz = s_iz[k];
+    const uint32_t D = bi * bufb + s_d[k], iz = s_iz[k];
     const uint32_t i0 = side - hi;  // first pixel index of the segment
     // frame offset of source row sr's pixel for this lane
     auto addr_of = [&](uint32_t sr) {
@@ -295,20 +331,20 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const uint32_t at = fa - uint32_t(t) * (RB - 3u);
-          const uint32_t* w = reinterpret_cast<const uint32_t*>(a.src + (at & ~3u));
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (at & ~3u));
           RCHECK(at == addr_of(sr - uint32_t(t)) && uint64_t(at & ~3u) + 8 <= uint64_t(side) * RB);
-          G.w0[t] = __ldg(w);
-          G.w1[t] = __ldg(w + 1);
+          G.w0[t] = ldf(w);
+          G.w1[t] = ldf(w + 1);
           G.sh[t] = at << 3;
         }
       } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const uint32_t at = addr_of(sr - uint32_t(t));
-          const uint32_t* w = reinterpret_cast<const uint32_t*>(a.src + (at & ~3u));
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(src + (at & ~3u));
           RCHECK(uint64_t(at & ~3u) + ((at & 3u) >= 2u ? 8 : 4) <= uint64_t(side) * RB);
-          G.w0[t] = __ldg(w);
-          G.w1[t] = __ldg(w + ((at & 3u) >= 2u ? 1 : 0));
+          G.w0[t] = ldf(w);
+          G.w1[t] = ldf(w + ((at & 3u) >= 2u ? 1 : 0));
           G.sh[t] = at << 3;
         }
         fa = addr_of(sr - 3u);
@@ -326,7 +362,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     const uint32_t q0 = D + 3u * i0;
     const uint32_t m8 = (q0 & 3u) * 8u;
     uint32_t qw = q0 & ~3u;  // aligned word of the current group's first byte
-    mbar_wait(mb, 0);        // keystream in shared memory
+    mbar_wait(su32(&mbar[bi]), PERSIST ? (kr >> 1) & 1u : 0u);  // keystream in shared memory
     auto smw = [&](uint32_t off) -> uint32_t& { return *reinterpret_cast<uint32_t*>(sm + off); };
     uint32_t W0 = smw(qw);
     uint32_t prev = 0;  // previous group's out2 (its top bytes precede this group)
@@ -337,7 +373,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
       if (g + 2u < ngroups) load(G, g + 2u);
       // keystream words of the group (12 bytes at q0 + 12 g)
       uint32_t W1, W2, W3;
-      RCHECK(qw >= k * a.rs && qw + 16u <= (k + 1u) * a.rs);
+      RCHECK(qw >= bi * bufb + k * a.rs && qw + 16u <= bi * bufb + (k + 1u) * a.rs);
       W1 = smw(qw + 4u);
       W2 = smw(qw + 8u);
       W3 = smw(qw + 12u);
@@ -434,7 +470,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   }
   if (a.h > 1) {
     // every CTA of the cluster has started (phase 0: the arrive at entry)
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (kr == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     if (tid > chunk && tid < a.h) {
       uint32_t ra, rb;
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(&agg_in[chunk])), "r"(tid));
@@ -446,8 +482,14 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     if (tid == 0) {
       uint32_t p = sd_val;
       if (chunk) {
-        mbar_wait(pmb, 0);
+        mbar_wait(pmb, kr & 1u);
         for (uint32_t jj = 0; jj < chunk; ++jj) p ^= agg_in[jj];
+        // re-armed for the next round before the grid barrier, so no earlier
+        // chunk's next total can arrive before its expectation
+        if (PERSIST && kr + 1u < nrounds)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pmb),
+                       "r"(4u * chunk)
+                       : "memory");
       }
       s_prefix = p;
     }
@@ -456,7 +498,7 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   }
   __syncthreads();
   ROWS_STAMP(5);
-  if (!a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!PERSIST && !a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // 5. Copy-out, one warp per row: unit x = 16u of row k lives at smem
   //    D_k + ((x - 3 rho_k) mod 3 side) (16-byte aligned) and belongs to
   //    s_t, t = x < x1 ? 0 : 1 + (x - x1) / 3L; at most one segment boundary
@@ -465,18 +507,18 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
   const uint32_t U = RB >> 4;
   const uint32_t L3 = 3u * a.L;
   for (uint32_t kk = warp; kk < cr; kk += blockDim.x >> 5) {
-    const uint32_t D = s_d[kk], rho3 = 3u * s_rho[kk], x1 = s_x1[kk];
+    const uint32_t D = bi * bufb + s_d[kk], rho3 = 3u * s_rho[kk], x1 = s_x1[kk];
     const uint32_t* rowc = rowc_all + kk * (nb + 2);
     uint32_t e = s_prefix;
     for (uint32_t r = 0; r < kk; ++r) e ^= s_tot[r];
     e = (e & 0xFFu) * 0x01010101u;
-    uint4* out = reinterpret_cast<uint4*>(a.dst + uint64_t(al0 + kk) * RB);
+    uint4* out = reinterpret_cast<uint4*>(dst + uint64_t(al0 + kk) * RB);
     for (uint32_t u = lane; u < U; u += 32) {
       const uint32_t x = 16u * u;
       int sgn = int(x) - int(rho3);
       sgn += sgn < 0 ? int(RB) : 0;
       const uint32_t su = uint32_t(sgn);
-      RCHECK(D + su >= kk * a.rs && D + su + 16u <= (kk + 1u) * a.rs);
+      RCHECK(D + su >= bi * bufb + kk * a.rs && D + su + 16u <= bi * bufb + (kk + 1u) * a.rs);
       uint4 v = *reinterpret_cast<const uint4*>(sm + D + su);
       uint32_t t = x < x1 ? 0u : 1u + __umulhi(x - x1, a.magic_3L);
       t = t > nb ? nb : t;
@@ -511,6 +553,23 @@ __global__ void __launch_bounds__(kRowThreads) k_encrypt_round_rows(const RowEnc
     }
   }
   ROWS_STAMP(6);
+  if (PERSIST && kr + 1u < nrounds) {
+    // grid barrier: every CTA's copy-out of this round is visible before any
+    // CTA's next round reads it (release before the arrival, acquire after)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(a.gbar, 1u);
+      const unsigned want = (kr + 1u) * gridDim.x;
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.gbar) : "memory");
+      } while (seen < want);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  }  // rounds
 }
 
 // ---------------------------------------------------------------------------
@@ -777,9 +836,12 @@ bool plan_rows_decrypt(const Geom& g, RowPlan& p) {
 }
 
 void configure_rows_kernels() {
-  cudaFuncSetAttribute(k_encrypt_round_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
-  cudaFuncSetAttribute(k_encrypt_round_rows, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_encrypt_round_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       227 * 1024);
+  cudaFuncSetAttribute(k_encrypt_round_rows<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_decrypt_round_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
 }
@@ -800,7 +862,8 @@ void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* s
                g.rows, p.cr, p.h, p.bpw, p.nb, p.L, p.rs,
                uint32_t((uint64_t(1) << 32) / p.L + ((uint64_t(1) << 32) % p.L ? 1 : 0)),
                g.region, 0,
-               uint32_t((uint64_t(1) << 32) / (3 * p.L) + ((uint64_t(1) << 32) % (3 * p.L) ? 1 : 0))};
+               uint32_t((uint64_t(1) << 32) / (3 * p.L) + ((uint64_t(1) << 32) % (3 * p.L) ? 1 : 0)),
+               1u, {nullptr, nullptr}, nullptr};
   if (const char* e = std::getenv("CVE_B200_ROWS_PDL_EARLY")) a.pdl_early = uint32_t(std::atoi(e));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g.n * p.h);
@@ -816,8 +879,44 @@ void launch_encrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* s
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = (pdl && !std::getenv("CVE_B200_NO_PDL")) ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k_encrypt_round_rows, a);
+  cudaLaunchKernelEx(&cfg, k_encrypt_round_rows<false>, a);
   rows_check("encrypt_round_rows");
+}
+
+bool launch_encrypt_frame_rows(const RowPlan& p, const Geom& g, uint8_t* buf, uint8_t* sc0,
+                               uint8_t* sc1, KsWindow ks, const double* sine, uint32_t seed,
+                               uint32_t rounds, unsigned* gbar, cudaStream_t s) {
+  const size_t smem = p.smem + size_t(p.cr) * p.rs;  // a second row buffer
+  if (rounds < 2 || smem > 227 * 1024) return false;
+  RowEncArgs a{buf, buf, ks.ring, ks.ring_bytes, ks.pos, sine, seed, g.side, g.n,
+               g.rows, p.cr, p.h, p.bpw, p.nb, p.L, p.rs,
+               uint32_t((uint64_t(1) << 32) / p.L + ((uint64_t(1) << 32) % p.L ? 1 : 0)),
+               g.region, 0,
+               uint32_t((uint64_t(1) << 32) / (3 * p.L) + ((uint64_t(1) << 32) % (3 * p.L) ? 1 : 0)),
+               rounds, {sc0, sc1}, gbar};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g.n * p.h);
+  cfg.blockDim = dim3(p.threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.h;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;  // the grid barrier needs a co-resident grid
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  if (cudaMemsetAsync(gbar, 0, sizeof(unsigned), s) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (cudaLaunchKernelEx(&cfg, k_encrypt_round_rows<true>, a) != cudaSuccess) {
+    cudaGetLastError();  // e.g. the grid cannot be co-resident: per-round launches
+    return false;
+  }
+  return true;
 }
 
 void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,

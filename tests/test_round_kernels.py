@@ -64,10 +64,13 @@ def encrypt_vs_oracle(side, n, r, seed):
 
 @pytest.mark.parametrize("side,n,r", GEOMS)
 def test_forward_rounds_k2r_and_k2s(side, n, r):
-    # default (K2r where it applies) and the K2s fallback forced
+    # default (K2r where it applies), the K2s fallback forced, and K2r with
+    # every round of a frame in one cooperative launch (opt-in)
     encrypt_vs_oracle(side, n, r, side * 17 + n + r)
     with env(CVE_B200_NO_ROWS="1"):
         encrypt_vs_oracle(side, n, r, side * 19 + n + r)
+    with env(CVE_B200_ROWS_PERSIST="1"):
+        encrypt_vs_oracle(side, n, r, side * 29 + n + r)
 
 
 @pytest.mark.parametrize("side,n,r", GEOMS)
