@@ -29,6 +29,12 @@
 //   (cluster) give the row's; the copy-out to global XORs the constant of the
 //   segment each 16-byte unit lies in.
 //
+//   k_encrypt_round_rows<true> runs every round of a frame in one
+//   cooperative launch (grid barrier between rounds, the next round's
+//   keystream rows prefetched into a second row buffer).  It is opt-in: it
+//   measured slower than per-round launches chained by programmatic
+//   dependent launch.
+//
 // Inverse round (K3r, k_decrypt_round_rows): inverse_diffuse_region
 // (engine.cpp:75-83, engine.hpp:36-38), head fix-up (engine.cpp:271-276),
 // inverse_confuse_rows (engine.cpp:49-64).  Output row a0+k, column o comes
