@@ -991,33 +991,6 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
     ++st_.frames;
     return done;
   }
-  // K3f (rows.cu): the inverse rounds as r + 1 launches (inverse diffusion
-  // of the last round, then gathers each fused with the next round's
-  // inverse diffusion): buf -> sc0 -> sc1 -> ... -> buf
-  RowPlan fplan{};
-  if (decrypt && std::getenv("CVE_B200_FDEC") && !std::getenv("CVE_B200_ROWS_DECRYPT") &&
-      plan_rows_fdec(g, fplan) && ks.pos % 16 == 0 && ks.ring_bytes % 16 == 0 &&
-      ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
-        reinterpret_cast<uintptr_t>(c.scratch[0]) | reinterpret_cast<uintptr_t>(c.scratch[1])) %
-       16) == 0) {
-    auto win = [&](uint32_t k) {
-      return KsWindow{ks.ring, ks.ring_bytes, (base + uint64_t(k) * g.region) % ks.ring_bytes};
-    };
-    launch_inv_diffuse(g, buf, c.scratch[0], win(r_ - 1), c.s_work);
-    uint8_t* src = c.scratch[0];
-    for (uint32_t k = r_; k-- > 0;) {
-      uint8_t* dst = k == 0 ? buf : (src == c.scratch[0] ? c.scratch[1] : c.scratch[0]);
-      launch_decrypt_fused(fplan, g, src, dst, win(k == 0 ? 0 : k - 1), c.d_shift, k > 0,
-                           c.s_work);
-      src = dst;
-    }
-    st_.kernel_launches += r_ + 1;
-    timed_end(c.s_work);
-    cudaEvent_t done = c.events.get();
-    ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
-    ++st_.frames;
-    return done;
-  }
   const EncPlan plan = decrypt ? EncPlan{} : plan_encrypt(g);
   // K3r (rows.cu) for the inverse rounds: opt-in (CVE_B200_ROWS_DECRYPT=1).
   // Alone it matches K3t (1920^2: 14.8 vs 14.1 us per round, 768^2: 7.4 vs

@@ -186,17 +186,6 @@ bool launch_encrypt_frame_rows(const RowPlan& p, const Geom& g, uint8_t* buf, ui
 void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const int32_t* shift, cudaStream_t s);
 
-// K3f (rows.cu): the inverse rounds regrouped into pure gathers.  D0 =
-// launch_inv_diffuse (inverse diffusion of round r-1, window ks); then for
-// k = r-1 .. 0 launch_decrypt_fused: inverse confusion of round k, and when
-// next (k > 0) the inverse diffusion of round k-1 (window ks_next) on the
-// gathered rows.
-bool plan_rows_fdec(const Geom& g, RowPlan& p);
-void launch_inv_diffuse(const Geom& g, const uint8_t* src, uint8_t* dst, KsWindow ks,
-                        cudaStream_t s);
-void launch_decrypt_fused(const RowPlan& p, const Geom& g, const uint8_t* src, uint8_t* dst,
-                          KsWindow ks_next, const int32_t* shift, bool next, cudaStream_t s);
-
 // Copies stream bytes [lo, hi) of every worker from one ring to another
 // (ring growth).
 void launch_ring_move(const uint8_t* src, uint64_t src_bytes, uint8_t* dst,

@@ -87,7 +87,6 @@ __device__ unsigned long long g_rows_prof[8192][8];
 constexpr uint32_t kRowThreads = 1024;  // K2r maximum (the plan picks the count)
 constexpr uint32_t kDecRowThreads = 512;  // K3r maximum
 constexpr uint32_t kRowMaxCr = 16;
-constexpr uint32_t kFdecSmem = 224 * 1024;  // K3f dynamic shared memory limit
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return uint32_t(__cvta_generic_to_shared(p));
@@ -593,7 +592,6 @@ struct RowDecArgs {
   uint64_t region;
   uint32_t magic_rows;    // ceil(2^32 / rows) (unused when rows == 1)
   uint32_t pos32, ring32; // pos, ring_bytes (< 2^32: checked by the plan)
-  uint64_t pos_n;         // K3f: stream window of the round the output belongs to
 };
 
 // Row k of the CTA out by TMA bulk stores: global byte x of the row is at
@@ -779,298 +777,6 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
     row_store_tma(a.dst + uint64_t(a0 + tid) * RB, su32(sm) + s_d[tid], 3u * s_rho[tid], RB);
 }
 
-
-// ---------------------------------------------------------------------------
-// K3f: the inverse rounds regrouped so that every launch is a pure gather.
-// The inverse round k is inverse diffusion of round k (elementwise, reads
-// the cipher frame and round k's keystream) followed by inverse confusion of
-// round k (a gather).  Regrouped:
-//   D0           inverse diffusion of round r-1 alone (k_inv_diffuse),
-//   F_k, k>0     inverse confusion of round k, then -- on the gathered rows in
-//                shared memory -- inverse diffusion of round k-1
-//                (k_decrypt_fused<true>),
-//   F_0          inverse confusion of round 0 alone (k_decrypt_fused<false>).
-// The gather lanes load 3 bytes per pixel and no keystream (K3r's lanes load
-// the byte before each pixel and its keystream too); the keystream of round
-// k-1 arrives row by row by TMA, rotated like the gathered rows, and the
-// elementwise pass runs over 16-byte units of shared memory.  Reference:
-// inverse_diffuse_region (engine.cpp:75-83), head fix-up (engine.cpp:271-276),
-// inverse_confuse_rows (engine.cpp:49-64), the round order (engine.cpp:259-284).
-
-// d = ((b ^ c ^ c_prev) - b) bytewise on whole words (engine.hpp:36-38).
-__device__ __forceinline__ uint32_t inv_word(uint32_t c, uint32_t cp, uint32_t kv) {
-  const uint32_t x = kv ^ c ^ cp;
-  return ((x | 0x80808080u) - (kv & 0x7F7F7F7Fu)) ^ ((x ^ ~kv) & 0x80808080u);
-}
-
-// The byte preceding every band's first byte in the inverse diffusion
-// (engine.cpp:271-276): the next band's last byte, inverse-diffused.  f is
-// the cipher frame of the round whose window pos is; last = the next band's
-// final byte offset.
-__device__ __forceinline__ uint32_t band_head_prev(uint32_t c_last, uint32_t c_last1,
-                                                   const uint8_t* ring, uint64_t ring_bytes,
-                                                   uint32_t nbd, uint64_t pos, uint64_t region) {
-  uint64_t kq = pos + region - 1;
-  kq %= ring_bytes;
-  const uint32_t bl = ring[uint64_t(nbd) * ring_bytes + kq];
-  return ((bl ^ c_last ^ c_last1) - bl) & 0xFFu;
-}
-
-struct InvDiffArgs {
-  const uint8_t* src;
-  uint8_t* dst;
-  const uint8_t* ring;
-  uint64_t ring_bytes, pos, region;
-  uint32_t n, units;  // units: 16-byte units of the frame
-};
-
-// D0: one thread per 16-byte unit of the frame (bands are multiples of 16
-// bytes, so a unit never straddles two bands or the ring's end).
-__global__ void __launch_bounds__(256) k_inv_diffuse(const InvDiffArgs a) {
-  // the first fused launch may stage its keystream rows meanwhile
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t lane = threadIdx.x & 31u;
-  uint4 c = make_uint4(0, 0, 0, 0);
-  const uint32_t off = u * 16u;
-  if (u < a.units) c = __ldg(reinterpret_cast<const uint4*>(a.src + off));
-  uint32_t pb = __shfl_up_sync(0xFFFFFFFFu, c.w >> 24, 1);
-  if (u < a.units) {
-    const uint32_t band = off / uint32_t(a.region);
-    const uint32_t j = off - band * uint32_t(a.region);
-    if (j == 0) {
-      const uint32_t nbd = band + 1 == a.n ? 0 : band + 1;
-      const uint64_t last = (uint64_t(nbd) + 1) * a.region - 1;
-      pb = band_head_prev(a.src[last], a.src[last - 1], a.ring, a.ring_bytes, nbd, a.pos,
-                          a.region);
-    } else if (lane == 0) {
-      pb = a.src[off - 1];
-    }
-    uint64_t kq = a.pos + j;
-    kq -= kq >= a.ring_bytes ? a.ring_bytes : 0;
-    RCHECK(kq + 16 <= a.ring_bytes && (kq & 15) == 0 && band < a.n);
-    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(a.ring + uint64_t(band) * a.ring_bytes + kq));
-    uint4 d;
-    d.x = inv_word(c.x, (c.x << 8) | pb, b.x);
-    d.y = inv_word(c.y, __funnelshift_l(c.x, c.y, 8), b.y);
-    d.z = inv_word(c.z, __funnelshift_l(c.y, c.z, 8), b.z);
-    d.w = inv_word(c.w, __funnelshift_l(c.z, c.w, 8), b.w);
-    *reinterpret_cast<uint4*>(a.dst + off) = d;
-  }
-}
-
-// F_k.  Output row a0+k, column o <- cipher row (a0+k+o) mod side (K3r's
-// mapping and smem rotation).  NEXT: the output rows are the cipher frame of
-// round k-1; its keystream rows (window pos_n) land in a second row buffer
-// by TMA, rotated the same way, and the inverse diffusion overwrites them.
-template <bool NEXT>
-__global__ void __launch_bounds__(kDecRowThreads) k_decrypt_fused(const RowDecArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ uint32_t s_d[kRowMaxCr], s_rho[kRowMaxCr], s_prev[kRowMaxCr];
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t side = a.side, cr = a.cr, RB = 3u * side;
-  const uint32_t a0 = blockIdx.x * cr;
-  const uint32_t bufb = cr * a.rs;
-  auto band_of = [&](uint32_t c) { return a.rows == 1 ? c : __umulhi(c, a.magic_rows); };
-  uint32_t* t_be0 = reinterpret_cast<uint32_t*>(sm + (NEXT ? 2u : 1u) * bufb);
-  const uint32_t mb = su32(&mbar);
-  if (tid < cr) {
-    uint32_t rho = 2u * side - a0 - tid;
-    rho -= rho >= side ? side : 0u;
-    rho -= rho >= side ? side : 0u;
-    s_rho[tid] = rho;
-    s_d[tid] = tid * a.rs + 16u + ((3u * rho) & 15u);
-  }
-  if (NEXT) {
-    if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(cr));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // round k-1's keystream of output row a0+k (stream offset (row - band
-    // start) * RB in its band's window), rotated: position r <-> byte
-    // (3 rho + r) mod RB of the row
-    if (tid < cr) {
-      const uint32_t k = tid, row = a0 + k, rho = s_rho[k];
-      uint32_t len1 = 0, len2 = 0;
-      if (row < side) {
-        const uint32_t cut = (3u * rho) & ~15u;
-        len1 = RB - cut;
-        len2 = (3u * rho + 15u) & ~15u;
-      }
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                   "r"(len1 + len2)
-                   : "memory");
-      if (row < side) {
-        const uint32_t b = band_of(row);
-        const uint64_t r0 = (a.pos_n + uint64_t(row - b * a.rows) * RB) % a.ring_bytes;
-        const uint8_t* ring = a.ring + uint64_t(b) * a.ring_bytes;
-        const uint32_t base = su32(sm) + bufb + s_d[k] - ((3u * rho) & 15u);
-        const uint64_t pol = evict_first_policy();
-        uint64_t o1 = r0 + (RB - len1);
-        o1 -= o1 >= a.ring_bytes ? a.ring_bytes : 0;
-        bulk_stream(base, ring, a.ring_bytes, o1, len1, mb, pol);
-        if (len2) bulk_stream(base + len1, ring, a.ring_bytes, r0, len2, mb, pol);
-      }
-    }
-  }
-  for (uint32_t c = tid; c < side; c += blockDim.x) {
-    uint32_t be = c + side - a0 + uint32_t(a.shift[c]);
-    be -= be >= side ? side : 0u;
-    be -= be >= side ? side : 0u;
-    t_be0[c] = be;
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous launch wrote src
-  __syncthreads();
-
-  const uint32_t bw = lane / cr, k = lane - bw * cr;
-  const uint32_t j = warp * a.bpw + bw;
-  const bool active = bw < a.bpw && j < a.nb && a0 + k < side;
-  if (active) {
-    const uint32_t L = a.L, lo = j * L;
-    uint32_t qw = su32(sm) + s_d[k] + 3u * lo;
-    const uint32_t m8 = (qw & 3u) * 8u;
-    qw &= ~3u;
-    uint32_t prev = 0;
-    struct Grp {
-      uint32_t c0[4], c1[4], csh[4];
-    };
-    auto load = [&](Grp& G, uint32_t g) {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const uint32_t c = lo + 4u * g + uint32_t(t);
-        const uint32_t be0 = t_be0[c];
-        uint32_t be = be0 - k;
-        be += be0 < k ? side : 0u;
-        const uint32_t ca = c * RB + 3u * be;
-        const uint8_t* cw = a.src + (ca & ~3u);
-        RCHECK(uint64_t(ca & ~3u) + ((ca & 3u) >= 2u ? 8 : 4) <= uint64_t(side) * RB);
-        G.c0[t] = __ldg(reinterpret_cast<const uint32_t*>(cw));
-        G.c1[t] = __ldg(reinterpret_cast<const uint32_t*>(cw + ((ca & 3u) >= 2u ? 4 : 0)));
-        G.csh[t] = ca << 3;
-      }
-    };
-    const uint32_t ngroups = L >> 2;
-    Grp GA, GB;
-    load(GA, 0);
-    if (ngroups > 1) load(GB, 1);
-    auto step = [&](Grp& G, uint32_t g) {
-      uint32_t d[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) d[t] = __funnelshift_r(G.c0[t], G.c1[t], G.csh[t]);
-      if (g + 2u < ngroups) load(G, g + 2u);
-      const uint32_t o0 = __byte_perm(d[0], d[1], 0x4210), o1 = __byte_perm(d[1], d[2], 0x5421),
-                     o2 = __byte_perm(d[2], d[3], 0x6542);
-      const uint32_t A0 = m8 ? __funnelshift_l(prev, o0, m8) : o0;
-      const uint32_t A1 = m8 ? __funnelshift_l(o0, o1, m8) : o1;
-      const uint32_t A2 = m8 ? __funnelshift_l(o1, o2, m8) : o2;
-      if (g == 0 && m8) {
-        for (uint32_t bb = m8 >> 3; bb < 4u; ++bb)
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(qw + bb), "r"(A0 >> (8u * bb)));
-      } else {
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw), "r"(A0));
-      }
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw + 4u), "r"(A1));
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(qw + 8u), "r"(A2));
-      prev = o2;
-      qw += 12u;
-    };
-    for (uint32_t g = 0; g < ngroups; g += 2) {
-      step(GA, g);
-      if (g + 1u < ngroups) step(GB, g + 1u);
-    }
-    for (uint32_t bb = 0; bb < (m8 >> 3); ++bb)
-      asm volatile("st.shared.u8 [%0], %1;" ::"r"(qw + bb), "r"(prev >> (8u * (4u - (m8 >> 3) + bb))));
-  }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  uint32_t out = 0;  // byte offset of the row buffer stored
-  if (NEXT) {
-    // the byte preceding each row's first byte: the previous row's last
-    // byte, or at a band start the band-head value of engine.cpp:271-276
-    uint32_t pv = 0;
-    if (tid < cr && a0 + tid < side) {
-      const uint32_t row = a0 + tid;
-      auto cipher_at = [&](uint32_t orow, uint32_t ch) {  // this output frame, column side-1
-        uint32_t al = orow + side - 1u;
-        al -= al >= side ? side : 0u;
-        uint32_t be = side - 1u + uint32_t(a.shift[al]);
-        be -= be >= side ? side : 0u;
-        return uint32_t(a.src[uint64_t(al) * RB + 3u * be + ch]);
-      };
-      const uint32_t b = band_of(row);
-      if (row == b * a.rows) {
-        const uint32_t nbd = b + 1 == a.n ? 0 : b + 1;
-        const uint32_t lr = nbd * a.rows + a.rows - 1u;
-        pv = band_head_prev(cipher_at(lr, 2), cipher_at(lr, 1), a.ring, a.ring_bytes, nbd, a.pos_n,
-                            a.region);
-      } else if (tid == 0) {
-        pv = cipher_at(row - 1u, 2);
-      }
-    }
-    __syncthreads();  // every gathered row is in shared memory
-    if (tid < cr && a0 + tid < side && !(a0 + tid == band_of(a0 + tid) * a.rows) && tid > 0) {
-      const uint32_t rp = s_rho[tid - 1];  // row tid-1's byte RB-1 at position (RB-1-3rp) mod RB
-      const uint32_t r = RB - 1u - 3u * rp;
-      uint32_t byte;
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(byte) : "r"(su32(sm) + s_d[tid - 1] + r));
-      pv = byte;
-    }
-    if (tid < cr) s_prev[tid] = pv;
-    __syncthreads();
-    mbar_wait(mb, 0);  // the keystream rows have landed
-    // 16-byte units of each row slot: unit q covers slot bytes [16 + 16q, 32 + 16q)
-    const uint32_t nq = RB / 16u + 1u;
-    const uint32_t rows_here = min(cr, side - a0);
-    for (uint32_t idx = tid; idx < rows_here * nq; idx += blockDim.x) {
-      const uint32_t kk = idx / nq, q = idx - kk * nq;
-      const uint32_t rho3 = 3u * s_rho[kk];
-      const uint32_t P = su32(sm) + kk * a.rs + 16u + 16u * q;
-      uint4 c;
-      uint32_t pb;
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w)
-                   : "r"(P));
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(pb) : "r"(P - 1u));
-      uint32_t cp0 = (c.x << 8), cp1 = __funnelshift_l(c.x, c.y, 8),
-               cp2 = __funnelshift_l(c.y, c.z, 8), cp3 = __funnelshift_l(c.z, c.w, 8);
-      // row position 0 (byte rho3 of the row): its predecessor is the row's
-      // byte rho3-1, at position RB-1 (rho > 0; else it is the row's first)
-      const uint32_t b1 = rho3 & 15u;
-      if (q == 0 && rho3) {
-        uint32_t v;
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(su32(sm) + s_d[kk] + RB - 1u));
-        if (b1 == 0) {
-          pb = v;
-        } else {
-          const uint32_t w = b1 >> 2, sh = 8u * (b1 & 3u), m = ~(0xFFu << sh);
-          if (w == 0) cp0 = (cp0 & m) | (v << sh);
-          if (w == 1) cp1 = (cp1 & m) | (v << sh);
-          if (w == 2) cp2 = (cp2 & m) | (v << sh);
-          if (w == 3) cp3 = (cp3 & m) | (v << sh);
-        }
-      }
-      // the row's byte 0 starts unit (RB - (rho3 & ~15)) / 16 (unit 0 if rho == 0)
-      const uint32_t q0 = rho3 ? (RB - (rho3 & ~15u)) >> 4 : 0u;
-      if (q == q0) pb = s_prev[kk];
-      cp0 |= pb;
-      const uint32_t K = P + bufb;
-      uint4 b;
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
-                   : "r"(K));
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(K), "r"(inv_word(c.x, cp0, b.x)),
-                   "r"(inv_word(c.y, cp1, b.y)), "r"(inv_word(c.z, cp2, b.z)),
-                   "r"(inv_word(c.w, cp3, b.w))
-                   : "memory");
-    }
-    out = bufb;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  if (tid < cr && a0 + tid < side)
-    row_store_tma(a.dst + uint64_t(a0 + tid) * RB, su32(sm) + out + s_d[tid], 3u * s_rho[tid], RB);
-}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1135,37 +841,7 @@ bool plan_rows_decrypt(const Geom& g, RowPlan& p) {
   return true;
 }
 
-// K3f: cr output rows per CTA (two row buffers when the launch also
-// inverse-diffuses), the be0 table; the largest cr <= 16 that fits.
-bool plan_rows_fdec(const Geom& g, RowPlan& p) {
-  if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32) || std::getenv("CVE_B200_NO_ROWS") ||
-      g.rows == 0)
-    return false;
-  uint32_t forced = 0;
-  if (const char* e = std::getenv("CVE_B200_FDEC_CR")) forced = uint32_t(std::atoi(e));
-  uint32_t threads = 512;
-  if (const char* e = std::getenv("CVE_B200_FDEC_THREADS")) threads = uint32_t(std::atoi(e));
-  threads = std::min(threads, kDecRowThreads);
-  const uint32_t rs = row_stride(g.side), nw = threads / 32;
-  for (uint32_t cr = std::min(g.side, kRowMaxCr); cr >= 1; --cr) {
-    if (forced && cr != forced) continue;
-    const size_t smem = 2 * size_t(cr) * rs + 4 * size_t(g.side);
-    if (smem > kFdecSmem) continue;
-    const uint32_t bpw = 32 / cr;
-    uint32_t nb = nw * bpw;
-    while (nb > 1 && (g.side / 4) % nb) --nb;
-    if ((g.side / 4) % nb) continue;
-    p = RowPlan{cr, 1, bpw, nb, g.side / nb, rs, smem, threads};
-    return true;
-  }
-  return false;
-}
-
 void configure_rows_kernels() {
-  cudaFuncSetAttribute(k_decrypt_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kFdecSmem);
-  cudaFuncSetAttribute(k_decrypt_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kFdecSmem);
   cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
   cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1267,37 +943,6 @@ void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* s
   cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 0 : 1;
   cudaLaunchKernelEx(&cfg, k_decrypt_round_rows, a);
   rows_check("decrypt_round_rows");
-}
-
-void launch_inv_diffuse(const Geom& g, const uint8_t* src, uint8_t* dst, KsWindow ks,
-                        cudaStream_t s) {
-  const InvDiffArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, g.region, g.n,
-                      uint32_t(g.frame_bytes / 16)};
-  k_inv_diffuse<<<(a.units + 255) / 256, 256, 0, s>>>(a);
-  rows_check("inv_diffuse");
-}
-
-void launch_decrypt_fused(const RowPlan& p, const Geom& g, const uint8_t* src, uint8_t* dst,
-                          KsWindow ks_next, const int32_t* shift, bool next, cudaStream_t s) {
-  RowDecArgs a{src, dst, ks_next.ring, ks_next.ring_bytes, 0, shift, g.side, g.n, g.rows,
-               p.cr, p.bpw, p.nb, p.L, p.rs, g.region,
-               uint32_t((uint64_t(1) << 32) / g.rows + ((uint64_t(1) << 32) % g.rows ? 1 : 0)),
-               0, uint32_t(ks_next.ring_bytes), ks_next.pos};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((g.side + p.cr - 1) / p.cr);
-  cfg.blockDim = dim3(p.threads);
-  cfg.dynamicSmemBytes = next ? p.smem : p.smem - size_t(p.cr) * p.rs;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = std::getenv("CVE_B200_NO_PDL") ? 0 : 1;
-  if (next)
-    cudaLaunchKernelEx(&cfg, k_decrypt_fused<true>, a);
-  else
-    cudaLaunchKernelEx(&cfg, k_decrypt_fused<false>, a);
-  rows_check("decrypt_fused");
 }
 
 }  // namespace cveb

@@ -104,28 +104,3 @@ def test_k2r_ring_wrap_many_frames():
     got = frames.copy()
     cve.Cipher(key, n, r).encrypt_frames(got)
     assert np.array_equal(got, want)
-
-
-@pytest.mark.parametrize("side,n,r", GEOMS)
-def test_inverse_rounds_k3f(side, n, r):
-    # K3f: inverse diffusion of the last round, then gathers fused with the
-    # next round's inverse diffusion; consecutive frames of one handle, a
-    # LASM key, and two forced row-chunk heights
-    with env(CVE_B200_FDEC="1"):
-        key, frames, ct = encrypt_vs_oracle(side, n, r, side * 31 + n + r)
-        d = cve.Cipher(key, n, r)
-        for t in range(len(frames)):
-            d.decrypt_frame(ct[t])
-        assert np.array_equal(ct, frames)
-        key = synth.det_key_lasm(side + n + r + 1)
-        frames = rand_frames(side, 2, side + 7)
-        ct = frames.copy()
-        cve.Cipher(key, n, r).encrypt_frames(ct)
-        cve.Cipher(key, n, r).decrypt_frames(ct)
-        assert np.array_equal(ct, frames)
-        for cr in ("3", "7"):
-            with env(CVE_B200_FDEC_CR=cr):
-                ct = frames.copy()
-                cve.Cipher(key, n, r).encrypt_frames(ct)
-                cve.Cipher(key, n, r).decrypt_frames(ct)
-                assert np.array_equal(ct, frames), cr
