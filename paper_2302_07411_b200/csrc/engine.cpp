@@ -959,22 +959,12 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
   // the frame's shifts itself (sine table and seed), so K4 runs only for the
   // other round kernels.
   RowPlan rplan{};
-  // K3x (rows.cu) for the inverse rounds (opt-in while measured):
-  // 16-byte aligned frames and keystream, side % 16 == 0; forms its shifts
-  uint32_t xT = 0, xthreads = 0;
-  size_t xsmem = 0;
-  const bool xdec = decrypt && std::getenv("CVE_B200_SCATTER") &&
-                    plan_rows_scatter(g, xT, xthreads, xsmem) && ks.pos % 16 == 0 &&
-                    ks.ring_bytes % 16 == 0 &&
-                    ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
-                      reinterpret_cast<uintptr_t>(c.scratch[0]) |
-                      reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
   const bool rows = !decrypt && !fuse_rounds_ && plan_rows_encrypt(g, rplan) &&
                     ks.pos % 16 == 0 && ks.ring_bytes % 16 == 0 &&
                     ((reinterpret_cast<uintptr_t>(buf) | reinterpret_cast<uintptr_t>(ks.ring) |
                       reinterpret_cast<uintptr_t>(c.scratch[0]) |
                       reinterpret_cast<uintptr_t>(c.scratch[1])) % 16 == 0);
-  if (!rows && !xdec) {
+  if (!rows) {
     launch_shift_table(c.sine_for(g.side), seed, c.d_shift, g.side, c.s_work);
     ++st_.kernel_launches;
   }
@@ -1020,11 +1010,7 @@ cudaEvent_t Engine::enqueue_rounds(CipherCtx& c, uint8_t* buf, const Geom& g, ui
                        ? buf
                        : (src == c.scratch[0] ? c.scratch[1] : c.scratch[0]);
     ks.pos = (base + uint64_t(k) * g.region) % ks.ring_bytes;
-    if (xdec) {
-      launch_decrypt_round_scatter(g, xT, xthreads, xsmem, src, dst, ks, sine, seed, c.s_work,
-                                   step > 0);
-      ++st_.kernel_launches;
-    } else if (drows) {
+    if (drows) {
       launch_decrypt_round_rows(dplan, g, src, dst, ks, c.d_shift, c.s_work);
       ++st_.kernel_launches;
     } else if (decrypt) {

@@ -186,14 +186,6 @@ bool launch_encrypt_frame_rows(const RowPlan& p, const Geom& g, uint8_t* buf, ui
 void launch_decrypt_round_rows(const RowPlan& p, const Geom& g, const uint8_t* src,
                                uint8_t* dst, KsWindow ks, const int32_t* shift, cudaStream_t s);
 
-// K3x (rows.cu): the inverse round in scatter form (T cipher rows per CTA,
-// read whole by TMA, inverse-diffused in shared memory, pixels scattered as
-// word-assembled runs).  Forms the shifts itself (no K4).
-bool plan_rows_scatter(const Geom& g, uint32_t& T, uint32_t& threads, size_t& smem);
-void launch_decrypt_round_scatter(const Geom& g, uint32_t T, uint32_t threads, size_t smem,
-                                  const uint8_t* src, uint8_t* dst, KsWindow ks,
-                                  const double* sine, uint32_t seed, cudaStream_t s, bool pdl);
-
 // Copies stream bytes [lo, hi) of every worker from one ring to another
 // (ring growth).
 void launch_ring_move(const uint8_t* src, uint64_t src_bytes, uint8_t* dst,

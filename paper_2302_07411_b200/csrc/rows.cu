@@ -777,183 +777,6 @@ __global__ void __launch_bounds__(kDecRowThreads) k_decrypt_round_rows(const Row
     row_store_tma(a.dst + uint64_t(a0 + tid) * RB, su32(sm) + s_d[tid], 3u * s_rho[tid], RB);
 }
 
-
-// ---------------------------------------------------------------------------
-// K3x: the inverse round in scatter form.  Each CTA owns T consecutive
-// CIPHER rows (the order the inverse diffusion runs in): it reads them by
-// TMA bulk copies (whole rows, no partial sectors), inverse-diffuses them in
-// shared memory with the round's keystream (prefetched into registers before
-// the previous round ends), and scatters the pixels: output row a receives
-// from these T cipher rows one run of T consecutive pixels, at columns
-// (c0 - a + i) mod side (pixel i from cipher row c0 + i, its column
-// (c0 - a + i + shift[c0 + i]) mod side).  Each run is assembled into
-// aligned 32-bit words by shuffles within a T-lane group and stored; the
-// runs' partial edge words go by bytes.  Reference: inverse_diffuse_region
-// (engine.cpp:75-83), head fix-up (engine.cpp:271-276), inverse_confuse_rows
-// (engine.cpp:49-64).
-struct ScatterArgs {
-  const uint8_t* src;
-  uint8_t* dst;
-  const uint8_t* ring;
-  uint64_t ring_bytes, pos, region;
-  const double* sine;
-  uint32_t seed;
-  uint32_t side, n, rows, T, rs;
-};
-
-// d = ((b ^ c ^ c_prev) - b) bytewise on whole words (engine.hpp:36-38).
-__device__ __forceinline__ uint32_t inv_word(uint32_t c, uint32_t cp, uint32_t kv) {
-  const uint32_t x = kv ^ c ^ cp;
-  return ((x | 0x80808080u) - (kv & 0x7F7F7F7Fu)) ^ ((x ^ ~kv) & 0x80808080u);
-}
-
-constexpr int kScatterCh = 6;  // 16-byte units per thread in the diffusion pass
-
-__global__ void __launch_bounds__(1024) k_decrypt_round_scatter(const ScatterArgs a) {
-  extern __shared__ __align__(128) uint8_t sm[];
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ uint32_t s_shift[16], s_prev[16];
-  const uint32_t tid = threadIdx.x, T = a.T, side = a.side, RB = 3u * side;
-  const uint32_t c0 = blockIdx.x * T;
-  const uint32_t upr = RB / 16u, units = T * upr;
-  const uint32_t mb = su32(&mbar);
-  if (tid < T) s_shift[tid] = shift_of(a.sine, a.seed, c0 + tid, side);
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // this round's keystream of the owned rows (independent of the previous round)
-  uint4 ks[kScatterCh];
-#pragma unroll
-  for (int t = 0; t < kScatterCh; ++t) {
-    const uint32_t q = tid + uint32_t(t) * blockDim.x;
-    ks[t] = make_uint4(0, 0, 0, 0);
-    if (q < units) {
-      const uint32_t i = q / upr, u = q - i * upr, row = c0 + i, b = row / a.rows;
-      uint64_t kq = a.pos + uint64_t(row - b * a.rows) * RB + 16u * u;
-      kq -= kq >= a.ring_bytes ? a.ring_bytes : 0;
-      RCHECK(kq + 16 <= a.ring_bytes && (kq & 15) == 0 && b < a.n);
-      ks[t] = __ldcs(reinterpret_cast<const uint4*>(a.ring + uint64_t(b) * a.ring_bytes + kq));
-    }
-  }
-  __syncthreads();
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous round wrote src
-  if (tid == 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(T * RB)
-                 : "memory");
-    for (uint32_t i = 0; i < T; ++i)
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              su32(sm) + i * a.rs),
-          "l"(a.src + uint64_t(c0 + i) * RB), "r"(RB), "r"(mb)
-          : "memory");
-  }
-  // the byte before each row's first byte: the previous row's last byte, or
-  // at a band start the next band's recovered last byte (engine.cpp:271-276)
-  if (tid < T) {
-    const uint32_t row = c0 + tid, b = row / a.rows;
-    uint32_t v = 0x100u;  // marker: row tid-1's last byte, from shared memory
-    if (row == b * a.rows) {
-      const uint32_t nbd = b + 1 == a.n ? 0 : b + 1;
-      const uint64_t last = (uint64_t(nbd) + 1) * a.region - 1;
-      uint64_t kq = a.pos + a.region - 1;
-      kq %= a.ring_bytes;
-      const uint32_t bl = a.ring[uint64_t(nbd) * a.ring_bytes + kq];
-      v = ((bl ^ a.src[last] ^ a.src[last - 1]) - bl) & 0xFFu;
-    } else if (tid == 0) {
-      v = a.src[uint64_t(row) * RB - 1];
-    }
-    s_prev[tid] = v;
-  }
-  mbar_wait(mb, 0);
-  __syncthreads();
-  // inverse diffusion: every unit read, then written back in place
-  uint4 d[kScatterCh];
-#pragma unroll
-  for (int t = 0; t < kScatterCh; ++t) {
-    const uint32_t q = tid + uint32_t(t) * blockDim.x;
-    d[t] = make_uint4(0, 0, 0, 0);
-    if (q < units) {
-      const uint32_t i = q / upr, u = q - i * upr;
-      const uint32_t P = su32(sm) + i * a.rs + 16u * u;
-      uint4 c;
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w)
-                   : "r"(P));
-      uint32_t pb;
-      if (u) {
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(pb) : "r"(P - 1u));
-      } else {
-        pb = s_prev[i];
-        if (pb == 0x100u)
-          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(pb) : "r"(su32(sm) + (i - 1u) * a.rs + RB - 1u));
-      }
-      d[t].x = inv_word(c.x, (c.x << 8) | pb, ks[t].x);
-      d[t].y = inv_word(c.y, __funnelshift_l(c.x, c.y, 8), ks[t].y);
-      d[t].z = inv_word(c.z, __funnelshift_l(c.y, c.z, 8), ks[t].z);
-      d[t].w = inv_word(c.w, __funnelshift_l(c.z, c.w, 8), ks[t].w);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < kScatterCh; ++t) {
-    const uint32_t q = tid + uint32_t(t) * blockDim.x;
-    if (q < units) {
-      const uint32_t i = q / upr, u = q - i * upr;
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(su32(sm) + i * a.rs + 16u * u),
-                   "r"(d[t].x), "r"(d[t].y), "r"(d[t].z), "r"(d[t].w)
-                   : "memory");
-    }
-  }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __syncthreads();
-  // scatter: a group of T lanes per output row, lane i = pixel i of the run
-  const uint32_t lane = tid & 31u, i = lane % T, gpw = 32u / T;
-  const uint32_t si = s_shift[i], rowb = su32(sm) + i * a.rs;
-  const uint32_t run = 3u * T;
-  for (uint32_t ar = (tid >> 5) * gpw + lane / T; ar < side; ar += (blockDim.x >> 5) * gpw) {
-    uint32_t o0 = c0 + side - ar;
-    o0 -= o0 >= side ? side : 0u;
-    uint32_t o = o0 + i;
-    o -= o >= side ? side : 0u;
-    uint32_t beta = o + si;
-    beta -= beta >= side ? side : 0u;
-    const uint32_t sa = rowb + 3u * beta;
-    uint32_t w0, w1;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(sa & ~3u));
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w1) : "r"((sa & ~3u) + 4u));
-    const uint32_t pv = __funnelshift_r(w0, w1, sa << 3) & 0xFFFFFFu;
-    // word i of the run: run bytes r0 .. r0+3, r0 = 4i - m (m = start mod 4)
-    const uint32_t s = 3u * o0, m = s & 3u;
-    const int r0 = int(4u * i) - int(m);
-    const int p0 = r0 >= 0 ? r0 / 3 : -1;
-    const uint32_t v0 = __shfl_sync(0xFFFFFFFFu, pv, p0 < 0 ? 0 : p0, T);
-    const uint32_t v1 = __shfl_sync(0xFFFFFFFFu, pv, min(p0 + 1, int(T) - 1), T);
-    const uint64_t u = uint64_t(p0 < 0 ? 0u : v0) | (uint64_t(v1) << 24);
-    const uint32_t word = uint32_t(u >> (8 * (r0 - 3 * p0)));
-    uint8_t* const grow = a.dst + uint64_t(ar) * RB;
-    if (o0 + T <= side) {
-      const uint32_t nw = (m + run + 3u) >> 2;
-      if (i < nw) {
-        if (r0 >= 0 && uint32_t(r0) + 4u <= run) {
-          RCHECK(s - m + 4u * i + 4u <= RB);
-          *reinterpret_cast<uint32_t*>(grow + s - m + 4u * i) = word;
-        } else {
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const int r = r0 + bb;
-            if (r >= 0 && r < int(run)) grow[s + uint32_t(r)] = uint8_t(word >> (8 * bb));
-          }
-        }
-      }
-    } else {  // the run wraps at the row end: per pixel
-      RCHECK(3u * o + 3u <= RB);
-      grow[3u * o] = uint8_t(pv);
-      grow[3u * o + 1u] = uint8_t(pv >> 8);
-      grow[3u * o + 2u] = uint8_t(pv >> 16);
-    }
-  }
-}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1018,44 +841,7 @@ bool plan_rows_decrypt(const Geom& g, RowPlan& p) {
   return true;
 }
 
-static void rows_check(const char* what);
-
-// K3x: T cipher rows per CTA (T divides 16, so it divides side), threads so
-// that each does at most kScatterCh 16-byte units of the diffusion pass.
-bool plan_rows_scatter(const Geom& g, uint32_t& T, uint32_t& threads, size_t& smem) {
-  if (g.side % 16 || g.frame_bytes >= (uint64_t(1) << 32) || g.rows == 0) return false;
-  T = 8;
-  if (const char* e = std::getenv("CVE_B200_SCATTER_T")) T = uint32_t(std::atoi(e));
-  if (T != 4 && T != 8 && T != 16) return false;
-  const uint32_t RB = 3 * g.side, units = T * (RB / 16);
-  threads = ((units + kScatterCh - 1) / kScatterCh + 31) / 32 * 32;
-  threads = std::max(threads, 64u);
-  smem = size_t(T) * (RB + 16);
-  return threads <= 1024 && smem <= 200 * 1024;
-}
-
-void launch_decrypt_round_scatter(const Geom& g, uint32_t T, uint32_t threads, size_t smem,
-                                  const uint8_t* src, uint8_t* dst, KsWindow ks,
-                                  const double* sine, uint32_t seed, cudaStream_t s, bool pdl) {
-  const ScatterArgs a{src, dst, ks.ring, ks.ring_bytes, ks.pos, g.region, sine, seed,
-                      g.side, g.n, g.rows, T, 3 * g.side + 16};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g.side / T);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = (pdl && !std::getenv("CVE_B200_NO_PDL")) ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_decrypt_round_scatter, a);
-  rows_check("decrypt_round_scatter");
-}
-
 void configure_rows_kernels() {
-  cudaFuncSetAttribute(k_decrypt_round_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       200 * 1024);
   cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
   cudaFuncSetAttribute(k_encrypt_round_rows<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

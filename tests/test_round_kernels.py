@@ -104,23 +104,3 @@ def test_k2r_ring_wrap_many_frames():
     got = frames.copy()
     cve.Cipher(key, n, r).encrypt_frames(got)
     assert np.array_equal(got, want)
-
-
-@pytest.mark.parametrize("side,n,r", GEOMS)
-def test_inverse_rounds_k3x(side, n, r):
-    # K3x (scatter form): oracle ciphertext decrypted back on consecutive
-    # frames of one handle, a LASM key, and every run length T
-    with env(CVE_B200_SCATTER="1"):
-        key, frames, ct = encrypt_vs_oracle(side, n, r, side * 37 + n + r)
-        d = cve.Cipher(key, n, r)
-        for t in range(len(frames)):
-            d.decrypt_frame(ct[t])
-        assert np.array_equal(ct, frames)
-        key = synth.det_key_lasm(side + n + r + 3)
-        frames = rand_frames(side, 2, side + 9)
-        for T in ("4", "8", "16"):
-            with env(CVE_B200_SCATTER_T=T):
-                ct = frames.copy()
-                cve.Cipher(key, n, r).encrypt_frames(ct)
-                cve.Cipher(key, n, r).decrypt_frames(ct)
-                assert np.array_equal(ct, frames), T
