@@ -181,6 +181,86 @@ typedef struct cve_crop_block {
 CVE_B200_API cve_status cve_crop_file(const char* in_path, const char* out_path,
                                       const cve_crop_block* blocks, size_t block_count);
 
+/* ---- the reference's benchmark and sweep entry points (cve.h:153-206) ---
+ * Same option structs (0 / NULL -> the reference's defaults), the same CSV
+ * schemas (bench.cpp:111-123, 165-184, 233-257, 303-315) and status codes,
+ * run on this engine.  *csv_out is malloc'd: free with cve_string_free. */
+
+/* Same layout as the reference (cve.h:155-161). */
+typedef struct cve_bench_bytegen_options {
+  const char* key_hex;          /* NULL -> fresh key of map_kind */
+  cve_map_kind map_kind;
+  const uint32_t* worker_counts;
+  size_t worker_count_len;      /* 0 -> {1,2,4,8} */
+  uint64_t iterations;          /* map iterations in total, 0 -> 50000000 */
+} cve_bench_bytegen_options;
+
+/* replaces cve.h:163-164 ("bench bytegen on K1").  One
+ * CSV row per worker count: `iterations` generator iterations in total over
+ * the workers' generators advancing together on the GPU (derivation, warm-up
+ * and allocation outside the timed window; the bytes stay on the device). */
+CVE_B200_API cve_status cve_bench_bytegen(const cve_bench_bytegen_options* options,
+                                          char** csv_out);
+
+/* Same layout as the reference (cve.h:166-174).  `serial` is accepted and
+ * ignored, like `parallel` of cve_cipher_create. */
+typedef struct cve_bench_phases_options {
+  const char* key_hex;
+  cve_map_kind map_kind;
+  uint32_t side;     /* 0 -> 960 */
+  uint32_t workers;  /* 0 -> 8 */
+  uint32_t rounds;   /* 0 -> 5 */
+  uint32_t images;   /* 0 -> 100 */
+  int serial;
+} cve_bench_phases_options;
+
+/* replaces cve.h:176-177.  Confusion-only and diffusion-only transforms
+ * (reference Engine::transform, engine.cpp:302-307) of noise images; the two
+ * halves run as separate kernels here -- these are NOT the fused production
+ * rounds, whose time cve_bench_video reports.  Host-clock times; the
+ * diffusion columns include keystream generation, as in the reference. */
+CVE_B200_API cve_status cve_bench_phases(const cve_bench_phases_options* options,
+                                         char** csv_out);
+
+/* Same layout as the reference (cve.h:179-189). */
+typedef struct cve_bench_video_options {
+  const char* key_hex;
+  cve_map_kind map_kind;
+  const uint32_t* sides;
+  size_t side_len;   /* 0 -> {96,192,288,384,480,576,672,768} */
+  uint32_t workers;  /* 0 -> 8 */
+  uint32_t rounds;   /* 0 -> 5 */
+  uint32_t frames;   /* 0 -> 600 */
+  uint16_t fps;      /* 0 -> 20; realtime_ok means mean <= 1000/fps ms */
+  int serial;
+} cve_bench_video_options;
+
+/* replaces cve.h:191-192 (the reference's timing method, bench.cpp:186-231):
+ * per side, `frames` synchronous in-place frame encryptions of noise frames
+ * on host memory, each timed on the host clock.  bytegen_mean_ms = the
+ * generator kernels' device time per frame, confuse_mean_ms = the fused
+ * confusion+diffusion round kernels' device time per frame, diffuse_mean_ms
+ * = 0.000 (no separate diffusion pass exists to time). */
+CVE_B200_API cve_status cve_bench_video(const cve_bench_video_options* options,
+                                        char** csv_out);
+
+/* Same layout as the reference (cve.h:194-202). */
+typedef struct cve_sweep_options {
+  const char* key_hex;
+  cve_map_kind map_kind;
+  const char* input;    /* P6 plain image; NULL -> synthetic */
+  uint32_t synth_side;  /* 0 -> 512 */
+  uint32_t workers;     /* 0 -> 1 */
+  uint32_t max_rounds;  /* 0 -> 10 */
+  uint64_t seed;
+} cve_sweep_options;
+
+/* replaces cve.h:206.  Per-round NPCR/UACI under a one-byte plaintext change
+ * (diffusion rounds only) and plain-vs-scrambled correlation (confusion
+ * rounds only), rounds 0..max_rounds: deterministic, byte-identical to the
+ * reference's CSV for the same key, image and seed. */
+CVE_B200_API cve_status cve_sweep_rounds(const cve_sweep_options* options, char** csv_out);
+
 /* ---- additive: batched / device-resident / introspection ---------------- */
 
 /* Additive (row f4 on resident frames): the analysis reductions of a

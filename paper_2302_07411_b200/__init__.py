@@ -68,6 +68,35 @@ class CropBlock(C.Structure):
     _fields_ = [("x", C.c_uint32), ("y", C.c_uint32), ("side", C.c_uint32), ("fill", C.c_uint8)]
 
 
+class BenchBytegenOptions(C.Structure):
+    """cve_bench_bytegen_options (reference cve.h:155-161)."""
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int),
+                ("worker_counts", C.POINTER(C.c_uint32)), ("worker_count_len", C.c_size_t),
+                ("iterations", C.c_uint64)]
+
+
+class BenchPhasesOptions(C.Structure):
+    """cve_bench_phases_options (reference cve.h:166-174)."""
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int), ("side", C.c_uint32),
+                ("workers", C.c_uint32), ("rounds", C.c_uint32), ("images", C.c_uint32),
+                ("serial", C.c_int)]
+
+
+class BenchVideoOptions(C.Structure):
+    """cve_bench_video_options (reference cve.h:179-189)."""
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int),
+                ("sides", C.POINTER(C.c_uint32)), ("side_len", C.c_size_t),
+                ("workers", C.c_uint32), ("rounds", C.c_uint32), ("frames", C.c_uint32),
+                ("fps", C.c_uint16), ("serial", C.c_int)]
+
+
+class SweepOptions(C.Structure):
+    """cve_sweep_options (reference cve.h:194-202)."""
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int), ("input", C.c_char_p),
+                ("synth_side", C.c_uint32), ("workers", C.c_uint32),
+                ("max_rounds", C.c_uint32), ("seed", C.c_uint64)]
+
+
 class Stats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("keystream_iters", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("prbg_launches", C.c_uint64),
@@ -123,6 +152,10 @@ def _load() -> C.CDLL:
         "cve_analyze": (C.c_int, [C.POINTER(AnalyzeOptions), C.POINTER(vp)]),
         "cve_add_noise_file": (C.c_int, [C.c_char_p, C.c_char_p, C.c_double, C.c_uint64]),
         "cve_crop_file": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(CropBlock), C.c_size_t]),
+        "cve_bench_bytegen": (C.c_int, [C.POINTER(BenchBytegenOptions), C.POINTER(vp)]),
+        "cve_bench_phases": (C.c_int, [C.POINTER(BenchPhasesOptions), C.POINTER(vp)]),
+        "cve_bench_video": (C.c_int, [C.POINTER(BenchVideoOptions), C.POINTER(vp)]),
+        "cve_sweep_rounds": (C.c_int, [C.POINTER(SweepOptions), C.POINTER(vp)]),
         "cve_frame_stats_device": (C.c_int, [vp, vp, C.c_uint32, vp, vp, vp]),
         "cve_padded_side": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]),
         "cve_cipher_encrypt_frames_wh": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]),
@@ -284,6 +317,57 @@ def crop_file(in_path: str, out_path: str, blocks) -> None:
     arr = (CropBlock * max(1, len(blocks)))(*[CropBlock(*b) for b in blocks])
     _check(lib.cve_crop_file(in_path.encode(), out_path.encode(), arr if blocks else None,
                              len(blocks)))
+
+
+def _csv_call(fn, options) -> str:
+    out = C.c_void_p()
+    _check(fn(C.byref(options), C.byref(out)))
+    try:
+        return C.string_at(out).decode()
+    finally:
+        lib.cve_string_free(out)
+
+
+def _u32_array(values):
+    vals = list(values or [])
+    return ((C.c_uint32 * len(vals))(*vals) if vals else None), len(vals)
+
+
+def bench_bytegen(key_hex=None, map_kind: int = CVE_MAP_PLCM, worker_counts=None,
+                  iterations: int = 0) -> str:
+    """Reference cve_bench_bytegen on the GPU generator: one CSV row per worker
+    count (default 1, 2, 4, 8), `iterations` map iterations in total."""
+    arr, n = _u32_array(worker_counts)
+    o = BenchBytegenOptions(_as_key(key_hex) if key_hex is not None else None, map_kind, arr, n,
+                            iterations)
+    return _csv_call(lib.cve_bench_bytegen, o)
+
+
+def bench_phases(key_hex=None, map_kind: int = CVE_MAP_PLCM, side: int = 0, workers: int = 0,
+                 rounds: int = 0, images: int = 0) -> str:
+    """Reference cve_bench_phases: confusion-only and diffusion-only transforms."""
+    o = BenchPhasesOptions(_as_key(key_hex) if key_hex is not None else None, map_kind, side,
+                           workers, rounds, images, 0)
+    return _csv_call(lib.cve_bench_phases, o)
+
+
+def bench_video(key_hex=None, map_kind: int = CVE_MAP_PLCM, sides=None, workers: int = 0,
+                rounds: int = 0, frames: int = 0, fps: int = 0) -> str:
+    """Reference cve_bench_video (its timing method): per-frame synchronous calls."""
+    arr, n = _u32_array(sides)
+    o = BenchVideoOptions(_as_key(key_hex) if key_hex is not None else None, map_kind, arr, n,
+                          workers, rounds, frames, fps, 0)
+    return _csv_call(lib.cve_bench_video, o)
+
+
+def sweep_rounds(key_hex=None, map_kind: int = CVE_MAP_PLCM, input_path: str = None,
+                 synth_side: int = 0, workers: int = 0, max_rounds: int = 0,
+                 seed: int = 0) -> str:
+    """Reference cve_sweep_rounds: per-round NPCR/UACI and confusion correlation."""
+    o = SweepOptions(_as_key(key_hex) if key_hex is not None else None, map_kind,
+                     input_path.encode() if input_path else None, synth_side, workers,
+                     max_rounds, seed)
+    return _csv_call(lib.cve_sweep_rounds, o)
 
 
 def frame_stats_device(frame_ptr: int, side: int, hist_ptr: int, second_ptr: int = 0,

@@ -18,6 +18,7 @@
 #include "engine.hpp"
 #include "fileio.hpp"
 #include "files.hpp"
+#include "harness.hpp"
 #include "keying.hpp"
 
 struct cve_cipher {
@@ -286,6 +287,104 @@ cve_status cve_analyze(const cve_analyze_options* options, char** text_out) {
     if (out == nullptr) throw std::bad_alloc();
     std::memcpy(out, text.c_str(), text.size() + 1);
     *text_out = out;
+  });
+}
+
+// capi.cpp:417-505: options and csv_out checked first, then the key (NULL ->
+// a fresh key of map_kind), then the defaults.
+namespace {
+cveb::Key harness_key(const char* key_hex, cve_map_kind fallback) {
+  if (key_hex != nullptr) return cveb::parse_key(key_hex);
+  require(fallback == CVE_MAP_PLCM || fallback == CVE_MAP_LASM, "unknown map kind");
+  return cveb::fresh_key(static_cast<cveb::MapKind>(fallback));
+}
+char* c_string(const std::string& text) {
+  char* out = static_cast<char*>(std::malloc(text.size() + 1));
+  if (out == nullptr) throw std::bad_alloc();
+  std::memcpy(out, text.c_str(), text.size() + 1);
+  return out;
+}
+}  // namespace
+
+cve_status cve_bench_bytegen(const cve_bench_bytegen_options* options, char** csv_out) {
+  return guarded([&] {
+    require(options != nullptr, "options is null");
+    require(csv_out != nullptr, "csv_out is null");
+    const cveb::Key key = harness_key(options->key_hex, options->map_kind);
+    std::vector<uint32_t> counts = {1, 2, 4, 8};
+    if (options->worker_count_len != 0) {
+      require(options->worker_counts != nullptr, "worker_counts is null");
+      counts.assign(options->worker_counts, options->worker_counts + options->worker_count_len);
+    }
+    const uint64_t iterations = options->iterations != 0 ? options->iterations : 50000000;
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    *csv_out = c_string(cveb::bytegen_table(key, counts, iterations, dev));
+  });
+}
+
+cve_status cve_bench_phases(const cve_bench_phases_options* options, char** csv_out) {
+  return guarded([&] {
+    require(options != nullptr, "options is null");
+    require(csv_out != nullptr, "csv_out is null");
+    const cveb::Key key = harness_key(options->key_hex, options->map_kind);
+    const uint32_t side = options->side != 0 ? options->side : 960;
+    const uint32_t workers = options->workers != 0 ? options->workers : 8;
+    const uint32_t rounds = options->rounds != 0 ? options->rounds : 5;
+    const uint32_t images = options->images != 0 ? options->images : 100;
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    *csv_out = c_string(cveb::phases_table(key, side, workers, rounds, images, dev));
+  });
+}
+
+cve_status cve_bench_video(const cve_bench_video_options* options, char** csv_out) {
+  return guarded([&] {
+    require(options != nullptr, "options is null");
+    require(csv_out != nullptr, "csv_out is null");
+    const cveb::Key key = harness_key(options->key_hex, options->map_kind);
+    std::vector<uint32_t> sides = {96, 192, 288, 384, 480, 576, 672, 768};
+    if (options->side_len != 0) {
+      require(options->sides != nullptr, "sides is null");
+      sides.assign(options->sides, options->sides + options->side_len);
+    }
+    const uint32_t workers = options->workers != 0 ? options->workers : 8;
+    const uint32_t rounds = options->rounds != 0 ? options->rounds : 5;
+    const uint32_t frames = options->frames != 0 ? options->frames : 600;
+    const uint16_t fps = options->fps != 0 ? options->fps : 20;
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    *csv_out = c_string(cveb::video_table(key, sides, workers, rounds, frames, fps, dev));
+  });
+}
+
+cve_status cve_sweep_rounds(const cve_sweep_options* options, char** csv_out) {
+  return guarded([&] {
+    require(options != nullptr, "options is null");
+    require(csv_out != nullptr, "csv_out is null");
+    const cveb::Key key = harness_key(options->key_hex, options->map_kind);
+    const uint32_t workers = options->workers != 0 ? options->workers : 1;
+    const uint32_t max_rounds = options->max_rounds != 0 ? options->max_rounds : 10;
+    cveb::HostFrame plain;
+    if (options->input != nullptr) {  // load_ppm: any P6, padded to a square (image_io.cpp:110-113)
+      const std::vector<uint8_t> data = cveb::read_whole_file(options->input);
+      const cveb::P6Image img = cveb::p6_parse(data.data(), data.size());
+      plain.side = cveb::padded_side_of(img.width, img.height, workers);
+      plain.orig_width = img.width;
+      plain.orig_height = img.height;
+      plain.px.assign(size_t(plain.side) * plain.side * 3, 0);
+      for (uint32_t r = 0; r < img.height; ++r)
+        std::memcpy(plain.px.data() + size_t(r) * plain.side * 3,
+                    img.rgb.data() + size_t(r) * img.width * 3, size_t(img.width) * 3);
+    } else {
+      const uint32_t side = options->synth_side != 0 ? options->synth_side : 512;
+      if (side % workers != 0)
+        cveb::raise(cveb::Errc::mismatch, "synthetic side is not divisible by the worker count");
+      plain = cveb::natural_frame(side, options->seed);
+    }
+    const int dev = current_device();
+    DeviceScope scope(dev);
+    *csv_out = c_string(cveb::sweep_table(key, plain, workers, max_rounds, options->seed, dev));
   });
 }
 

@@ -1915,19 +1915,34 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
     return;
   }
   // generic path: scratch holds y (frame_bytes) followed by chunk aggregates
-  const uint64_t pix = uint64_t(g.side) * g.side;
-  k_gather<<<uint32_t((pix + 255) / 256), 256, 0, s>>>(src, scratch, shift, g.side);
-  check_launch("gather");
-  const uint32_t nch = uint32_t((g.region + kGenChunk - 1) / kGenChunk);
+  launch_confuse_only(g, src, scratch, shift, s, launches);
   uint32_t* agg = reinterpret_cast<uint32_t*>(scratch + ((g.frame_bytes + 255) & ~uint64_t(255)));
-  GenArgs a{scratch, dst, ks.ring, ks.ring_bytes, ks.pos, g.region, g.n, nch, agg};
+  launch_diffuse_only(g, scratch, dst, ks, agg, s, launches);
+}
+
+// Confusion alone (confuse_rows, engine.cpp:32-47): dst = the permuted src.
+void launch_confuse_only(const Geom& g, const uint8_t* src, uint8_t* dst, const int32_t* shift,
+                         cudaStream_t s, uint64_t* launches) {
+  const uint64_t pix = uint64_t(g.side) * g.side;
+  k_gather<<<uint32_t((pix + 255) / 256), 256, 0, s>>>(src, dst, shift, g.side);
+  check_launch("gather");
+  ++*launches;
+}
+
+// Diffusion alone (diffuse_region per band, engine.cpp:232-244): dst = the
+// band-wise chained rewrite of y with the round's keystream window; agg holds
+// n * ceil(region / 4096) chunk aggregates.
+void launch_diffuse_only(const Geom& g, const uint8_t* y, uint8_t* dst, KsWindow ks,
+                         uint32_t* agg, cudaStream_t s, uint64_t* launches) {
+  const uint32_t nch = uint32_t((g.region + kGenChunk - 1) / kGenChunk);
+  GenArgs a{y, dst, ks.ring, ks.ring_bytes, ks.pos, g.region, g.n, nch, agg};
   k_gen_aggregate<<<dim3(nch, g.n), 256, 0, s>>>(a);
   check_launch("gen_aggregate");
   k_gen_prefix<<<(g.n + 127) / 128, 128, 0, s>>>(a);
   check_launch("gen_prefix");
   k_gen_scan<<<dim3(nch, g.n), 256, 0, s>>>(a);
   check_launch("gen_scan");
-  *launches += 4;
+  *launches += 3;
 }
 
 // Slot-staged inverse round: tile rows T in [6, 15] (<= side) minimising the

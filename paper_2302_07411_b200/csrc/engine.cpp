@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <atomic>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1204,6 +1205,90 @@ void Engine::run_device(uint8_t* d_px, uint32_t side, uint32_t count,
   ck(cudaStreamWaitEvent(user, done, 0), "join user stream");
 }
 
+// Reference Engine::transform (engine.cpp:302-307 -> forward, 207-250): seed
+// first, then the geometry check, the streams only when diffusion is on, and
+// per round the confusion half (a -> b, swap), the diffusion half (a -> b,
+// swap; s_d from the pre-diffusion snapshot a), then the callback.
+void Engine::transform_host(uint8_t* px, uint32_t side, uint32_t rounds, bool confusion,
+                            bool diffusion,
+                            const std::function<void(uint32_t, const uint8_t*)>& per_round,
+                            PhaseMs* t) {
+  NvtxRange nvtx("cve: transform");
+  if (!shards_.empty())
+    raise(Errc::invalid_argument, "sharded handle: transform runs on single-device handles");
+  draw_and_check(side, 1);
+  const uint32_t seed = coord_.next_seed();
+  const Geom g = geometry(side);
+  CipherCtx& c = *local_;
+  c.ensure_buffers(g, 0);
+  using Clock = std::chrono::steady_clock;
+  const auto since = [](Clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - a).count();
+  };
+  const uint64_t need = diffusion ? uint64_t(rounds) * g.region : 0;
+  uint64_t lo = 0;
+  if (need) {
+    const auto t0 = Clock::now();
+    ensure_ring(need);
+    lo = cons_;
+    cons_ += need;
+    gen_until(lo + need);
+    if (cudaEvent_t ge = gen_event_covering(lo + need))
+      ck(cudaStreamWaitEvent(c.s_work, ge, 0), "wait keystream");
+    if (t) {
+      ck(cudaStreamSynchronize(c.s_work), "keystream");
+      t->bytegen_ms += since(t0);
+    }
+  }
+  uint8_t* a = c.scratch[0];
+  uint8_t* b = c.scratch[1];
+  const uint64_t agg_off = round_up(g.frame_bytes, 256);
+  ck(cudaMemcpyAsync(a, px, g.frame_bytes, cudaMemcpyHostToDevice, c.s_work), "H2D");
+  if (confusion) {
+    launch_shift_table(c.sine_for(side), seed, c.d_shift, side, c.s_work);
+    ++st_.kernel_launches;
+  }
+  if (t) ck(cudaStreamSynchronize(c.s_work), "transform input");
+  std::vector<uint8_t> state(per_round ? g.frame_bytes : 0);
+  for (uint32_t k = 0; k < rounds; ++k) {
+    if (confusion) {
+      const auto t0 = Clock::now();
+      launch_confuse_only(g, a, b, c.d_shift, c.s_work, &st_.kernel_launches);
+      std::swap(a, b);
+      if (t) {
+        ck(cudaStreamSynchronize(c.s_work), "confusion");
+        t->confuse_ms += since(t0);
+      }
+    }
+    if (diffusion) {
+      const auto t0 = Clock::now();
+      const KsWindow ks{ring_, ring_bytes_, (lo + uint64_t(k) * g.region) % ring_bytes_};
+      launch_diffuse_only(g, a, b, ks, reinterpret_cast<uint32_t*>(b + agg_off), c.s_work,
+                          &st_.kernel_launches);
+      std::swap(a, b);
+      if (t) {
+        ck(cudaStreamSynchronize(c.s_work), "diffusion");
+        t->diffuse_ms += since(t0);
+      }
+    }
+    if (per_round) {
+      ck(cudaMemcpyAsync(state.data(), a, g.frame_bytes, cudaMemcpyDeviceToHost, c.s_work),
+         "D2H");
+      ck(cudaStreamSynchronize(c.s_work), "transform round");
+      per_round(k + 1, state.data());
+    }
+  }
+  ck(cudaMemcpyAsync(px, a, g.frame_bytes, cudaMemcpyDeviceToHost, c.s_work), "D2H");
+  cudaEvent_t done = c.events.get();
+  ck(cudaEventRecord(done, c.s_work), "cudaEventRecord");
+  if (need) {
+    consumers_.push_back(Consumer{lo, lo + need, done, &c.events});  // read the ring
+  } else {
+    c.events.put(done);
+  }
+  ck(cudaStreamSynchronize(c.s_work), "transform");
+}
+
 void Engine::run_device_sharded(uint8_t* const* shard_px, uint32_t side, uint32_t count,
                                 bool decrypt, const cudaStream_t* users) {
   NvtxRange nvtx("cve: frames (device-resident, sharded)");
@@ -1425,6 +1510,20 @@ void KeystreamSource::next(uint8_t* host, uint64_t bytes) {
     carry_ += take;
     got += take;
   }
+}
+
+void KeystreamSource::burn(uint64_t iters) {
+  DeviceScope scope(dev_);
+  const uint64_t cb = chunk_bytes();
+  while (iters > 0) {
+    const uint32_t now = uint32_t(std::min<uint64_t>(round_up(iters, 8), gen_.max_iters()));
+    gen_.chain(slot_, now, s_);
+    gen_.emit(slot_, d_buf_, cb, 0, now, s_);
+    slot_ ^= 1;
+    iters -= std::min<uint64_t>(iters, now);
+  }
+  carry_ = have_ = 0;
+  ck(cudaStreamSynchronize(s_), "keystream");
 }
 
 }  // namespace cveb

@@ -33,6 +33,7 @@
 
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <utility>
@@ -237,6 +238,20 @@ class Engine {
   // (entries may be null: the legacy default stream of that device).
   void run_device_sharded(uint8_t* const* shard_px, uint32_t side, uint32_t count, bool decrypt,
                           const cudaStream_t* users);
+  // The reference's Engine::transform (engine.cpp:302-307, forward 207-250):
+  // one frame in host memory, in place, through `rounds` rounds with
+  // confusion and/or diffusion switched off -- the two halves of the generic
+  // round as separate kernels, not the fused production rounds.  Draws one
+  // confusion seed (and, with diffusion, rounds * region stream bytes per
+  // worker) like a frame call.  per_round(k, state) sees the frame after
+  // round k = 1..rounds.  `t` (optional) receives host-clock phase times.
+  struct PhaseMs {
+    double bytegen_ms = 0, confuse_ms = 0, diffuse_ms = 0;
+  };
+  void transform_host(uint8_t* px, uint32_t side, uint32_t rounds, bool confusion,
+                      bool diffusion,
+                      const std::function<void(uint32_t, const uint8_t*)>& per_round,
+                      PhaseMs* t);
   void synchronize();
   void peek(uint32_t worker, uint8_t* out, size_t len);
   void prefetch(uint64_t bytes);
@@ -338,6 +353,10 @@ class KeystreamSource {
   KeystreamSource& operator=(const KeystreamSource&) = delete;
   uint64_t chunk_bytes() const { return uint64_t(gen_.max_iters()) * gen_.bytes_per_iter(); }
   void next(uint8_t* host, uint64_t bytes);
+  // Advances every worker by `iters` iterations (rounded up to a multiple of
+  // 8) and drops the bytes on the device: generation alone, for timing.
+  // Not to be mixed with next() on one source.
+  void burn(uint64_t iters);
 
  private:
   void release() noexcept;

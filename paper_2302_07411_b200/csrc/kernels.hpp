@@ -140,6 +140,16 @@ void launch_encrypt_round(const EncPlan& plan, const Geom& g,
                           const int32_t* shift, uint8_t* scratch,
                           cudaStream_t s, uint64_t* launches);
 
+// The two halves of the generic forward round on their own (the reference's
+// Engine::transform with confusion or diffusion switched off,
+// engine.cpp:207-250): the permutation src -> dst, and the band-wise chained
+// rewrite y -> dst with one round's keystream window (agg: n * ceil(region /
+// 4096) words of scratch).
+void launch_confuse_only(const Geom& g, const uint8_t* src, uint8_t* dst, const int32_t* shift,
+                         cudaStream_t s, uint64_t* launches);
+void launch_diffuse_only(const Geom& g, const uint8_t* y, uint8_t* dst, KsWindow ks,
+                         uint32_t* agg, cudaStream_t s, uint64_t* launches);
+
 // K6: all `rounds` forward rounds of one frame (in place in `buf`) in one
 // thread-block cluster, when the frame fits one (side % 16 == 0, up to
 // ~768^2); false: not applicable, nothing launched.

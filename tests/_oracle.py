@@ -228,3 +228,75 @@ def ref_crop_file(in_path, out_path, blocks):
     arr = (RefCropBlock * max(1, len(blocks)))(*[RefCropBlock(*b) for b in blocks])
     return L.cve_crop_file(in_path.encode(), out_path.encode(), arr if blocks else None,
                            len(blocks))
+
+
+# ---- the reference's bench / sweep entry points (cve.h:153-206) -------------
+
+class RefBytegenOptions(C.Structure):
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int),
+                ("worker_counts", C.POINTER(C.c_uint32)), ("worker_count_len", C.c_size_t),
+                ("iterations", C.c_uint64)]
+
+
+class RefPhasesOptions(C.Structure):
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int), ("side", C.c_uint32),
+                ("workers", C.c_uint32), ("rounds", C.c_uint32), ("images", C.c_uint32),
+                ("serial", C.c_int)]
+
+
+class RefVideoOptions(C.Structure):
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int),
+                ("sides", C.POINTER(C.c_uint32)), ("side_len", C.c_size_t),
+                ("workers", C.c_uint32), ("rounds", C.c_uint32), ("frames", C.c_uint32),
+                ("fps", C.c_uint16), ("serial", C.c_int)]
+
+
+class RefSweepOptions(C.Structure):
+    _fields_ = [("key_hex", C.c_char_p), ("map_kind", C.c_int), ("input", C.c_char_p),
+                ("synth_side", C.c_uint32), ("workers", C.c_uint32),
+                ("max_rounds", C.c_uint32), ("seed", C.c_uint64)]
+
+
+def _ref_csv(name, options):
+    """(status, csv) from one of the reference's csv_out entry points."""
+    L = Reference.load()
+    fn = getattr(L, name)
+    fn.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    fn.restype = C.c_int
+    L.cve_string_free.argtypes = [C.c_void_p]
+    out = C.c_void_p()
+    st = fn(C.byref(options) if options is not None else None, C.byref(out))
+    if st:
+        return st, None
+    text = C.string_at(out).decode()
+    L.cve_string_free(out)
+    return 0, text
+
+
+def _u32s(values):
+    vals = list(values or [])
+    return ((C.c_uint32 * len(vals))(*vals) if vals else None), len(vals)
+
+
+def ref_bench_bytegen(key_hex=None, map_kind=0, worker_counts=None, iterations=0):
+    arr, n = _u32s(worker_counts)
+    return _ref_csv("cve_bench_bytegen", RefBytegenOptions(
+        key_hex.encode() if key_hex else None, map_kind, arr, n, iterations))
+
+
+def ref_bench_phases(key_hex=None, map_kind=0, side=0, workers=0, rounds=0, images=0):
+    return _ref_csv("cve_bench_phases", RefPhasesOptions(
+        key_hex.encode() if key_hex else None, map_kind, side, workers, rounds, images, 0))
+
+
+def ref_bench_video(key_hex=None, map_kind=0, sides=None, workers=0, rounds=0, frames=0, fps=0):
+    arr, n = _u32s(sides)
+    return _ref_csv("cve_bench_video", RefVideoOptions(
+        key_hex.encode() if key_hex else None, map_kind, arr, n, workers, rounds, frames, fps, 0))
+
+
+def ref_sweep_rounds(key_hex=None, map_kind=0, input_path=None, synth_side=0, workers=0,
+                     max_rounds=0, seed=0):
+    return _ref_csv("cve_sweep_rounds", RefSweepOptions(
+        key_hex.encode() if key_hex else None, map_kind,
+        input_path.encode() if input_path else None, synth_side, workers, max_rounds, seed))
