@@ -58,6 +58,36 @@ int main(int argc, char** argv) {
     return 7;
   }
   cve_cipher_destroy(d);
+
+  /* the reference's sweep and bench entry points through its option structs */
+  cve_sweep_options sw;
+  memset(&sw, 0, sizeof sw);
+  sw.key_hex = key;
+  sw.synth_side = 32;
+  sw.workers = 2;
+  sw.max_rounds = 2;
+  sw.seed = 5;
+  char* csv = NULL;
+  if (cve_sweep_rounds(&sw, &csv) != CVE_OK || csv == NULL) return 8;
+  if (strncmp(csv, "round,npcr_r,", 13) != 0) return 9;
+  unsigned lines = 0;
+  for (const char* q = csv; *q; ++q) lines += *q == '\n';
+  cve_string_free(csv);
+  if (lines != 4) return 10; /* header + rounds 0..2 */
+  const uint32_t sides[1] = {32};
+  cve_bench_video_options bv;
+  memset(&bv, 0, sizeof bv);
+  bv.key_hex = key;
+  bv.sides = sides;
+  bv.side_len = 1;
+  bv.workers = 2;
+  bv.frames = 3;
+  csv = NULL;
+  if (cve_bench_video(&bv, &csv) != CVE_OK || csv == NULL) return 11;
+  if (strncmp(csv, "map,side,workers,rounds,frames,fps,", 35) != 0) return 12;
+  cve_string_free(csv);
+  sw.synth_side = 33; /* not divisible by 2 workers */
+  if (cve_sweep_rounds(&sw, &csv) != CVE_ERROR_MISMATCH) return 13;
   printf("ok %08x seeds=%llu\n", x, (unsigned long long)seeds);
   free(px);
   free(orig);
