@@ -258,6 +258,7 @@ def rows_measure(stream) -> dict:
     c = synth.CONFIGS["C4"]
     W, H, n = c["width"], c["height"], c["workers"]
     key = synth.config_key("C4")
+    side_c4 = synth.config_side("C4")
     nf = 24
     rows = {}
 
@@ -332,6 +333,35 @@ def rows_measure(stream) -> dict:
             f3["reference"] = {"value": nbytes / (time.perf_counter() - t0) / 1e6,
                                "unit": "MB/s", "cores": 1}
             f3["identical"] = blob(r3) == blob(o3)
+        # the reference's own bench entry points, both libraries: cve_bench_bytegen
+        # (64 workers) and cve_bench_video (its timing method, bench.cpp:186-231:
+        # synchronous per-frame calls on host memory) at the C4 geometry
+        from _oracle import ref_bench_bytegen, ref_bench_video
+
+        def table(csv):
+            lines = csv.strip().split("\n")
+            return [dict(zip(lines[0].split(","), ln.split(","))) for ln in lines[1:]]
+        its = 20_000_000
+        bg = table(cve.bench_bytegen(key, worker_counts=[n], iterations=its))[0]
+        f3["bench_bytegen"] = {"workers": n, "iterations": its,
+                               "throughput_mbps": float(bg["throughput_mbps"])}
+        bv = table(cve.bench_video(key, sides=[side_c4], workers=n, frames=40, fps=20))[0]
+        f3["bench_video"] = {"side": side_c4, "workers": n, "frames": 40,
+                             "total_mean_ms": float(bv["total_mean_ms"]),
+                             "throughput_mbps": float(bv["throughput_mbps"]),
+                             "bytegen_mean_ms": float(bv["bytegen_mean_ms"]),
+                             "rounds_mean_ms": float(bv["confuse_mean_ms"])}
+        if have_ref:
+            st, csv = ref_bench_bytegen(key, 0, [n], its)
+            if st == 0:
+                f3["bench_bytegen"]["reference_throughput_mbps"] = float(
+                    table(csv)[0]["throughput_mbps"])
+            st, csv = ref_bench_video(key, 0, [side_c4], n, 5, 12, 20)
+            if st == 0:
+                rv = table(csv)[0]
+                f3["bench_video"]["reference"] = {"frames": 12,
+                                                  "total_mean_ms": float(rv["total_mean_ms"]),
+                                                  "throughput_mbps": float(rv["throughput_mbps"])}
         rows["f3"] = f3
 
         side = synth.config_side("C4")
