@@ -22,7 +22,11 @@ workloads.synth and records:
   config geometries C1-C4 under a LASM key, and worker keystream digests.
   Also refreshes reference_unit.json (which holds the LASM unit goldens).
 
-Usage:  python tests/golden/make_golden.py [--full-clips | --lasm]   (needs oracle/_ref)
+* sweeps.json (--sweeps) -- the reference's cve_sweep_rounds CSV (per-round
+  NPCR/UACI and confusion correlation; bench.cpp:259-315) for a few keys,
+  sides, worker counts and seeds on its synthetic image.
+
+Usage:  python tests/golden/make_golden.py [--full-clips | --lasm | --sweeps]   (needs oracle/_ref)
 """
 from __future__ import annotations
 
@@ -271,6 +275,28 @@ def lasm_full_clips() -> None:
     print("wrote lasm_clips.json")
 
 
+SWEEP_CASES = [  # (key recipe, seed of the key, synth_side, workers, max_rounds, seed)
+    ("plcm", 31, 64, 2, 3, 9), ("plcm", 31, 96, 1, 5, 1234), ("plcm", 44, 120, 8, 4, 7),
+    ("lasm", 32, 64, 4, 3, 5), ("plcm", 45, 51, 3, 2, 77), ("plcm", 46, 256, 16, 6, 2024),
+    ("lasm", 47, 80, 5, 4, 1),
+]
+
+
+def sweeps() -> None:
+    from _oracle import ref_sweep_rounds
+    out = []
+    for kind, kseed, side, workers, rounds, seed in SWEEP_CASES:
+        key = synth.det_key_lasm(kseed) if kind == "lasm" else synth.det_key(kseed)
+        st, csv = ref_sweep_rounds(key, 0, None, side, workers, rounds, seed)
+        assert st == 0
+        out.append({"key": key, "synth_side": side, "workers": workers, "max_rounds": rounds,
+                    "seed": seed, "csv": csv})
+    with open(os.path.join(HERE, "sweeps.json"), "w") as fh:
+        json.dump({"source": "reference cve_sweep_rounds (oracle/_ref), synthetic image",
+                   "cases": out}, fh, indent=1)
+    print(f"sweeps.json: {len(out)} cases")
+
+
 def _frame_job(arg):
     name, t = arg
     return synth.config_frame(name, t)
@@ -283,5 +309,7 @@ if __name__ == "__main__":
         lasm_full_clips()
     elif "--lasm" in sys.argv:
         lasm()
+    elif "--sweeps" in sys.argv:
+        sweeps()
     else:
         main()
