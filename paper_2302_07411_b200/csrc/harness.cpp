@@ -251,8 +251,12 @@ std::string video_table(const Key& key, const std::vector<uint32_t>& sides, uint
     std::vector<uint8_t> work;
     const EngineStats before = engine.stats();
     for (uint32_t i = 0; i < frames; ++i) {
-      work = pool[i % pool.size()].px;  // the call is in place: a fresh plaintext each time
+      // The call is in place, so each frame needs a fresh plaintext: that
+      // copy is inside the window, like the reference's copy-in
+      // (engine.cpp:219).  Outside it, the generator's run-ahead would work
+      // during the copy and the mean would undercut the frame period.
       const auto t0 = Clock::now();
+      work = pool[i % pool.size()].px;
       engine.run_host(work.data(), side, 1, false);
       total.take(elapsed_ms(t0));
     }
