@@ -15,20 +15,21 @@ cases = [(4096, 1, 2), (4096, 256, 5), (5000, 8, 3), (6144, 512, 2), (8192, 64, 
 if len(sys.argv) > 1:
     cases = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
 bad = 0
+NF = int(os.environ.get('LARGE_FRAMES', '2'))
 for side, n, r in cases:
     key = synth.det_key(side + n)
-    f = np.random.default_rng(side).integers(0, 256, size=(2, side, side, 3), dtype=np.uint8)
+    f = np.random.default_rng(side).integers(0, 256, size=(NF, side, side, 3), dtype=np.uint8)
     want = f.copy()
     t0 = time.time()
     o = Oracle(key, n, r)
-    for t in range(2):
+    for t in range(NF):
         assert o.encrypt(want[t]) == 0
     o.close()
     t1 = time.time()
     got = f.copy()
     h = cve.Cipher(key, n, r)
-    h.encrypt_frame(got[0])
-    h.encrypt_frame(got[1])
+    for t in range(NF):
+        h.encrypt_frame(got[t])
     t2 = time.time()
     ok = np.array_equal(got, want)
     cve.Cipher(key, n, r).decrypt_frames(got)
