@@ -193,64 +193,15 @@ __device__ __forceinline__ double plcm_check_step(double x, const LaneConst& c, 
   const unsigned hi = unsigned(__double2hiint(y));
   const unsigned lo = unsigned(__double2loint(y));
   const unsigned ex = hi & 0x7FF00000u;
-  const double r = __fma_rn(-y, low ? c.p : c.q, num);
-  const double ulp = __hiloint2double(int(ex - (52u << 20)), 0);
-  const double thr = __dmul_rn(low ? c.hp : c.hq, ulp);
-  suspect |= (lo == 0u) | (lo == c.plo) | (ex < (53u << 20));
-  ok &= fabs(r) < thr;
-  return y;
-}
-
-// plcm_check_step with the case's CONSTANTS selected on the FMA pipe instead
-// of the ALU pipe: the verifier is bound by the ALU pipe (FSEL, LOP3, ISETP:
-// one warp instruction per 2 cycles), while IMAD issues on the FMA pipe.  A
-// constant pair (P for f < p, Q otherwise) is picked per 32-bit half as
-// Q + m * (P - Q) with m = 0 / 1 -- exact modulo 2^32 -- and m is hidden
-// from the compiler (it would turn the multiply back into a select).  The
-// numerator is f - (low ? 0 : p), the subtrahend picked the same way
-// (f - 0 == f), and the rounding threshold is den * ulp(y)/2 formed from den
-// (p/2 and q/2 are exact), so hp/hq need no select.  Same decision, same
-// suspect flags (the exponent floor is one higher: ulp(y)/2 must be normal).
-struct CaseSel {
-  uint32_t yh[2], yl[2], den[2];  // (P - Q) bit differences: low word, high word
-};
-__device__ __forceinline__ CaseSel make_case_sel(const LaneConst& c) {
-  CaseSel s;
-  s.yh[0] = uint32_t(__double2loint(c.yh_p)) - uint32_t(__double2loint(c.yh_q));
-  s.yh[1] = uint32_t(__double2hiint(c.yh_p)) - uint32_t(__double2hiint(c.yh_q));
-  s.yl[0] = uint32_t(__double2loint(c.yl_p)) - uint32_t(__double2loint(c.yl_q));
-  s.yl[1] = uint32_t(__double2hiint(c.yl_p)) - uint32_t(__double2hiint(c.yl_q));
-  s.den[0] = uint32_t(__double2loint(c.p)) - uint32_t(__double2loint(c.q));
-  s.den[1] = uint32_t(__double2hiint(c.p)) - uint32_t(__double2hiint(c.q));
-  return s;
-}
-__device__ __forceinline__ double pick(uint32_t m, double q, const uint32_t d[2]) {
-  const uint32_t lo = uint32_t(__double2loint(q)) + m * d[0];
-  const uint32_t hi = uint32_t(__double2hiint(q)) + m * d[1];
-  return __hiloint2double(int(hi), int(lo));
-}
-__device__ __forceinline__ double plcm_check_step_i(double x, const LaneConst& c,
-                                                    const CaseSel& cs, bool& ok,
-                                                    bool& suspect) {
-  const bool fold = x >= 0.5;
-  const double f = fold ? __dsub_rn(1.0, x) : x;  // exact when folded (Sterbenz)
-  const bool low = f < c.p;
-  uint32_t m = low ? 1u : 0u, nm = low ? 0u : 1u;
-  asm("" : "+r"(m), "+r"(nm));
-  const double sub = __hiloint2double(int(nm * uint32_t(__double2hiint(c.p))),
-                                      int(nm * uint32_t(__double2loint(c.p))));
-  const double num = __dsub_rn(f, sub);  // low: f - 0
-  const double yh = pick(m, c.yh_q, cs.yh);
-  const double yl = pick(m, c.yl_q, cs.yl);
-  const double den = pick(m, c.q, cs.den);
-  const double y = __fma_rn(num, yh, __dmul_rn(num, yl));
-  const unsigned hi = unsigned(__double2hiint(y));
-  const unsigned lo = unsigned(__double2loint(y));
-  const unsigned ex = hi & 0x7FF00000u;
+  // threshold den * ulp(y)/2 formed from den (p/2 and q/2 are exact halves):
+  // no hp/hq select, 96 registers, so five 128-thread CTAs fit an SM
+  // (57.7 -> 52.6 us per 144k-iteration C4 launch with the smaller CTAs)
+  const double den = low ? c.p : c.q;
   const double r = __fma_rn(-y, den, num);
   const double hulp = __hiloint2double(int(ex - (53u << 20)), 0);  // ulp(y) / 2
+  const double thr = __dmul_rn(den, hulp);
   suspect |= (lo == 0u) | (lo == c.plo) | (ex < (54u << 20));
-  ok &= fabs(r) < __dmul_rn(den, hulp);
+  ok &= fabs(r) < thr;
   return y;
 }
 
@@ -401,11 +352,14 @@ __global__ void __launch_bounds__(128, 1)
 #endif
 constexpr int kVerifyIlp = VERIFY_ILP;
 #ifndef VERIFY_MIN_BLOCKS
-#define VERIFY_MIN_BLOCKS 1
+#define VERIFY_MIN_BLOCKS 5
 #endif
 
+#ifndef VERIFY_THREADS
+#define VERIFY_THREADS 128  // 256: 57.7 us per 144k-iteration C4 launch, 128: 52.6, 96/32: 58-59 (spills)
+#endif
 template <bool DENSE>
-__global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
+__global__ void __launch_bounds__(VERIFY_THREADS, VERIFY_MIN_BLOCKS)
     k_prbg_verify_emit(const double* __restrict__ ckpt,
                        const double* __restrict__ verified_end,
                        const LaneConst* __restrict__ lcs,
@@ -425,9 +379,6 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
   const uint32_t l = uint32_t(me % nlanes);
   const uint32_t g0 = uint32_t(me / nlanes);
   const LaneConst c = lcs[l];
-#ifdef VERIFY_IMAD_SELECT
-  const CaseSel csel = make_case_sel(c);
-#endif
   const uint32_t odd = l & 1u;
   // kVerifyIlp groups per trip, regenerated interleaved: a group's 8 steps
   // are one dependent chain, so independent groups are the ILP
@@ -495,11 +446,7 @@ __global__ void __launch_bounds__(256, VERIFY_MIN_BLOCKS)
       for (int t = 0; t < 8; ++t)
 #pragma unroll
         for (int j = 0; j < kVerifyIlp; ++j)
-#ifdef VERIFY_IMAD_SELECT
-          y[j][t] = plcm_check_step_i(t ? y[j][t - 1] : x[j], c, csel, ok[j], suspect[j]);
-#else
           y[j][t] = VERIFY_STEP(t ? y[j][t - 1] : x[j], c, ok[j], suspect[j]);
-#endif
     }
 #pragma unroll
     for (int j = 0; j < kVerifyIlp; ++j) {
@@ -651,7 +598,7 @@ void launch_prbg_verify(const PrbgBuffers& b, int slot, const LaneConst* lc,
       1, std::min<uint64_t>(groups, (target + nlanes - 1) / nlanes)));
   const uint64_t threads = uint64_t(gs) * nlanes;
   auto vk = b.dense ? k_prbg_verify_emit<true> : k_prbg_verify_emit<false>;
-  vk<<<uint32_t((threads + 255) / 256), 256, 0, s>>>(
+  vk<<<uint32_t((threads + VERIFY_THREADS - 1) / VERIFY_THREADS), VERIFY_THREADS, 0, s>>>(
       b.ckpt[slot], b.verified_end, lc, b.orbit[slot], iters, nlanes, gs, ring, ring_bytes,
       it0, b.bad);
   k_prbg_fixup<<<(nw + 127) / 128, 128, 0, s>>>(b.orbit[slot], b.verified_end, lc,
