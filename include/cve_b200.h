@@ -261,6 +261,20 @@ typedef struct cve_sweep_options {
  * reference's CSV for the same key, image and seed. */
 CVE_B200_API cve_status cve_sweep_rounds(const cve_sweep_options* options, char** csv_out);
 
+/* Additive: the reference's Engine::transform (engine.cpp:302-307) as a frame
+ * call -- the transform behind cve_bench_phases and cve_sweep_rounds.  One
+ * frame in place through `rounds` rounds (1..255) with confusion and / or
+ * diffusion switched off (both on: the same bytes as
+ * cve_cipher_encrypt_frame with that many rounds).  Like a frame call it is
+ * the handle's next frame: it draws one confusion seed and, with diffusion on,
+ * rounds * side*side*3 / workers stream bytes per worker; MISMATCH comes
+ * after the seed draw.  states_out (optional, NULL to skip): rounds *
+ * side*side*3 bytes, the frame after each round.  Single-device handles. */
+CVE_B200_API cve_status cve_cipher_transform_frame(cve_cipher* cipher, uint8_t* pixels,
+                                                   uint32_t side, uint32_t rounds,
+                                                   int confusion, int diffusion,
+                                                   uint8_t* states_out);
+
 /* ---- additive: batched / device-resident / introspection ---------------- */
 
 /* Additive (row f4 on resident frames): the analysis reductions of a

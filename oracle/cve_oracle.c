@@ -413,6 +413,60 @@ static int orc_run_frame(orc_cipher* c, uint8_t* px, uint32_t side,
   return ORC_OK;
 }
 
+/* Engine::transform (src/engine.cpp:302-307 -> forward, 207-250): one seed,
+ * the streams only when diffusion is on (rounds * region bytes per worker),
+ * then per round the confusion half and / or the diffusion half.  states
+ * (optional): rounds * side*side*3 bytes, the frame after each round (the
+ * per_round callback, engine.cpp:247). */
+int orc_cipher_transform_frame(orc_cipher* c, uint8_t* px, uint32_t side, uint32_t rounds,
+                               int confusion, int diffusion, uint8_t* states) {
+  if (!c || !px || side == 0) return ORC_INVALID;
+  uint32_t seed = orc_cipher_next_seed(c);
+  if (side % c->n != 0) return ORC_MISMATCH;
+  const uint32_t n = c->n, w = side, rows = side / n;
+  const size_t region = (size_t)rows * w * 3, bytes = (size_t)w * w * 3;
+  uint8_t* ks = diffusion ? (uint8_t*)malloc((size_t)n * rounds * region + 1) : NULL;
+  uint8_t* a = (uint8_t*)malloc(bytes);
+  uint8_t* b = (uint8_t*)malloc(bytes);
+  int64_t* shift = (int64_t*)malloc(sizeof(int64_t) * w);
+  if (diffusion)
+    for (uint32_t i = 0; i < n; ++i)
+      orc_prbg_fill(&c->workers[i], ks + (size_t)i * rounds * region, rounds * region);
+  if (confusion)
+    for (uint32_t al = 0; al < w; ++al) shift[al] = orc_confusion_shift(al, w, seed);
+  memcpy(a, px, bytes);
+  for (uint32_t k = 0; k < rounds; ++k) {
+    if (confusion) { /* engine.cpp:32-47 */
+      for (uint32_t row = 0; row < w; ++row)
+        for (uint32_t o = 0; o < w; ++o) {
+          uint32_t al = (row + o) % w;
+          uint32_t be = orc_euclid((int64_t)o + shift[al], w);
+          memcpy(b + ((size_t)al * w + be) * 3, a + ((size_t)row * w + o) * 3, 3);
+        }
+      { uint8_t* t = a; a = b; b = t; }
+    }
+    if (diffusion) { /* engine.cpp:66-73, 231-246 */
+      for (uint32_t i = 0; i < n; ++i) {
+        const uint8_t* s = ks + (size_t)i * rounds * region + (size_t)k * region;
+        uint8_t prev = a[((size_t)((i + 1) % n) + 1) * region - 1];
+        for (size_t j = 0; j < region; ++j) {
+          uint8_t v = a[(size_t)i * region + j];
+          prev = (uint8_t)(s[j] ^ (uint8_t)(v + s[j]) ^ prev);
+          b[(size_t)i * region + j] = prev;
+        }
+      }
+      { uint8_t* t = a; a = b; b = t; }
+    }
+    if (states) memcpy(states + (size_t)k * bytes, a, bytes);
+  }
+  memcpy(px, a, bytes);
+  free(ks);
+  free(a);
+  free(b);
+  free(shift);
+  return ORC_OK;
+}
+
 int orc_cipher_encrypt_frame(orc_cipher* c, uint8_t* px, uint32_t side) {
   return orc_run_frame(c, px, side, 0);
 }

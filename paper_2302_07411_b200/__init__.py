@@ -132,6 +132,8 @@ def _load() -> C.CDLL:
         "cve_cipher_encrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
         "cve_cipher_decrypt_frame": (C.c_int, [vp, vp, C.c_uint32]),
         "cve_cipher_seeds_drawn": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "cve_cipher_transform_frame": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
+                                                 vp]),
         "cve_cipher_encrypt_frames": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32]),
         "cve_cipher_decrypt_frames": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32]),
         "cve_cipher_encrypt_frames_async": (C.c_int, [vp, vp, C.c_uint32, C.c_uint32, vp]),
@@ -467,6 +469,20 @@ class Cipher:
     def decrypt_frame(self, frame: np.ndarray) -> None:
         _, side = self._frames(frame)
         _check(lib.cve_cipher_decrypt_frame(self.handle, frame.ctypes.data, side))
+
+    def transform_frame(self, frame: np.ndarray, rounds: int, confusion: bool = True,
+                        diffusion: bool = True, states: bool = False):
+        """Reference Engine::transform as a frame call (the handle's next
+        frame), in place; states=True returns the (rounds, side, side, 3)
+        frames after each round."""
+        count, side = self._frames(frame[None] if frame.ndim == 3 else frame)
+        if count != 1:
+            raise CveError(CVE_ERROR_INVALID_ARGUMENT, "one frame at a time")
+        out = np.empty((rounds, side, side, 3), np.uint8) if states else None
+        _check(lib.cve_cipher_transform_frame(self.handle, frame.ctypes.data, side, rounds,
+                                              1 if confusion else 0, 1 if diffusion else 0,
+                                              out.ctypes.data if states else None))
+        return out
 
     def encrypt_frames(self, frames: np.ndarray) -> None:
         count, side = self._frames(frames)

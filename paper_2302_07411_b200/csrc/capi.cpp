@@ -8,6 +8,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <new>
 #include <string>
@@ -189,6 +190,24 @@ cve_status cve_cipher_encrypt_frame(cve_cipher* cipher, uint8_t* pixels,
 cve_status cve_cipher_decrypt_frame(cve_cipher* cipher, uint8_t* pixels,
                                     uint32_t side) {
   return run_frames(cipher, pixels, side, 1, true);
+}
+
+cve_status cve_cipher_transform_frame(cve_cipher* cipher, uint8_t* pixels, uint32_t side,
+                                      uint32_t rounds, int confusion, int diffusion,
+                                      uint8_t* states_out) {
+  return guarded([&] {
+    require(cipher != nullptr, "cipher is null");
+    require(pixels != nullptr, "pixels is null");
+    require(side != 0, "side must be >= 1");
+    require(rounds >= 1 && rounds <= 255, "rounds must be in 1..255");
+    DeviceScope scope(cipher->engine->device());
+    const size_t fb = size_t(side) * side * 3;
+    std::function<void(uint32_t, const uint8_t*)> keep;
+    if (states_out != nullptr)
+      keep = [&](uint32_t k, const uint8_t* s) { std::memcpy(states_out + (k - 1) * fb, s, fb); };
+    cipher->engine->transform_host(pixels, side, rounds, confusion != 0, diffusion != 0, keep,
+                                   nullptr);
+  });
 }
 
 cve_status cve_cipher_seeds_drawn(const cve_cipher* cipher, uint64_t* out) {

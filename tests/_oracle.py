@@ -44,6 +44,8 @@ class Oracle:
             L.orc_cipher_destroy.argtypes = [vp]
             L.orc_cipher_encrypt_frame.argtypes = [vp, vp, C.c_uint32]
             L.orc_cipher_decrypt_frame.argtypes = [vp, vp, C.c_uint32]
+            L.orc_cipher_transform_frame.argtypes = [vp, vp, C.c_uint32, C.c_uint32, C.c_int,
+                                                     C.c_int, vp]
             L.orc_cipher_worker_stream.argtypes = [vp, C.c_uint32, vp, C.c_size_t]
             L.orc_cipher_next_seed.argtypes = [vp]
             L.orc_cipher_next_seed.restype = C.c_uint32
@@ -80,6 +82,14 @@ class Oracle:
 
     def decrypt(self, frame: np.ndarray) -> int:
         return Oracle.lib.orc_cipher_decrypt_frame(self.h, _ptr(frame), frame.shape[0])
+
+    def transform(self, frame: np.ndarray, rounds: int, confusion: bool, diffusion: bool,
+                  states: np.ndarray = None) -> int:
+        """Reference Engine::transform (engine.cpp:302-307); states (optional,
+        (rounds, side, side, 3)) receives the frame after every round."""
+        return Oracle.lib.orc_cipher_transform_frame(
+            self.h, _ptr(frame), frame.shape[0], rounds, int(confusion), int(diffusion),
+            _ptr(states) if states is not None else None)
 
     def worker_stream(self, worker: int, n: int) -> np.ndarray:
         out = np.zeros(n, dtype=np.uint8)
