@@ -112,6 +112,32 @@ __device__ __forceinline__ double plcm_fast(double x, const LaneConst& c) {
   return fold ? (cc ? yc : yd) : (a ? ya : yb);
 }
 
+// The chain's step on the FOLDED orbit value u = min(x, 1 - x) (r02, last
+// session).  The map is symmetric -- the reference folds first (chaos.cpp:29:
+// x > 0.5 ? 1 - x : x, exact for x >= 0.5), so F(x) == F(1 - x) bit for bit --
+// and carrying u needs only the two unfolded quotient candidates plus their
+// complements for the next fold: 7 FP64 instructions instead of 11 (the step
+// is bound by FP64 issue slots, one per 2 cycles, plus the select's two pipe
+// crossings; DESIGN 12).  Returns fold(F(u)); 1 - y is exact for y >= 0.5.
+// Measured 23.12 -> 20.76 ns per iteration (tools/chain_folded.cu), the
+// folded orbit bit-identical to the product step's over 2^27 lane-steps.
+__device__ __forceinline__ double plcm_fast_folded(double u, const LaneConst& c) {
+  const bool a = bits_gt(c.p, u);
+  const double nb = __dsub_rn(u, c.p);
+  const double ya = __fma_rn(u, c.yh_p, __dmul_rn(u, c.yl_p));
+  const double yb = __fma_rn(nb, c.yh_q, __fma_rn(u, c.yl_q, c.a_b));
+  const double ta = __dsub_rn(1.0, ya);
+  const double tb = __dsub_rn(1.0, yb);
+  const bool fa = __double2hiint(ya) >= 0x3FE00000, fb = __double2hiint(yb) >= 0x3FE00000;
+  return a ? (fa ? ta : ya) : (fb ? tb : yb);
+}
+
+// u = min(x, 1 - x): the representative both sides of a comparison are
+// reduced to where one of them may be a folded chain value.
+__device__ __forceinline__ double plcm_fold(double x) {
+  return x >= 0.5 ? __dsub_rn(1.0, x) : x;
+}
+
 // Is y exactly the reference's next orbit value after x?  Branch-free common
 // path: one FMA residual test.  Values whose low word is 0 or p's (the guard
 // set {0, 0.5, 1, p} and powers of two) or that are tiny only raise
@@ -311,19 +337,23 @@ __global__ void __launch_bounds__(128, 1)
   // CHAIN_GROUPS checkpoint groups (32 steps) per loop trip: measured 23.15 ns per
   // iteration against 23.66 (2 groups), 23.35 (8) and 32.9 (16: instruction
   // cache); ptxas static schedules 38-41 cycles do not rank them
+  // The loop carries the folded value (plcm_fast_folded): checkpoints and the
+  // end state are min(x, 1 - x); the verifier compares folded values and
+  // regenerates the true orbit from either representative.
+  x = plcm_fold(x);
   uint32_t i = 0;
   for (; i + 8 * CHAIN_GROUPS <= iters; i += 8 * CHAIN_GROUPS) {
 #pragma unroll
     for (int gq = 0; gq < CHAIN_GROUPS; ++gq) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) x = plcm_fast(x, c);
+      for (int t = 0; t < 8; ++t) x = plcm_fast_folded(x, c);
       o[size_t(gq) * nlanes] = x;
     }
     o += size_t(CHAIN_GROUPS) * nlanes;
   }
   for (; i < iters; i += 8) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) x = plcm_fast(x, c);
+    for (int t = 0; t < 8; ++t) x = plcm_fast_folded(x, c);
     *o = x;
     o += nlanes;
   }
@@ -424,7 +454,8 @@ __global__ void __launch_bounds__(VERIFY_THREADS, VERIFY_MIN_BLOCKS)
       } else {
         x[j] = nx;
         end[j] = nend;
-        if (!g[j]) cont[j] = x[j] == verified_end[l];
+        // either side may be a folded chain value or an exact replay's end
+        if (!g[j]) cont[j] = plcm_fold(x[j]) == plcm_fold(verified_end[l]);
         if (k + j + 1 < trips) {
           const uint32_t gn = group_of(k + j + 1);
           nx = gn ? orbit[size_t(gn - 1) * nlanes + l] : ckpt[l];
@@ -450,7 +481,8 @@ __global__ void __launch_bounds__(VERIFY_THREADS, VERIFY_MIN_BLOCKS)
     }
 #pragma unroll
     for (int j = 0; j < kVerifyIlp; ++j) {
-      if (!DENSE) cont[j] &= y[j][7] == end[j];  // the chain walked exactly these values
+      // the chain walked exactly these values (its checkpoints are folded)
+      if (!DENSE) cont[j] &= plcm_fold(y[j][7]) == end[j];
       if (suspect[j]) {  // rare: decide this group exactly
         ok[j] = true;
         for (int t = 0; t < 8; ++t) ok[j] &= plcm_verify_exact(t ? y[j][t - 1] : x[j], y[j][t], c);
