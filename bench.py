@@ -926,12 +926,12 @@ def run_b200(args) -> None:
                                            "(the reference's call pattern)"}},
         "gpu_launches": launches,
         "roofline": {
-            "bound": "hbm", "kernel": "k_prbg_chain (dominant: %.0f%% of the step)"
+            "bound": "hbm", "kernel": "k_prbg_chain_walk (dominant: %.0f%% of the step)"
             % (100 * chain_ms / ms if ms else 0),
             "achieved": chain_gbs, "peak": hbm, "unit": "GB/s",
             "frac": chain_gbs / hbm if chain_gbs else None, "peak_source": hbm_src,
             "traffic": traffic_per_launch,
-            "traffic_note": "ncu dram__bytes_read+write of one k_prbg_chain launch (cold), per "
+            "traffic_note": "ncu dram__bytes_read+write of one k_prbg_chain_walk launch (cold), per "
                             "launch of this run; the chain writes one 8-byte checkpoint per lane "
                             "per 8 iterations (checkpoint_bytes_per_launch), which the verifier "
                             "reads back from L2",
@@ -943,13 +943,15 @@ def run_b200(args) -> None:
                     "HBM; the kernel is bound by the FP64 dependency latency of 2n "
                     "sequential orbits instead (see 'chain')"},
         "chain": {
-            "kernel": "k_prbg_chain (dominant: sequential FP64 orbit, latency-bound)",
+            "kernel": "k_prbg_chain_walk (dominant: sequential FP64 orbit, latency-bound)",
             "ns_per_iteration": ns_iter, "iterations_per_lane": iters_timed,
             "cycles_per_iteration": ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3,
-            # ptxas stall counts of the unrolled 32-iteration loop body (SASS
-            # control bits, tools/iter_cycles.py): 7 x 41 + 38 per 8 steps
-            "static_schedule_cycles": 40.6,
-            "frac_of_static_schedule": 40.6 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
+            # ptxas stall counts of the unrolled 32-iteration loop body of the
+            # folded step (SASS control bits, tools/iter_cycles.py build/csrc/prbg.o
+            # k_prbg_chain_walk DMUL): 38 per step (the unfolded step: 40.6)
+            "static_schedule_cycles": 38.0,
+            "frac_of_static_schedule": 38.0 / (ns_iter * (clk.summary()["sm_mhz"] or 1965.0) / 1e3),
+            "fp64_instructions_per_iteration": 7,
             "launches": int(len(chain_times)),
             "avg_launch_ms": float(np.mean(chain_times)) if len(chain_times) else None,
             "share_of_step": chain_ms / ms if ms else None,

@@ -928,7 +928,7 @@ void Engine::gen_until(uint64_t end_byte) {
     gen_.emit(slot, ring_, ring_bytes_, gen_iters_, uint32_t(chunk), s_work_);
     timed_end(s_work_);
     ck(cudaEventRecord(ver_done_[slot], s_work_), "cudaEventRecord");
-    st_.kernel_launches += gen_.kind() == MapKind::Plcm ? 3 : 2;
+    st_.kernel_launches += gen_.kernels_per_launch();
     ++st_.prbg_launches;
     ++launches_;
     gen_iters_ += chunk;

@@ -176,6 +176,11 @@ class Generator {
   void release(cudaStream_t after = nullptr) noexcept;
   MapKind kind() const { return kind_; }
   uint32_t bytes_per_iter() const { return kind_ == MapKind::Lasm ? 12 : 6; }
+  // kernels one chain() + emit() pair launches: PLCM chain (start + walk when
+  // checkpointed, one kernel when dense), verify/emit, fix-up; LASM chain, emit
+  uint32_t kernels_per_launch() const {
+    return kind_ == MapKind::Lasm ? 2u : (pb_.dense ? 3u : 4u);
+  }
   uint32_t max_iters() const { return kind_ == MapKind::Lasm ? lb_.max_iters : pb_.max_iters; }
   // Largest launch (iterations, multiple of 8) the orbit memory budget allows.
   uint32_t orbit_cap_iters() const;

@@ -289,19 +289,25 @@ __device__ __noinline__ double chain_resync(uint32_t l, const LaneConst& c,
   return x;
 }
 
+#ifndef CHAIN_GROUPS
+#define CHAIN_GROUPS 4
+#endif
 // (1) The chain.  One orbit per thread, 4 warps per CTA, one CTA per SM, so
-// every warp owns an SM sub-partition's in-order issue.  Per 8-iteration
-// group: 8 speculative iterations and ONE coalesced 8-byte store of the
-// group's last orbit value (a checkpoint).  plcm_fast is deterministic (IEEE
-// _rn intrinsics, integer compares, selects), so the verifier regenerates the
-// 7 values in between bit for bit from the previous checkpoint instead of
-// reading them: 1/8 of the stores on the chain and 1/8 of the orbit traffic.
-template <bool DENSE>
+// every warp owns an SM sub-partition's in-order issue.  Two forms:
+//   dense (many-clips handles): every orbit value stored, the verifier
+//     streams them from memory (k_prbg_chain_dense, the unfolded step);
+//   checkpointed (single clips, the fastest chain): per 8-iteration group 8
+//     speculative iterations and ONE coalesced 8-byte store of the group's
+//     last (folded) orbit value.  plcm_fast_folded is deterministic (IEEE _rn
+//     intrinsics, integer compares, selects); the verifier regenerates the
+//     true orbit exactly from the previous checkpoint and requires it to end
+//     on this one: 1/8 of the stores on the chain and of the orbit traffic.
 __global__ void __launch_bounds__(128, 1)
-    k_prbg_chain(double* __restrict__ state, double* __restrict__ ckpt,
-                 const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
-                 uint32_t iters, uint32_t nlanes, const double* __restrict__ verified_end,
-                 unsigned long long* __restrict__ resync, uint64_t launch, uint32_t prev_iters) {
+    k_prbg_chain_dense(double* __restrict__ state, double* __restrict__ ckpt,
+                       const LaneConst* __restrict__ lcs, double* __restrict__ orbit,
+                       uint32_t iters, uint32_t nlanes, const double* __restrict__ verified_end,
+                       unsigned long long* __restrict__ resync, uint64_t launch,
+                       uint32_t prev_iters) {
   const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= nlanes) return;
   const LaneConst c = lcs[l];
@@ -319,28 +325,51 @@ __global__ void __launch_bounds__(128, 1)
     x = chain_resync(l, c, verified_end, resync, launch - R == 2 ? prev_iters : 0u);
   ckpt[l] = x;
   double* o = orbit + l;
-  if (DENSE) {  // every orbit value stored: the verifier streams them from memory
-    for (uint32_t i = 0; i < iters; i += 8) {
+  for (uint32_t i = 0; i < iters; i += 8) {
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        x = plcm_fast(x, c);
-        o[size_t(t) * nlanes] = x;
-      }
-      o += size_t(8) * nlanes;
+    for (int t = 0; t < 8; ++t) {
+      x = plcm_fast(x, c);
+      o[size_t(t) * nlanes] = x;
     }
-    state[l] = x;
-    return;
+    o += size_t(8) * nlanes;
   }
-#ifndef CHAIN_GROUPS
-#define CHAIN_GROUPS 4
-#endif
-  // CHAIN_GROUPS checkpoint groups (32 steps) per loop trip: measured 23.15 ns per
-  // iteration against 23.66 (2 groups), 23.35 (8) and 32.9 (16: instruction
-  // cache); ptxas static schedules 38-41 cycles do not rank them
-  // The loop carries the folded value (plcm_fast_folded): checkpoints and the
-  // end state are min(x, 1 - x); the verifier compares folded values and
-  // regenerates the true orbit from either representative.
-  x = plcm_fold(x);
+  state[l] = x;
+}
+
+// Checkpointed generator as two kernels (r02, last session): the launch's
+// start-up -- resynchronisation, the start checkpoint, folding the state --
+// in a tiny kernel of its own, so that the chain kernel is nothing but the
+// loop.  With the start-up code in the same kernel ptxas left a register move
+// behind every step's select (on the dependency chain); alone, the loop gets
+// the stand-alone probe's code (tools/chain_folded.cu).
+__global__ void __launch_bounds__(128)
+    k_prbg_chain_start(double* __restrict__ state, double* __restrict__ ckpt,
+                       const LaneConst* __restrict__ lcs, uint32_t nlanes,
+                       const double* __restrict__ verified_end,
+                       unsigned long long* __restrict__ resync, uint64_t launch,
+                       uint32_t prev_iters) {
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlanes) return;
+  double x = state[l];
+  unsigned long long R;  // see k_prbg_chain_dense
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(R) : "l"(resync + l) : "memory");
+  if (R != ~0ull && R < launch && launch - R <= 2)
+    x = chain_resync(l, lcs[l], verified_end, resync, launch - R == 2 ? prev_iters : 0u);
+  ckpt[l] = x;
+  state[l] = plcm_fold(x);
+}
+
+__global__ void __launch_bounds__(128, 1)
+    k_prbg_chain_walk(double* __restrict__ state, const LaneConst* __restrict__ lcs,
+                      double* __restrict__ orbit, uint32_t iters, uint32_t nlanes) {
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlanes) return;
+  const LaneConst c = lcs[l];
+  double x = state[l];  // folded by k_prbg_chain_start
+  double* o = orbit + l;
+  // CHAIN_GROUPS checkpoint groups (32 steps) per loop trip: measured (unfolded
+  // step) 23.15 ns per iteration against 23.66 (2 groups), 23.35 (8) and 32.9
+  // (16: instruction cache); folded step 21.53 / 21.97 (2) / 21.52 (8)
   uint32_t i = 0;
   for (; i + 8 * CHAIN_GROUPS <= iters; i += 8 * CHAIN_GROUPS) {
 #pragma unroll
@@ -596,8 +625,10 @@ int chain_reserve() {
 }
 
 void configure_prbg_kernels() {
-  for (auto k : {k_prbg_chain<false>, k_prbg_chain<true>})
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, chain_reserve());
+  cudaFuncSetAttribute(k_prbg_chain_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       chain_reserve());
+  cudaFuncSetAttribute(k_prbg_chain_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       chain_reserve());
 }
 
 void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
@@ -605,8 +636,14 @@ void launch_prbg_chain(const PrbgBuffers& b, int slot, const LaneConst* lc,
                        cudaStream_t s) {
   // 128 threads/CTA, one CTA per SM; the dynamic shared memory request only
   // enforces SM exclusivity (chain_reserve).
-  auto kern = b.dense ? k_prbg_chain<true> : k_prbg_chain<false>;
-  kern<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
+  if (!b.dense) {
+    k_prbg_chain_start<<<(nlanes + 127) / 128, 128, 0, s>>>(
+        b.state, b.ckpt[slot], lc, nlanes, b.verified_end, b.resync, launch, prev_iters);
+    k_prbg_chain_walk<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
+        b.state, lc, b.orbit[slot], iters, nlanes);
+    return;
+  }
+  k_prbg_chain_dense<<<(nlanes + 127) / 128, 128, chain_reserve(), s>>>(
       b.state, b.ckpt[slot], lc, b.orbit[slot], iters, nlanes, b.verified_end, b.resync, launch,
       prev_iters);
 }

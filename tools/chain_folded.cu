@@ -51,10 +51,30 @@ __device__ __forceinline__ double step_folded(double u, const LaneConst& c) {
     const double other = a ? wa : yb;
     return (!a && fb) ? tb : other;
   }
-  // V == 2: select y first, then complement of the selected
-  const double y = a ? ya : yb;
-  const double t = a ? ta : tb;
-  return __double2hiint(y) >= 0x3FE00000 ? t : y;
+  if (V == 2) {  // select y first, then complement of the selected
+    const double y = a ? ya : yb;
+    const double t = a ? ta : tb;
+    return __double2hiint(y) >= 0x3FE00000 ? t : y;
+  }
+  if (V == 3) {  // four predicated assignments
+    const bool pa1 = a & fa, pa0 = a & !fa, pb1 = (!a) & fb;
+    double r = yb;
+    if (pb1) r = tb;
+    if (pa0) r = ya;
+    if (pa1) r = ta;
+    return r;
+  }
+  if (V == 4) {  // 64-bit integer selects
+    const long long ia = fa ? __double_as_longlong(ta) : __double_as_longlong(ya);
+    const long long ib = fb ? __double_as_longlong(tb) : __double_as_longlong(yb);
+    return __longlong_as_double(a ? ia : ib);
+  }
+  // V == 5: halves selected separately and re-paired
+  const int lo = a ? (fa ? __double2loint(ta) : __double2loint(ya))
+                   : (fb ? __double2loint(tb) : __double2loint(yb));
+  const int hi = a ? (fa ? __double2hiint(ta) : __double2hiint(ya))
+                   : (fb ? __double2hiint(tb) : __double2hiint(yb));
+  return __hiloint2double(hi, lo);
 }
 
 template <int V>
@@ -114,11 +134,13 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  void (*ks[])(double*, const LaneConst*, double*, uint32_t, uint32_t) = {k<0>, k<1>, k<2>, k<3>};
+  void (*ks[])(double*, const LaneConst*, double*, uint32_t, uint32_t) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>};
   const char* names[] = {"product step (11 FP64)", "folded, nested selects (7 FP64)",
-                         "folded, tb selected last", "folded, select then fold"};
+                         "folded, tb selected last", "folded, select then fold",
+                         "folded, predicated assigns", "folded, 64-bit int selects",
+                         "folded, halves re-paired"};
   std::vector<double> ref(nck), got(nck);
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < 7; ++m) {
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemcpy(dx, x0.data(), T * 8, cudaMemcpyHostToDevice);
