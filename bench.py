@@ -891,7 +891,7 @@ def run_b200(args) -> None:
     try:  # DRAM bytes per launch from the committed ncu --set full captures
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
-        ch = tr["k_prbg_chain"]
+        ch = tr.get("k_prbg_chain_walk") or tr["k_prbg_chain"]
         traffic_per_launch = ch["dram_bytes"] / ch["iterations"] * launch_iters
         ckpt_per_launch = ch["checkpoint_bytes_written"] / ch["iterations"] * launch_iters
         # per-frame device DRAM traffic, cold-cache upper bound: the sum of

@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KERNELS = ["k_prbg_chain", "k_prbg_verify_emit", "k_encrypt_round_rows", "k_decrypt_round_rows",
+KERNELS = ["k_prbg_chain_walk", "k_prbg_chain_start", "k_prbg_chain_dense", "k_prbg_verify_emit", "k_encrypt_round_rows", "k_decrypt_round_rows",
            "k_encrypt_round_slots",
            "k_decrypt_round_tiles", "k_encrypt_frame_cluster", "k_lasm_chain"]
 
@@ -47,10 +47,10 @@ def main(tag):
             ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", i).split()[0] for i in ins if i)
             lines.append(f"== {k}  ({name})  {len(ins)} instructions")
             lines.append("   " + ", ".join(f"{op} {c}" for op, c in ops.most_common()))
-            if k == "k_prbg_chain<checkpointed>":
+            if k == "k_prbg_chain_walk":
                 # the main loop: 32 unrolled iterations (4 checkpoint stores),
                 # from its first DADD to its backward branch
-                start = next(i for i, s in enumerate(ins) if s.startswith("DADD"))
+                start = next(i for i, s in enumerate(ins) if s.startswith(("DADD", "DMUL")))
                 end = next(i for i in range(start, len(ins)) if "BRA" in ins[i])
                 lines.append("   main loop body (32 iterations, 4 checkpoint stores):")
                 lines.extend("     " + s for s in ins[start:end + 1])

@@ -41,9 +41,9 @@ for p in sys.argv[1:]:
                "grid": r["launch__grid_size"][0], "block": r["launch__block_size"][0]}
         out.setdefault(name, rec)  # first launch of each kernel
 # the generator launches of tools/ncu_capture.py: one C4 launch of 131072
-# iterations x 128 lanes (k_prbg_chain writes one 8-byte checkpoint per lane
+# iterations x 128 lanes (k_prbg_chain_walk writes one 8-byte checkpoint per lane
 # per 8 iterations: 2.1 MB, consumed from L2 by k_prbg_verify_emit)
-for k in ("k_prbg_chain", "k_prbg_verify_emit"):
+for k in ("k_prbg_chain", "k_prbg_chain_walk", "k_prbg_verify_emit"):
     if k in out:
         out[k].update({"iterations": 131072, "lanes": 128,
                        "checkpoint_bytes_written": 131072 // 8 * 128 * 8})
