@@ -1,5 +1,5 @@
 """Short, fixed-size workload for ncu --set full captures: one C4 generator
-launch of exactly 131072 iterations (k_prbg_chain + k_prbg_verify_emit), then
+launch of exactly 131072 iterations (k_prbg_chain_start + k_prbg_chain_walk + k_prbg_verify_emit), then
 one C4 frame encrypted and decrypted (k_encrypt_round / k_decrypt_round)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
