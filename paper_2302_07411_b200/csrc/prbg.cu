@@ -294,8 +294,8 @@ __device__ __noinline__ double chain_resync(uint32_t l, const LaneConst& c,
 #endif
 // (1) The chain.  One orbit per thread, 4 warps per CTA, one CTA per SM, so
 // every warp owns an SM sub-partition's in-order issue.  Two forms:
-//   dense (many-clips handles): every orbit value stored, the verifier
-//     streams them from memory (k_prbg_chain_dense, the unfolded step);
+//   dense (many-clips handles): every true orbit value stored, the verifier
+//     streams them from memory (k_prbg_chain_dense; the same folded step);
 //   checkpointed (single clips, the fastest chain): per 8-iteration group 8
 //     speculative iterations and ONE coalesced 8-byte store of the group's
 //     last (folded) orbit value.  plcm_fast_folded is deterministic (IEEE _rn
@@ -325,10 +325,22 @@ __global__ void __launch_bounds__(128, 1)
     x = chain_resync(l, c, verified_end, resync, launch - R == 2 ? prev_iters : 0u);
   ckpt[l] = x;
   double* o = orbit + l;
+  // the folded step (plcm_fast_folded), storing the TRUE orbit value of each
+  // step -- the selected quotient before its fold -- for the streaming
+  // verifier; the end state is the last true value
+  double u = plcm_fold(x);
   for (uint32_t i = 0; i < iters; i += 8) {
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      x = plcm_fast(x, c);
+      const bool a = bits_gt(c.p, u);
+      const double nb = __dsub_rn(u, c.p);
+      const double ya = __fma_rn(u, c.yh_p, __dmul_rn(u, c.yl_p));
+      const double yb = __fma_rn(nb, c.yh_q, __fma_rn(u, c.yl_q, c.a_b));
+      const double ta = __dsub_rn(1.0, ya);
+      const double tb = __dsub_rn(1.0, yb);
+      const bool fa = __double2hiint(ya) >= 0x3FE00000, fb = __double2hiint(yb) >= 0x3FE00000;
+      u = a ? (fa ? ta : ya) : (fb ? tb : yb);
+      x = a ? ya : yb;
       o[size_t(t) * nlanes] = x;
     }
     o += size_t(8) * nlanes;
